@@ -1,0 +1,205 @@
+/* bnff.h -- C ABI of libbnff: the B200 (sm_100a) kernels of the restructured
+ * batch-norm training path (BN fission-n-fusion, arXiv 1807.01702).
+ *
+ * Every entry point replaces one reference function of the Python/numpy
+ * package `bnfuse` (paths relative to /root/reference/pkg/src/bnfuse/); the
+ * Python mirror (paper_1807_01702_b200/kernels.py) binds them with ctypes and
+ * keeps the reference names and argument meaning.
+ *
+ * Conventions
+ *  - Feature maps are NHWC views: `ptr` points at (n=0,h=0,w=0,c=channel offset)
+ *    and consecutive pixels are `row_stride` ELEMENTS apart, so a channel-offset
+ *    slice of a DenseNet block buffer is just (base + offset, row_stride = C_total).
+ *  - dtype BNFF_BF16: bf16 storage, bf16 tcgen05 MMA (kind::f16), fp32 accumulate.
+ *    dtype BNFF_F32 : fp32 storage, 3xTF32 split tcgen05 MMA (kind::tf32, ~fp32).
+ *  - Channel counts and channel offsets must be multiples of 8 (bf16) / 4 (f32).
+ *  - Per-channel statistics are float64; per-tile partials are float32 and are
+ *    combined in a fixed order (bitwise run-to-run deterministic, no atomics).
+ *  - No allocation, no host synchronisation; all work is ordered on `stream`
+ *    (a cudaStream_t, NULL = legacy default stream).
+ *  - Return: 0 ok, 1 shape (ShapeError), 2 state (StateError), 3 unsupported,
+ *    4 CUDA error; bnff_last_error() gives the message.
+ */
+#ifndef BNFF_H_
+#define BNFF_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { BNFF_OK = 0, BNFF_ERR_SHAPE = 1, BNFF_ERR_STATE = 2, BNFF_ERR_UNSUPPORTED = 3,
+       BNFF_ERR_CUDA = 4 };
+enum { BNFF_F32 = 0, BNFF_BF16 = 1 };
+
+/* operand transforms applied while a conv kernel reads a feature map */
+enum {
+  BNFF_PRO_NONE = 0,
+  BNFF_PRO_RELU = 1,         /* max(x,0): RCF clip-on-read (execute.py:170, fusion.py:127-148) */
+  BNFF_PRO_BN_RELU = 2,      /* max((x-mean)*scale+beta,0): sub-BN2 + ReLU (fused.py:133-135) */
+  BNFF_PRO_BN_DX = 3,        /* g*(dt1-k1-xhat*k2): deferred sub-BN1' dx (ops.py:283-298) */
+};
+/* dgrad epilogues */
+enum {
+  BNFF_DG_PLAIN = 0,         /* dx (ops.py:193-202) */
+  BNFF_DG_CLIP = 1,          /* dx where x>0 (execute.py:331-332) */
+  BNFF_DG_NRC = 2,           /* dt1 = dx where relu(bn(x))>0, + sum dt1, sum dt1*xhat (fused.py:176-188) */
+};
+
+typedef struct {
+  void* ptr;
+  int64_t n, h, w, c;
+  int64_t row_stride; /* elements between consecutive pixels */
+} bnff_view;
+
+/* Per-channel coefficient table consumed by the operand prologues:
+ *   BNFF_PRO_BN_RELU: a = mean, b = scale (=gamma*invstd), c = beta
+ *   BNFF_PRO_BN_DX  : a = mean, b = invstd, c = k1 (=dbeta/m), d = k2 (=dgamma/m), e = g (=gamma*invstd)
+ * each array holds `c` floats (channels of the transformed tensor).            */
+typedef struct {
+  const float* a;
+  const float* b;
+  const float* c;
+  const float* d;
+  const float* e;
+} bnff_coef;
+
+typedef struct {
+  int32_t dtype;
+  int32_t kh, kw, stride, pad;
+  bnff_view x;        /* conv input  (n, h, w, c_in)  */
+  bnff_view y;        /* conv output (n, oh, ow, c_out) */
+  const void* wpack;  /* packed weights [c_out][kh*kw*c_in (padded)] (bnff_pack_weights) */
+  const float* bias;  /* c_out, nullable */
+  int32_t x_pro;      /* BNFF_PRO_NONE / RELU / BN_RELU */
+  bnff_coef x_coef;
+  float* stat_part;   /* nullable: sum/sumsq partials [m_tiles][2][c_out] of the stored y */
+} bnff_fprop_args;
+
+typedef struct {
+  int32_t dtype;
+  int32_t kh, kw, stride, pad;
+  bnff_view dy;       /* grad wrt conv output (or dt1 of a deferred package) */
+  bnff_view dy_x;     /* BNFF_PRO_BN_DX: the package's normalized-input tensor (conv output) */
+  int32_t dy_pro;     /* BNFF_PRO_NONE / BN_DX */
+  bnff_coef dy_coef;
+  bnff_view dx;       /* output: grad wrt conv input (n, h, w, c_in) */
+  bnff_view x;        /* conv input (for CLIP / NRC epilogues) */
+  const void* wpack_t;/* packed transposed weights [c_in][kh*kw*c_out (padded)] */
+  int32_t epi;        /* BNFF_DG_* */
+  bnff_coef x_coef;   /* NRC: a = mean, b = scale, c = beta, d = invstd */
+  float* stat_part;   /* NRC: partials [m_tiles][2][c_in] of (sum dt1, sum dt1*xhat) */
+} bnff_dgrad_args;
+
+typedef struct {
+  int32_t dtype;
+  int32_t kh, kw, stride, pad;
+  bnff_view x;        /* conv input (n, h, w, c_in) */
+  int32_t x_pro;      /* NONE / RELU / BN_RELU (recompute of the saved post-ReLU input) */
+  bnff_coef x_coef;
+  bnff_view dy;       /* (n, oh, ow, c_out) */
+  bnff_view dy_x;
+  int32_t dy_pro;     /* NONE / BN_DX */
+  bnff_coef dy_coef;
+  int32_t splits;     /* split-K factor (0 = choose); see bnff_wgrad_workspace */
+  float* workspace;   /* splits * (kh*kw*c_in) * c_out floats */
+  float* dw;          /* output (c_out, dw_cin, kh, kw) fp32, reference layout */
+  int32_t dw_cin;     /* real input channels (<= x.c when the input is channel-padded); 0 = x.c */
+  float* dbias;       /* nullable, c_out fp32: sum of (transformed) dy */
+} bnff_wgrad_args;
+
+const char* bnff_last_error(void);
+int bnff_version(void);
+int bnff_device_ok(void); /* 1 if device 0 is sm_100 */
+
+/* K1: conv2d_fwd (ops.py:151-175), fused_conv_stats_fwd (fused.py:79-100),
+ *     fused_norm_relu_conv_fwd (fused.py:103-154), RCF clipped conv (execute.py:167-179) */
+int bnff_conv_fprop(const bnff_fprop_args* a, void* stream);
+/* K2: conv2d_bwd dx (ops.py:193-202), fused_nrc_bwd gradient pass (fused.py:176-188),
+ *     fused_conv_stats_bwd dx (fused.py:203-219) */
+int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream);
+/* K3: conv2d_bwd dw/dbias (ops.py:195-203), fused_nrc_bwd weight pass (fused.py:190-199) */
+int64_t bnff_wgrad_workspace(int32_t n, int32_t oh, int32_t ow, int32_t kh, int32_t kw,
+                             int32_t c_in, int32_t c_out, int32_t splits);
+int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream);
+int32_t bnff_wgrad_default_splits(int32_t n, int32_t oh, int32_t ow, int32_t kh, int32_t kw,
+                                  int32_t c_in, int32_t c_out);
+
+/* weight re-layout (once per optimizer step): w (c_out, c_in, kh, kw) fp32 ->
+ * forward pack [c_out][tap][c_in] and transposed pack [c_in][tap][c_out] in dtype,
+ * K padded to a multiple of 64 (bf16) / 32 (f32) with zeros. c_in_store >= c_in pads
+ * input channels with zeros (e.g. the 3-channel image stem).                     */
+int64_t bnff_pack_size(int32_t dtype, int32_t c_out, int32_t c_in_store, int32_t kh, int32_t kw);
+int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, int32_t c_in,
+                      int32_t c_in_store, int32_t kh, int32_t kw, void* wpack, void* wpack_t,
+                      void* stream);
+
+/* K5: channel sums over an NHWC view -> partials [tiles][2][c]:
+ *   mode 0: (x, x^2)                         -- bn_stats_onepass (ops.py:231-237)
+ *   mode 1: (dy, dy*xhat), xhat from x,coef(a=mean,b=invstd); optional relu mask
+ *           from coef (mask_x>0 via c=... see kernels)  -- bn_bwd pass 1 (ops.py:271-274),
+ *           FissionSubBN2 bwd (execute.py:381-399)
+ *   mode 2: (dy, 0)                          -- conv dbias (ops.py:203)                */
+int32_t bnff_sum_tiles(int64_t pixels);
+int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_view dy, bnff_coef coef,
+                      float* part, void* stream);
+/* K4: partials -> float64 (sum, sumsq) and (mean, var) per channel plus the fp32
+ * prologue table (mean32, scale32 = gamma*invstd, beta32, invstd32)
+ * (ChannelStats.from_sums / inv_std, ops.py:109-116).  Writes sums at channel
+ * offset `c_off` of the f64 arrays so per-piece stats assemble in place
+ * (concat_stats, ops.py:128-143).                                               */
+int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count,
+                        double* sum, double* sumsq, double* mean, double* var, void* stream);
+/* two-pass centred variance for the unfused BN (ops.py:212-228): var from x and mean */
+int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, float* part,
+                      void* stream);
+int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+                      void* stream);
+int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
+                   const float* beta, float eps, float* mean32, float* scale32, float* beta32,
+                   float* inv32, void* stream);
+/* backward coefficient table from the reduced (dgamma, dbeta) sums:
+ * k1 = dbeta/m, k2 = dgamma/m, g = gamma*invstd (ops.py:287-293). Also writes
+ * the fp32 parameter gradients dgamma32/dbeta32 (nullable). */
+int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count,
+                   const double* mean, const double* var, const float* gamma, float eps,
+                   double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
+                   float* mean32, float* inv32, float* dgamma32, float* dbeta32, void* stream);
+
+/* K6: y = (x-mean)*scale+beta [relu]  (bn_fwd ops.py:240-254, FissionSubBN2 execute.py:211-217) */
+int bnff_bn_apply(int32_t dtype, bnff_view x, bnff_view y, bnff_coef coef, int32_t relu,
+                  void* stream);
+/* K7/K8: out = [acc +] sum_i resolve(in_i) where resolve is identity or the deferred
+ * BN dx transform g*(dt1 - k1 - xhat*k2) with xhat from x_i (bn_dx_from_sums
+ * ops.py:283-298, DeferredBNGrad.materialize execute.py:123-126, split_bwd
+ * ops.py:398-408, fused_split_bwd_bn_dx fused.py:222-230).  Up to 2 inputs.      */
+typedef struct {
+  bnff_view g;     /* plain gradient or dt1 */
+  bnff_view x;     /* deferred: the normalized-input tensor */
+  int32_t deferred;
+  bnff_coef coef;  /* a=mean b=invstd c=k1 d=k2 e=g */
+} bnff_grad_term;
+int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, const bnff_grad_term* terms,
+                  int32_t nterms, void* stream);
+/* ReLU (ops.py:306-319) */
+int bnff_relu_fwd(int32_t dtype, bnff_view x, bnff_view y, void* stream);
+int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view dx, void* stream);
+/* K9: avgpool k x k non-overlapping (ops.py:428-454); optional fused stats partials */
+int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, float* stat_part,
+                     void* stream);
+int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void* stream);
+/* K10: y = a + zero-channel-padded b (execute.py:266-280) */
+int bnff_ews_fwd(int32_t dtype, bnff_view a, bnff_view b, bnff_view y, void* stream);
+/* K11: copy a view into another (physical concat piece / gradient slice copy) */
+int bnff_copy(int32_t dtype, bnff_view src, bnff_view dst, void* stream);
+/* boundary layout conversions, NCHW fp32 host-format <-> NHWC dtype (channel-padded) */
+int bnff_nchw_to_nhwc(int32_t dtype, const float* src, int64_t n, int64_t c, int64_t h,
+                      int64_t w, bnff_view dst, void* stream);
+int bnff_nhwc_to_nchw(int32_t dtype, bnff_view src, float* dst, void* stream);
+/* K12: multi-tensor SGD w -= lr*g over a flat fp32 buffer */
+int bnff_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNFF_H_ */

@@ -1,0 +1,783 @@
+// channel.cu -- HBM-bound kernels of the restructured-BN path (sm_100a).
+//
+// Everything here streams NHWC views with 128-bit loads/stores (8 bf16 / 4 f32
+// per access, consecutive threads on consecutive channel chunks of a pixel) and
+// reduces per-channel quantities deterministically: per-tile partials written
+// to a [tiles][2][C] buffer, then combined in a fixed order in float64.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "sm100.cuh"
+#include "common.cuh"
+
+namespace bnff {
+
+static thread_local char g_err[512] = "";
+char* last_error_buf() { return g_err; }
+
+// ---------------------------------------------------------------------------
+// vector access helpers
+// ---------------------------------------------------------------------------
+template <typename T> struct VecIO;
+template <> struct VecIO<__nv_bfloat16> {
+  static constexpr int V = 8;
+  __device__ static __forceinline__ void load(const void* base, long long off, float (&f)[8]) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + off));
+    f[0] = bf16lo(r.x); f[1] = bf16hi(r.x); f[2] = bf16lo(r.y); f[3] = bf16hi(r.y);
+    f[4] = bf16lo(r.z); f[5] = bf16hi(r.z); f[6] = bf16lo(r.w); f[7] = bf16hi(r.w);
+  }
+  __device__ static __forceinline__ void store(void* base, long long off, const float (&f)[8]) {
+    uint4 o;
+    o.x = pack_bf16(f[0], f[1]); o.y = pack_bf16(f[2], f[3]);
+    o.z = pack_bf16(f[4], f[5]); o.w = pack_bf16(f[6], f[7]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + off) = o;
+  }
+  __device__ static __forceinline__ float round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+};
+template <> struct VecIO<float> {
+  static constexpr int V = 4;
+  __device__ static __forceinline__ void load(const void* base, long long off, float (&f)[4]) {
+    const float4 r = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off));
+    f[0] = r.x; f[1] = r.y; f[2] = r.z; f[3] = r.w;
+  }
+  __device__ static __forceinline__ void store(void* base, long long off, const float (&f)[4]) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+  __device__ static __forceinline__ float round(float v) { return v; }
+};
+
+struct View {
+  const void* p;
+  long long rs;
+};
+
+__device__ __forceinline__ float bn_dx_elem(float dt, float x, int c, const bnff_coef& cf) {
+  const float xh = __fmul_rn(__fsub_rn(x, __ldg(cf.a + c)), __ldg(cf.b + c));
+  const float t = __fsub_rn(__fsub_rn(dt, __ldg(cf.c + c)), __fmul_rn(xh, __ldg(cf.d + c)));
+  return __fmul_rn(__ldg(cf.e + c), t);
+}
+
+// ---------------------------------------------------------------------------
+// K5: channel sums -> partials [tiles][2][C]
+// ---------------------------------------------------------------------------
+constexpr int kSumThreads = 256;
+constexpr int kMaxTiles = 1184;  // 8 x 148
+
+__host__ __device__ inline int sum_tiles(long long pixels) {
+  long long t = (pixels + 31) / 32;
+  return (int)(t < kMaxTiles ? (t < 1 ? 1 : t) : kMaxTiles);
+}
+
+// mode 0: (x, x^2); mode 1: (dy, dy*xhat) xhat=(x-a)*b; mode 2: (dy', 0) with dy'
+// = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double)
+template <typename T>
+__global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
+                                    bnff_coef cf, const double* mean64, float* part) {
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[2][kSumThreads][V];
+  const int cpr = C / V;
+  const int tiles = gridDim.x;
+  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
+  const long long r_begin = blockIdx.x * rows_per_tile;
+  const long long r_end = min(pixels, r_begin + rows_per_tile);
+  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, cpr - cbase);
+    const int rows_per_iter = kSumThreads / ccount;
+    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
+    const bool active = trow < rows_per_iter;
+    const int c0 = (cbase + tcol) * V;
+    float s1[V], s2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    if (active) {
+      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+        float v[V], x[V];
+        if (mode == 0 || mode == 3) {
+          VecIO<T>::load(xv.p, r * xv.rs + c0, v);
+        } else {
+          VecIO<T>::load(dyv.p, r * dyv.rs + c0, v);
+          if (mode == 1 || cf.e != nullptr) VecIO<T>::load(xv.p, r * xv.rs + c0, x);
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          if (mode == 0) {
+            s1[i] += v[i];
+            s2[i] += v[i] * v[i];
+          } else if (mode == 1) {
+            const float xh = __fmul_rn(__fsub_rn(x[i], __ldg(cf.a + c0 + i)), __ldg(cf.b + c0 + i));
+            s1[i] += v[i];
+            s2[i] += v[i] * xh;
+          } else if (mode == 2) {
+            s1[i] += cf.e != nullptr ? bn_dx_elem(v[i], x[i], c0 + i, cf) : v[i];
+          } else {
+            const float d = (float)((double)v[i] - mean64[c0 + i]);
+            s1[i] += d * d;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sh[0][threadIdx.x][i] = s1[i];
+      sh[1][threadIdx.x][i] = s2[i];
+    }
+    __syncthreads();
+    // fixed-order combine of the rows_per_iter threads sharing a column
+    if (threadIdx.x < ccount) {
+      float a[V], b[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int rr = 0; rr < rows_per_iter; ++rr) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          a[i] += sh[0][rr * ccount + threadIdx.x][i];
+          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+        }
+      }
+      const int cc = (cbase + threadIdx.x) * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// partials -> float64 totals: 256 threads per 32 channels, fixed order
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, int C, int slot,
+                                    double* __restrict__ out) {
+  __shared__ double sh[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  double acc = 0.0;
+  if (c < C)
+    for (int t = ty; t < tiles; t += 8) acc += (double)part[((long long)t * 2 + slot) * C + c];
+  sh[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < C) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += sh[k][tx];
+    out[c] = s;
+  }
+}
+
+__global__ void stats_from_sums_kernel(int C, long long count, const double* sum, const double* sumsq,
+                                       double* mean, double* var) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double m = sum[c] / (double)count;
+  mean[c] = m;
+  const double v = sumsq[c] / (double)count - m * m;
+  var[c] = v > 0.0 ? v : 0.0;
+}
+
+__global__ void bn_coeffs_kernel(int C, const double* mean, const double* var, const float* gamma,
+                                 const float* beta, float eps, float* mean32, float* scale32,
+                                 float* beta32, float* inv32) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double v = var[c] > 0.0 ? var[c] : 0.0;
+  const double inv = 1.0 / sqrt(v + (double)eps);
+  mean32[c] = (float)mean[c];
+  if (scale32) scale32[c] = (float)((double)gamma[c] * inv);
+  if (beta32) beta32[c] = beta[c];
+  if (inv32) inv32[c] = (float)inv;
+}
+
+__global__ void dx_coeffs_kernel(int C, long long count, const double* dsum, const double* dsum2,
+                                 const double* mean, const double* var, const float* gamma,
+                                 float eps, float* k1, float* k2, float* g, float* mean32,
+                                 float* inv32, float* dgamma32, float* dbeta32) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double v = var[c] > 0.0 ? var[c] : 0.0;
+  const double inv = 1.0 / sqrt(v + (double)eps);
+  const double dbeta = dsum[c], dgamma = dsum2[c];
+  k1[c] = (float)(dbeta / (double)count);
+  k2[c] = (float)(dgamma / (double)count);
+  g[c] = (float)((double)gamma[c] * inv);
+  mean32[c] = (float)mean[c];
+  inv32[c] = (float)inv;
+  if (dgamma32) dgamma32[c] = (float)dgamma;
+  if (dbeta32) dbeta32[c] = (float)dbeta;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise families (grid-stride over pixels x chunks)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void bn_apply_kernel(View x, View y, long long pixels, int C, bnff_coef cf, int relu) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = pixels * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    float f[V];
+    VecIO<T>::load(x.p, r * x.rs + c0, f);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float t = __fmul_rn(__fsub_rn(f[k], __ldg(cf.a + c0 + k)), __ldg(cf.b + c0 + k));
+      t = __fadd_rn(t, __ldg(cf.c + c0 + k));
+      f[k] = relu ? fmaxf(t, 0.f) : t;
+    }
+    VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, f);
+  }
+}
+
+struct TermDev {
+  View g, x;
+  int deferred;
+  bnff_coef cf;
+};
+
+template <typename T>
+__global__ void grad_sum_kernel(View out, long long pixels, int C, int accumulate, TermDev t0,
+                                TermDev t1, int nterms) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = pixels * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    float acc[V], v[V], xv[V];
+    VecIO<T>::load(t0.g.p, r * t0.g.rs + c0, v);
+    if (t0.deferred) VecIO<T>::load(t0.x.p, r * t0.x.rs + c0, xv);
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = t0.deferred ? bn_dx_elem(v[k], xv[k], c0 + k, t0.cf) : v[k];
+    if (nterms > 1) {
+      VecIO<T>::load(t1.g.p, r * t1.g.rs + c0, v);
+      if (t1.deferred) VecIO<T>::load(t1.x.p, r * t1.x.rs + c0, xv);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        // round each resolved term to storage precision (the reference materialises it)
+        const float a = VecIO<T>::round(acc[k]);
+        const float b = VecIO<T>::round(t1.deferred ? bn_dx_elem(v[k], xv[k], c0 + k, t1.cf) : v[k]);
+        acc[k] = a + b;
+      }
+    }
+    if (accumulate) {
+      VecIO<T>::load(out.p, r * out.rs + c0, v);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = v[k] + VecIO<T>::round(acc[k]);
+    }
+    VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, acc);
+  }
+}
+
+template <typename T>
+__global__ void relu_kernel(View x, View dy, View out, long long pixels, int C, int bwd) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = pixels * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    float f[V], g[V];
+    VecIO<T>::load(x.p, r * x.rs + c0, f);
+    if (bwd) {
+      VecIO<T>::load(dy.p, r * dy.rs + c0, g);
+#pragma unroll
+      for (int k = 0; k < V; ++k) f[k] = f[k] > 0.f ? g[k] : 0.f;
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) f[k] = fmaxf(f[k], 0.f);
+    }
+    VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, f);
+  }
+}
+
+// avgpool forward with optional statistics of the written output (same tiling
+// as channel_sums: tile = range of output pixels)
+template <typename T>
+__global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, int ow, int C, int k,
+                                   float* part) {
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[2][kSumThreads][V];
+  const long long pixels = (long long)n * oh * ow;
+  const int cpr = C / V;
+  const int tiles = gridDim.x;
+  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
+  const long long r_begin = blockIdx.x * rows_per_tile;
+  const long long r_end = min(pixels, r_begin + rows_per_tile);
+  const float inv = 1.f / (float)(k * k);
+  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, cpr - cbase);
+    const int rows_per_iter = kSumThreads / ccount;
+    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
+    const int c0 = (cbase + tcol) * V;
+    float s1[V], s2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    if (trow < rows_per_iter) {
+      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+        const int img = (int)(r / ((long long)oh * ow));
+        const int rem = (int)(r - (long long)img * oh * ow);
+        const int oy = rem / ow, ox = rem - oy * ow;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        for (int dy = 0; dy < k; ++dy)
+          for (int dx = 0; dx < k; ++dx) {
+            float f[V];
+            const long long src = ((long long)img * h + oy * k + dy) * w + ox * k + dx;
+            VecIO<T>::load(x.p, src * x.rs + c0, f);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] += f[i];
+          }
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = VecIO<T>::round(acc[i] * inv);
+        VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, acc);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          s1[i] += acc[i];
+          s2[i] += acc[i] * acc[i];
+        }
+      }
+    }
+    if (part == nullptr) continue;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sh[0][threadIdx.x][i] = s1[i];
+      sh[1][threadIdx.x][i] = s2[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < ccount) {
+      float a[V], b[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int rr = 0; rr < rows_per_iter; ++rr)
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          a[i] += sh[0][rr * ccount + threadIdx.x][i];
+          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+        }
+      const int cc = (cbase + threadIdx.x) * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void avgpool_bwd_kernel(View dy, View dx, int n, int h, int w, int oh, int ow, int C, int k) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = (long long)n * h * w * cpr;
+  const float inv = 1.f / (float)(k * k);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    const int img = (int)(r / ((long long)h * w));
+    const int rem = (int)(r - (long long)img * h * w);
+    const int y = rem / w, x = rem - y * w;
+    float f[V];
+    if (y < oh * k && x < ow * k) {
+      const long long src = ((long long)img * oh + y / k) * ow + x / k;
+      VecIO<T>::load(dy.p, src * dy.rs + c0, f);
+#pragma unroll
+      for (int q = 0; q < V; ++q) f[q] = f[q] / (float)(k * k);
+    } else {
+#pragma unroll
+      for (int q = 0; q < V; ++q) f[q] = 0.f;
+    }
+    (void)inv;
+    VecIO<T>::store(const_cast<void*>(dx.p), r * dx.rs + c0, f);
+  }
+}
+
+template <typename T>
+__global__ void ews_kernel(View a, View b, View y, long long pixels, int C, int Cb) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = pixels * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    float f[V], g[V];
+    VecIO<T>::load(a.p, r * a.rs + c0, f);
+    if (c0 < Cb) {
+      VecIO<T>::load(b.p, r * b.rs + c0, g);
+#pragma unroll
+      for (int q = 0; q < V; ++q) f[q] += g[q];
+    }
+    VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, f);
+  }
+}
+
+template <typename T>
+__global__ void copy_kernel(View s, View d, long long pixels, int C) {
+  constexpr int V = VecIO<T>::V;
+  const int cpr = C / V;
+  const long long total = pixels * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int c0 = (int)(i - r * cpr) * V;
+    float f[V];
+    VecIO<T>::load(s.p, r * s.rs + c0, f);
+    VecIO<T>::store(const_cast<void*>(d.p), r * d.rs + c0, f);
+  }
+}
+
+template <typename T>
+__global__ void nchw_to_nhwc_kernel(const float* src, long long n, long long c, long long h, long long w,
+                                    View d, int Cs) {
+  const long long total = n * h * w * Cs;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % Cs);
+    const long long pix = i / Cs;
+    const long long img = pix / (h * w), rem = pix - img * h * w;
+    const float v = ch < c ? src[(img * c + ch) * h * w + rem] : 0.f;
+    T* dst = reinterpret_cast<T*>(const_cast<void*>(d.p)) + pix * d.rs + ch;
+    if constexpr (sizeof(T) == 2) *dst = __float2bfloat16_rn(v);
+    else *dst = v;
+  }
+}
+
+template <typename T>
+__global__ void nhwc_to_nchw_kernel(View s, long long n, long long c, long long h, long long w, float* dst) {
+  const long long total = n * c * h * w;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long hw = i % (h * w);
+    const long long t = i / (h * w);
+    const int ch = (int)(t % c);
+    const long long img = t / c;
+    const T v = reinterpret_cast<const T*>(s.p)[(img * h * w + hw) * s.rs + ch];
+    if constexpr (sizeof(T) == 2) dst[i] = __bfloat162float(v);
+    else dst[i] = v;
+  }
+}
+
+__global__ void sgd_kernel(float* w, const float* g, long long n, float lr) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    w[i] = w[i] - lr * g[i];
+}
+
+template <typename T>
+__global__ void pack_weights_kernel(const float* w, int co_n, int ci_n, int ci_s, int taps, int kpad,
+                                    int kpad_t, T* wp, T* wt) {
+  // forward pack [co][tap*ci_s + ci], transposed pack [ci][tap*co_n + co]
+  const long long tot_f = (long long)co_n * kpad;
+  const long long tot_t = (long long)ci_s * kpad_t;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot_f + tot_t;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (i < tot_f) {
+      const int co = (int)(i / kpad), k = (int)(i - (long long)co * kpad);
+      const int tap = k / ci_s, ci = k - tap * ci_s;
+      if (tap < taps && ci < ci_n) v = w[((long long)co * ci_n + ci) * taps + tap];
+      if (wp) {
+        if constexpr (sizeof(T) == 2) wp[i] = __float2bfloat16_rn(v);
+        else wp[i] = v;
+      }
+    } else {
+      const long long j = i - tot_f;
+      const int ci = (int)(j / kpad_t), k = (int)(j - (long long)ci * kpad_t);
+      const int tap = k / co_n, co = k - tap * co_n;
+      if (tap < taps && ci < ci_n) v = w[((long long)co * ci_n + ci) * taps + tap];
+      if (wt) {
+        if constexpr (sizeof(T) == 2) wt[j] = __float2bfloat16_rn(v);
+        else wt[j] = v;
+      }
+    }
+  }
+}
+
+inline int grid_for(long long work, int threads = 256) {
+  long long b = (work + threads - 1) / threads;
+  const long long cap = 148 * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+inline View vw(const bnff_view& v) { return View{v.ptr, (long long)v.row_stride}; }
+
+inline int check_view(int dtype, const bnff_view& v, const char* what) {
+  const int vec = dtype == BNFF_BF16 ? 8 : 4;
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "dtype %d", dtype);
+  if (v.ptr == nullptr) return set_error(BNFF_ERR_STATE, "%s: null pointer", what);
+  if (v.c % vec != 0 || v.row_stride % vec != 0 || (reinterpret_cast<uintptr_t>(v.ptr) & 15))
+    return set_error(BNFF_ERR_UNSUPPORTED, "%s: c=%lld rs=%lld must be multiples of %d, 16B aligned", what,
+                     (long long)v.c, (long long)v.row_stride, vec);
+  return BNFF_OK;
+}
+
+inline bool same_dims(const bnff_view& a, const bnff_view& b) {
+  return a.n == b.n && a.h == b.h && a.w == b.w && a.c == b.c;
+}
+
+}  // namespace bnff
+
+using namespace bnff;
+
+#define BNFF_DISPATCH(dtype, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                         \
+  do {                                                                                       \
+    if ((dtype) == BNFF_BF16) KERNEL<__nv_bfloat16><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); \
+    else KERNEL<float><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__);                          \
+  } while (0)
+
+extern "C" const char* bnff_last_error(void) { return g_err; }
+extern "C" int bnff_version(void) { return 100; }
+extern "C" int bnff_device_ok(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0 ? 1 : 0;
+}
+
+extern "C" int32_t bnff_sum_tiles(int64_t pixels) { return sum_tiles(pixels); }
+
+extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_view dy, bnff_coef coef,
+                                 float* part, void* stream) {
+  int rc;
+  const bnff_view& shape = (mode == 0) ? x : dy;
+  if ((rc = check_view(dtype, shape, "channel_sums"))) return rc;
+  if ((mode == 1 || (mode == 2 && coef.e)) && (rc = check_view(dtype, x, "channel_sums x"))) return rc;
+  if (mode == 1 && !same_dims(x, dy)) return set_error(BNFF_ERR_SHAPE, "channel_sums: x/dy dims differ");
+  const long long pixels = shape.n * shape.h * shape.w;
+  const int tiles = sum_tiles(pixels);
+  BNFF_DISPATCH(dtype, channel_sums_kernel, tiles, kSumThreads, 0, (cudaStream_t)stream, mode, vw(x), vw(dy),
+                pixels, (int)shape.c, coef, nullptr, part);
+  return check_launch("channel_sums");
+}
+
+extern "C" int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* sum,
+                                   double* sumsq, double* mean, double* var, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = (c + 31) / 32;
+  reduce_parts_kernel<<<g, 256, 0, st>>>(part, tiles, c, 0, sum);
+  reduce_parts_kernel<<<g, 256, 0, st>>>(part, tiles, c, 1, sumsq);
+  if (mean && var) stats_from_sums_kernel<<<(c + 127) / 128, 128, 0, st>>>(c, count, sum, sumsq, mean, var);
+  return check_launch("stats_finalize");
+}
+
+extern "C" int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, float* part, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "centered_var"))) return rc;
+  const long long pixels = x.n * x.h * x.w;
+  const int tiles = sum_tiles(pixels);
+  bnff_coef cf{};
+  BNFF_DISPATCH(dtype, channel_sums_kernel, tiles, kSumThreads, 0, (cudaStream_t)stream, 3, vw(x), vw(x),
+                pixels, (int)x.c, cf, mean, part);
+  return check_launch("centered_var");
+}
+
+extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+                                 void* stream);
+
+namespace bnff {
+__global__ void scale_kernel(double* v, int c, double s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < c) v[i] = v[i] * s;
+}
+}  // namespace bnff
+
+extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+                                 void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  reduce_parts_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, 0, var);
+  // var = sum(d^2) / count, as ops.py:227 divides the centred sum by the count
+  scale_kernel<<<(c + 127) / 128, 128, 0, st>>>(var, c, 1.0 / (double)count);
+  return check_launch("var_finalize");
+}
+
+extern "C" int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
+                              const float* beta, float eps, float* mean32, float* scale32, float* beta32,
+                              float* inv32, void* stream) {
+  bn_coeffs_kernel<<<(c + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c, mean, var, gamma, beta, eps, mean32,
+                                                                       scale32, beta32, inv32);
+  return check_launch("bn_coeffs");
+}
+
+extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count, const double* mean,
+                              const double* var, const float* gamma, float eps, double* dgamma64,
+                              double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
+                              float* dgamma32, float* dbeta32, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int gr = (c + 31) / 32;
+  reduce_parts_kernel<<<gr, 256, 0, st>>>(part, tiles, c, 0, dbeta64);
+  reduce_parts_kernel<<<gr, 256, 0, st>>>(part, tiles, c, 1, dgamma64);
+  dx_coeffs_kernel<<<(c + 127) / 128, 128, 0, st>>>(c, count, dbeta64, dgamma64, mean, var, gamma, eps, k1,
+                                                     k2, g, mean32, inv32, dgamma32, dbeta32);
+  return check_launch("dx_coeffs");
+}
+
+extern "C" int bnff_bn_apply(int32_t dtype, bnff_view x, bnff_view y, bnff_coef coef, int32_t relu,
+                             void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "bn_apply x")) || (rc = check_view(dtype, y, "bn_apply y"))) return rc;
+  if (!same_dims(x, y)) return set_error(BNFF_ERR_SHAPE, "bn_apply: x/y dims differ");
+  if (!coef.a || !coef.b || !coef.c) return set_error(BNFF_ERR_STATE, "bn_apply: missing statistics");
+  const long long pixels = x.n * x.h * x.w;
+  BNFF_DISPATCH(dtype, bn_apply_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(x), vw(y), pixels, (int)x.c, coef, relu);
+  return check_launch("bn_apply");
+}
+
+extern "C" int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, const bnff_grad_term* terms,
+                             int32_t nterms, void* stream) {
+  int rc;
+  if (nterms < 1 || nterms > 2) return set_error(BNFF_ERR_UNSUPPORTED, "grad_sum: 1..2 terms");
+  if ((rc = check_view(dtype, out, "grad_sum out"))) return rc;
+  TermDev td[2]{};
+  for (int i = 0; i < nterms; ++i) {
+    if ((rc = check_view(dtype, terms[i].g, "grad_sum term"))) return rc;
+    if (!same_dims(terms[i].g, out)) return set_error(BNFF_ERR_SHAPE, "grad_sum: term %d dims differ", i);
+    if (terms[i].deferred && (rc = check_view(dtype, terms[i].x, "grad_sum term x"))) return rc;
+    td[i].g = vw(terms[i].g);
+    td[i].x = vw(terms[i].x);
+    td[i].deferred = terms[i].deferred;
+    td[i].cf = terms[i].coef;
+  }
+  const long long pixels = out.n * out.h * out.w;
+  BNFF_DISPATCH(dtype, grad_sum_kernel, grid_for(pixels * out.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(out), pixels, (int)out.c, accumulate, td[0], td[1], nterms);
+  return check_launch("grad_sum");
+}
+
+extern "C" int bnff_relu_fwd(int32_t dtype, bnff_view x, bnff_view y, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "relu x")) || (rc = check_view(dtype, y, "relu y"))) return rc;
+  const long long pixels = x.n * x.h * x.w;
+  BNFF_DISPATCH(dtype, relu_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(x), vw(x), vw(y), pixels, (int)x.c, 0);
+  return check_launch("relu_fwd");
+}
+
+extern "C" int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view dx, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "relu_bwd x")) || (rc = check_view(dtype, dy, "relu_bwd dy")) ||
+      (rc = check_view(dtype, dx, "relu_bwd dx")))
+    return rc;
+  if (!same_dims(x, dy)) return set_error(BNFF_ERR_SHAPE, "relu_bwd: shape mismatch");
+  const long long pixels = x.n * x.h * x.w;
+  BNFF_DISPATCH(dtype, relu_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(x), vw(dy), vw(dx), pixels, (int)x.c, 1);
+  return check_launch("relu_bwd");
+}
+
+extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, float* stat_part,
+                                void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "avgpool x")) || (rc = check_view(dtype, y, "avgpool y"))) return rc;
+  if (y.h != x.h / k || y.w != x.w / k || y.c != x.c || y.n != x.n || y.h < 1 || y.w < 1)
+    return set_error(BNFF_ERR_SHAPE, "avgpool: bad output dims");
+  const long long pixels = y.n * y.h * y.w;
+  BNFF_DISPATCH(dtype, avgpool_fwd_kernel, sum_tiles(pixels), kSumThreads, 0, (cudaStream_t)stream, vw(x), vw(y),
+                (int)x.n, (int)x.h, (int)x.w, (int)y.h, (int)y.w, (int)x.c, k, stat_part);
+  return check_launch("avgpool_fwd");
+}
+
+extern "C" int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, dy, "avgpool_bwd dy")) || (rc = check_view(dtype, dx, "avgpool_bwd dx"))) return rc;
+  const long long pixels = dx.n * dx.h * dx.w;
+  BNFF_DISPATCH(dtype, avgpool_bwd_kernel, grid_for(pixels * dx.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(dy), vw(dx), (int)dx.n, (int)dx.h, (int)dx.w, (int)dy.h, (int)dy.w,
+                (int)dx.c, k);
+  return check_launch("avgpool_bwd");
+}
+
+extern "C" int bnff_ews_fwd(int32_t dtype, bnff_view a, bnff_view b, bnff_view y, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, a, "ews a")) || (rc = check_view(dtype, b, "ews b")) ||
+      (rc = check_view(dtype, y, "ews y")))
+    return rc;
+  if (b.c > a.c || a.n != b.n || a.h != b.h || a.w != b.w) return set_error(BNFF_ERR_SHAPE, "ews: bad dims");
+  const long long pixels = a.n * a.h * a.w;
+  BNFF_DISPATCH(dtype, ews_kernel, grid_for(pixels * a.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(a), vw(b), vw(y), pixels, (int)a.c, (int)b.c);
+  return check_launch("ews_fwd");
+}
+
+extern "C" int bnff_copy(int32_t dtype, bnff_view src, bnff_view dst, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, src, "copy src")) || (rc = check_view(dtype, dst, "copy dst"))) return rc;
+  if (!same_dims(src, dst)) return set_error(BNFF_ERR_SHAPE, "copy: dims differ");
+  const long long pixels = src.n * src.h * src.w;
+  BNFF_DISPATCH(dtype, copy_kernel, grid_for(pixels * src.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+                (cudaStream_t)stream, vw(src), vw(dst), pixels, (int)src.c);
+  return check_launch("copy");
+}
+
+extern "C" int bnff_nchw_to_nhwc(int32_t dtype, const float* src, int64_t n, int64_t c, int64_t h, int64_t w,
+                                 bnff_view dst, void* stream) {
+  if (dst.c < c || dst.n != n || dst.h != h || dst.w != w) return set_error(BNFF_ERR_SHAPE, "nchw_to_nhwc dims");
+  BNFF_DISPATCH(dtype, nchw_to_nhwc_kernel, grid_for(n * h * w * dst.c), 256, 0, (cudaStream_t)stream, src, n,
+                c, h, w, vw(dst), (int)dst.c);
+  return check_launch("nchw_to_nhwc");
+}
+
+extern "C" int bnff_nhwc_to_nchw(int32_t dtype, bnff_view src, float* dst, void* stream) {
+  BNFF_DISPATCH(dtype, nhwc_to_nchw_kernel, grid_for(src.n * src.c * src.h * src.w), 256, 0,
+                (cudaStream_t)stream, vw(src), src.n, src.c, src.h, src.w, dst);
+  return check_launch("nhwc_to_nchw");
+}
+
+extern "C" int bnff_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
+  sgd_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(w, g, n, lr);
+  return check_launch("sgd");
+}
+
+extern "C" int64_t bnff_pack_size(int32_t dtype, int32_t c_out, int32_t c_in_store, int32_t kh, int32_t kw) {
+  const int kb = dtype == BNFF_BF16 ? 64 : 32;
+  const long long k = (long long)kh * kw * c_in_store;
+  return (long long)c_out * ((k + kb - 1) / kb * kb);
+}
+
+extern "C" int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t c_in_store,
+                                 int32_t kh, int32_t kw, void* wpack, void* wpack_t, void* stream) {
+  const int kb = dtype == BNFF_BF16 ? 64 : 32;
+  const int taps = kh * kw;
+  const int kpad = (taps * c_in_store + kb - 1) / kb * kb;
+  const int kpad_t = (taps * c_out + kb - 1) / kb * kb;
+  const long long work = (long long)c_out * kpad + (long long)c_in_store * kpad_t;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == BNFF_BF16)
+    pack_weights_kernel<__nv_bfloat16><<<grid_for(work), 256, 0, st>>>(
+        w, c_out, c_in, c_in_store, taps, kpad, kpad_t, (__nv_bfloat16*)wpack, (__nv_bfloat16*)wpack_t);
+  else
+    pack_weights_kernel<float><<<grid_for(work), 256, 0, st>>>(w, c_out, c_in, c_in_store, taps, kpad, kpad_t,
+                                                               (float*)wpack, (float*)wpack_t);
+  return check_launch("pack_weights");
+}
+
+// dbias = sum over pixels of dy (optionally BN_DX-transformed); scratch is the
+// caller's partial buffer [tiles][2][C] placed after the wgrad workspace.
+namespace bnff {
+__global__ void parts_to_f32_kernel(const float* part, int tiles, int C, float* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int t = 0; t < tiles; ++t) s += (double)part[(long long)t * 2 * C + c];
+  out[c] = (float)s;
+}
+}  // namespace bnff
+
+extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, int32_t dy_pro, bnff_coef coef,
+                                  float* scratch, float* dbias, void* stream) {
+  bnff_coef cf = coef;
+  if (dy_pro != BNFF_PRO_BN_DX) cf.e = nullptr;
+  int rc = bnff_channel_sums(dtype, 2, dy_x, dy, cf, scratch, stream);
+  if (rc) return rc;
+  const long long pixels = dy.n * dy.h * dy.w;
+  parts_to_f32_kernel<<<(int)((dy.c + 127) / 128), 128, 0, (cudaStream_t)stream>>>(scratch, sum_tiles(pixels),
+                                                                                   (int)dy.c, dbias);
+  return check_launch("dbias");
+}

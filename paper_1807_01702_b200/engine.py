@@ -1,0 +1,809 @@
+"""Device executor: runs a (rewritten) layer graph on B200 through libbnff.
+
+Counterpart of the reference executor ``pkg/src/bnfuse/execute.py`` (forward
+/ backward handler tables, Activations with shared block buffers, the
+DeferredBNGrad hand-off).  The difference is *when* dispatch happens: the
+graph is walked ONCE at construction time ("compile"), every handler emits
+launch thunks with prebuilt C-ABI argument structs and statically placed
+device buffers, and a training step is then a flat replay of those thunks on
+one CUDA stream -- capturable as a single CUDA graph (``capture()``).
+
+Device layout:
+  * feature maps NHWC in bf16 or fp32; in view-concat mode every slot with a
+    ``buffer`` annotation is a channel-offset view of one (N,H,W,C_total)
+    block buffer, so Concat is free and producers write in place;
+  * per-channel statistics float64, placed at the same channel offsets of a
+    per-block stats array, so FusedConcatStats (concat_stats) is free too;
+  * gradients NHWC; a deferred BN gradient is (dt1, x, coefficient table) and
+    its dx transform runs inside whichever kernel reads it next (conv dgrad /
+    wgrad operand prologue, or the Split gradient-sum kernel);
+  * parameters: one flat fp32 master buffer in reference layout, one flat
+    fp32 gradient buffer (NCCL all-reduce target), packed bf16/fp32 copies of
+    the conv weights ([co][tap][ci] and [ci][tap][co]) refreshed after SGD.
+  * FusedNormReluConv does not materialise ``saved_postrelu`` unless asked:
+    backward recomputes relu(bn(x)) from x (bitwise identical in fp32 mode).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import graph as G
+from .errors import ShapeError, StateError
+
+# ---------------------------------------------------------------------------
+# small helpers
+# ---------------------------------------------------------------------------
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def view_of(t: torch.Tensor) -> _lib.View:
+    """NHWC torch tensor (possibly a channel slice) -> bnff_view."""
+    if t.dim() != 4 or t.stride(3) != 1:
+        raise ShapeError(f"expected an NHWC view with unit channel stride, got {tuple(t.shape)}")
+    n, h, w, c = t.shape
+    return _lib.View(_ptr(t), n, h, w, c, t.stride(2))
+
+
+def coef_of(a=None, b=None, c=None, d=None, e=None) -> _lib.Coef:
+    return _lib.Coef(_ptr(a), _ptr(b), _ptr(c), _ptr(d), _ptr(e))
+
+
+def _vec_of(dtype_code: int) -> int:
+    return 8 if dtype_code == _lib.BF16 else 4
+
+
+def _round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+@dataclass
+class Stats:
+    """Device ChannelStats: float64 sums/moments (possibly views into a block array)."""
+    sum: torch.Tensor
+    sumsq: torch.Tensor
+    mean: torch.Tensor
+    var: torch.Tensor
+    count: int
+
+    def slice(self, lo, hi):
+        return Stats(self.sum[lo:hi], self.sumsq[lo:hi], self.mean[lo:hi], self.var[lo:hi],
+                     self.count)
+
+
+@dataclass
+class Deferred:
+    """Device DeferredBNGrad (execute.py:93-126): gradient dt1 at the normalized
+    position + per-channel table (mean, invstd, k1, k2, g) + the tensor x the
+    normalization was applied to."""
+    dt1: torch.Tensor
+    x: torch.Tensor
+    mean: torch.Tensor
+    inv: torch.Tensor
+    k1: torch.Tensor
+    k2: torch.Tensor
+    g: torch.Tensor
+
+    def slice(self, lo, hi):
+        return Deferred(self.dt1[..., lo:hi], self.x[..., lo:hi], self.mean[lo:hi],
+                        self.inv[lo:hi], self.k1[lo:hi], self.k2[lo:hi], self.g[lo:hi])
+
+    def coef(self):
+        return coef_of(self.mean, self.inv, self.k1, self.k2, self.g)
+
+
+@dataclass
+class Plain:
+    t: torch.Tensor
+
+
+# ---------------------------------------------------------------------------
+# engine
+# ---------------------------------------------------------------------------
+
+
+class Engine:
+    """Compile a graph for the device and run training steps on it.
+
+    Parameters
+    ----------
+    g : Graph (any fusion level; ``fusion.plan`` output)
+    dtype : "bf16" (tensor-core bf16, perf mode) or "f32" (3xTF32 parity mode)
+    input_grad : also produce the gradient w.r.t. the graph input (reference
+        ``GradBundle.inputs``); off for training throughput runs.
+    save_postrelu : materialise FusedNormReluConv's saved post-ReLU tensor
+        (reference schedule) instead of recomputing it in backward.
+    """
+
+    def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
+                 save_postrelu: bool = False, lr: float = 0.0):
+        self.L = _lib.lib()
+        self.g = g
+        self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
+        self.tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.vec = _vec_of(self.dcode)
+        self.dev = torch.device(device)
+        self.input_grad = input_grad
+        self.save_postrelu = save_postrelu
+        self.lr = float(lr)
+        self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
+                              (n.kind == G.CONCAT and not n.attrs.physical) for n in g.nodes)
+        self.fwd: list = []
+        self.bwd: list = []
+        self.opt: list = []
+        self.launch_counts = {"fwd": 0, "bwd": 0, "opt": 0}
+        self._cur = None
+        self._keep: list = []  # ctypes structs referenced by thunks
+        self._alloc_params()
+        self._alloc_acts()
+        self._compile_forward()
+        self._compile_backward()
+        self._compile_optimizer()
+        self.graph_exec = None
+
+    # ------------------------------------------------------------------ alloc
+    def _empty(self, shape, dtype=None):
+        return torch.empty(shape, dtype=dtype or self.tdt, device=self.dev)
+
+    def _zeros(self, shape, dtype=None):
+        return torch.zeros(shape, dtype=dtype or self.tdt, device=self.dev)
+
+    def _alloc_params(self):
+        g = self.g
+        self.param_names = list(g.params)
+        sizes = [int(np.asarray(g.params[k]).size) for k in self.param_names]
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        total = int(offs[-1])
+        host = np.concatenate([np.asarray(g.params[k], np.float32).reshape(-1)
+                               for k in self.param_names]) if total else np.zeros(0, np.float32)
+        self.wflat = torch.from_numpy(host).to(self.dev)
+        self.gflat = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        self.poff = {k: (int(offs[i]), int(sizes[i])) for i, k in enumerate(self.param_names)}
+        self.packs = {}  # conv name -> (wpack, wpack_t, cin_store)
+
+    def param(self, name):
+        o, n = self.poff[name]
+        return self.wflat[o:o + n]
+
+    def grad(self, name):
+        o, n = self.poff[name]
+        return self.gflat[o:o + n]
+
+    def _store_c(self, c: int) -> int:
+        return _round_up(c, self.vec)
+
+    def _alloc_acts(self):
+        g = self.g
+        self.acts: dict = {}
+        self.group_buf: dict = {}
+        self.group_stats: dict = {}
+        if self.use_shared:
+            for grp, (ct, h, w) in g.buffer_groups.items():
+                n = next(s.shape[0] for s in g.slots.values() if s.buffer and s.buffer[0] == grp)
+                if ct % self.vec:
+                    raise _lib.UnsupportedError(
+                        f"block buffer {grp}: {ct} channels not a multiple of {self.vec}")
+                self.group_buf[grp] = self._zeros((n, h, w, ct))
+                self.group_stats[grp] = [self._zeros((ct,), torch.float64) for _ in range(4)]
+        # graph input: channel-padded NHWC
+        for sid in g.inputs:
+            n, c, h, w = g.slots[sid].shape
+            self.acts[sid] = self._zeros((n, h, w, self._store_c(c)))
+        self.input_c = {sid: g.slots[sid].shape[1] for sid in g.inputs}
+
+    def _feature(self, sid) -> torch.Tensor:
+        """Device storage for a feature slot produced by a node (allocated on first use)."""
+        if sid in self.acts:
+            return self.acts[sid]
+        s = self.g.slots[sid]
+        n, c, h, w = s.shape
+        if c % self.vec:
+            raise _lib.UnsupportedError(
+                f"slot {sid} ({s.name}): {c} channels not a multiple of {self.vec}")
+        if self.use_shared and s.buffer is not None:
+            grp, off = s.buffer
+            t = self.group_buf[grp][..., off:off + c]
+        else:
+            t = self._empty((n, h, w, c))
+        self.acts[sid] = t
+        return t
+
+    def _stats_for(self, feat_sid: int, c: int, count: int) -> Stats:
+        s = self.g.slots[feat_sid]
+        if self.use_shared and s.buffer is not None:
+            grp, off = s.buffer
+            arrs = [a[off:off + c] for a in self.group_stats[grp]]
+        else:
+            arrs = [self._zeros((c,), torch.float64) for _ in range(4)]
+        return Stats(*arrs, count=count)
+
+    # ------------------------------------------------------------ emit helpers
+    def _emit(self, fn, *args, what=""):
+        """Append a launch thunk calling fn(*args, stream)."""
+        L = self.L
+        check = _lib.check
+        self._keep.append(args)
+        cur = self._cur
+
+        def thunk(stream):
+            check(fn(*args, stream), what)
+        cur.append(thunk)
+
+    def _emit_stats_finalize(self, part, tiles, c, count, st: Stats):
+        self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
+                   _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize")
+
+    def _pack(self, conv, cin_store):
+        key = conv.name
+        if key not in self.packs:
+            n = self.L.bnff_pack_size(self.dcode, conv.out_c, cin_store, conv.kh, conv.kw)
+            nt = self.L.bnff_pack_size(self.dcode, cin_store, conv.out_c, conv.kh, conv.kw)
+            self.packs[key] = (self._zeros((n,)), self._zeros((nt,)), cin_store, conv)
+        return self.packs[key]
+
+    def _bn_tables(self, st: Stats, bn, tag):
+        """fp32 (mean, scale, beta, inv) for a normalize prologue (bn_fwd ops.py:246-249)."""
+        c = st.mean.shape[0]
+        mean32, scale32, beta32, inv32 = (self._zeros((c,), torch.float32) for _ in range(4))
+        gam = self.param(f"{bn.name}.gamma")
+        bet = self.param(f"{bn.name}.beta")
+        self._emit(self.L.bnff_bn_coeffs, c, _ptr(st.mean), _ptr(st.var), _ptr(gam), _ptr(bet),
+                   C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32), _ptr(inv32),
+                   what=f"bn_coeffs {tag}")
+        return mean32, scale32, beta32, inv32
+
+    def _channel_stats(self, x: torch.Tensor, st: Stats, tag):
+        pixels = x.shape[0] * x.shape[1] * x.shape[2]
+        tiles = self.L.bnff_sum_tiles(pixels)
+        part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+        self._emit(self.L.bnff_channel_sums, self.dcode, 0, view_of(x), view_of(x), coef_of(),
+                   _ptr(part), what=f"channel_sums {tag}")
+        self._emit_stats_finalize(part, tiles, x.shape[3], pixels, st)
+
+    # ---------------------------------------------------------------- forward
+    def _compile_forward(self):
+        self._cur = self.fwd
+        self.node_stats: dict = {}   # BN node id -> Stats (two/one-pass, baseline)
+        self.node_tables: dict = {}  # node id -> fp32 tables
+        self.stats: dict = {}        # stats slot id -> Stats
+        for node in self.g.nodes:
+            try:
+                getattr(self, "_f_" + node.kind)(node)
+            except ShapeError as e:
+                raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
+        self.launch_counts["fwd"] = len(self.fwd)
+
+    def _conv_fprop(self, node, x, y, conv, pro, tables, stat_part):
+        cin_store = x.shape[3]
+        wp, _, _, _ = self._pack(conv, cin_store)
+        if tables is None:
+            cf = coef_of()
+        else:
+            cf = coef_of(tables[0], tables[1], tables[2])
+        args = _lib.FpropArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x),
+                              view_of(y), _ptr(wp), _ptr(self.param(f"{conv.name}.bias")), pro, cf,
+                              _ptr(stat_part))
+        self._emit(self.L.bnff_conv_fprop, C.byref(args), what=f"fprop {node.name}")
+        self._keep.append(args)
+
+    def _f_Conv2D(self, node):
+        at = node.attrs
+        x = self.acts[node.inputs[0]]
+        y = self._feature(node.outputs[0])
+        pro = _lib.PRO_RELU if at.clip_input else _lib.PRO_NONE
+        if node.kind == G.FUSED_CONV_STATS:
+            mt = (y.shape[0] * y.shape[1] * y.shape[2] + 127) // 128
+            part = self._empty((mt, 2, y.shape[3]), torch.float32)
+            self._conv_fprop(node, x, y, at.conv, pro, None, part)
+            st = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
+            self._emit_stats_finalize(part, mt, y.shape[3], st.count, st)
+            self.stats[node.outputs[1]] = st
+        else:
+            self._conv_fprop(node, x, y, at.conv, pro, None, None)
+
+    _f_FusedConvStats = _f_Conv2D
+
+    def _f_BatchNorm(self, node):
+        x = self.acts[node.inputs[0]]
+        y = self._feature(node.outputs[0])
+        c = x.shape[3]
+        pixels = x.shape[0] * x.shape[1] * x.shape[2]
+        st = Stats(*(self._zeros((c,), torch.float64) for _ in range(4)), count=pixels)
+        self._channel_stats(x, st, node.name)
+        if not node.attrs.onepass:  # two-pass: centred variance overwrites var (ops.py:226-227)
+            tiles = self.L.bnff_sum_tiles(pixels)
+            part = self._empty((tiles, 2, c), torch.float32)
+            self._emit(self.L.bnff_centered_var, self.dcode, view_of(x), _ptr(st.mean), _ptr(part),
+                       what="centered_var")
+            self._emit(self.L.bnff_var_finalize, _ptr(part), tiles, c, pixels, _ptr(st.var),
+                       what="var_finalize")
+        self.node_stats[node.id] = st
+        tb = self._bn_tables(st, node.attrs.bn, node.name)
+        self.node_tables[node.id] = tb
+        self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(y),
+                   coef_of(tb[0], tb[1], tb[2]), 0, what="bn_apply")
+
+    def _f_ReLU(self, node):
+        x = self.acts[node.inputs[0]]
+        y = self._feature(node.outputs[0])
+        self._emit(self.L.bnff_relu_fwd, self.dcode, view_of(x), view_of(y), what="relu_fwd")
+
+    def _f_FissionSubBN1(self, node):
+        x = self.acts[node.inputs[0]]
+        st = self._stats_for(node.inputs[0], x.shape[3], x.shape[0] * x.shape[1] * x.shape[2])
+        self._channel_stats(x, st, node.name)
+        self.stats[node.outputs[0]] = st
+
+    def _f_FissionSubBN2(self, node):
+        x = self.acts[node.inputs[0]]
+        st = self.stats.get(node.inputs[1])
+        if st is None:
+            raise StateError(f"{node.name}: statistics slot {node.inputs[1]} never produced")
+        y = self._feature(node.outputs[0])
+        tb = self._bn_tables(st, node.attrs.bn, node.name)
+        self.node_tables[node.id] = tb
+        self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(y),
+                   coef_of(tb[0], tb[1], tb[2]), 0, what="subbn2")
+
+    def _f_FusedNormReluConv(self, node):
+        at = node.attrs
+        x = self.acts[node.inputs[0]]
+        st = self.stats.get(node.inputs[1])
+        if st is None:
+            raise StateError(f"{at.conv.name}: no statistics available for normalization input")
+        y = self._feature(node.outputs[0])
+        tb = self._bn_tables(st, at.bn, node.name)
+        self.node_tables[node.id] = tb
+        if self.save_postrelu:
+            saved = self._feature(node.outputs[1])
+            self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(saved),
+                       coef_of(tb[0], tb[1], tb[2]), 1, what="saved_postrelu")
+        part = None
+        if at.emit_stats:
+            mt = (y.shape[0] * y.shape[1] * y.shape[2] + 127) // 128
+            part = self._empty((mt, 2, y.shape[3]), torch.float32)
+        self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
+        if at.emit_stats:
+            ost = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
+            self._emit_stats_finalize(part, mt, y.shape[3], ost.count, ost)
+            self.stats[node.outputs[2]] = ost
+
+    def _f_Concat(self, node):
+        y = self._feature(node.outputs[0])
+        if node.attrs.physical:
+            off = 0
+            for s in node.inputs:
+                piece = self.acts[s]
+                c = piece.shape[3]
+                self._emit(self.L.bnff_copy, self.dcode, view_of(piece), view_of(y[..., off:off + c]),
+                           what="concat_copy")
+                off += c
+        else:
+            off = 0
+            for s in node.inputs:  # view mode: producers already wrote in place
+                piece = self.acts[s]
+                if piece.data_ptr() != y[..., off:].data_ptr():
+                    raise StateError(f"{node.name}: view-concat piece {s} not in the block buffer")
+                off += piece.shape[3]
+
+    def _f_FusedConcatStats(self, node):
+        feat = [s for s in node.inputs if self.g.slots[s].kind == "feature"]
+        stat = [s for s in node.inputs if self.g.slots[s].kind == "stats"]
+        self._f_Concat(node)
+        y = self.acts[node.outputs[0]]
+        st = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
+        off = 0
+        for fs, ss in zip(feat, stat):
+            piece = self.stats[ss]
+            c = piece.mean.shape[0]
+            for a, b in zip((st.sum, st.sumsq, st.mean, st.var),
+                            (piece.sum, piece.sumsq, piece.mean, piece.var)):
+                if a[off:off + c].data_ptr() != b.data_ptr():  # not in place: copy (ops.py:128-143)
+                    dst = a[off:off + c]
+                    self._cur.append(lambda stream, d=dst, s=b: d.copy_(s))
+            off += c
+        self.stats[node.outputs[1]] = st
+
+    def _f_Split(self, node):
+        x = self.acts[node.inputs[0]]
+        for o in node.outputs:
+            self.acts[o] = x
+
+    def _f_EltwiseSum(self, node):
+        a, b = self.acts[node.inputs[0]], self.acts[node.inputs[1]]
+        y = self._feature(node.outputs[0])
+        if not node.attrs.pad_channels and a.shape != b.shape:
+            raise ShapeError(f"EltwiseSum operands {tuple(a.shape)} vs {tuple(b.shape)}")
+        self._emit(self.L.bnff_ews_fwd, self.dcode, view_of(a), view_of(b), view_of(y), what="ews")
+
+    def _f_AvgPool(self, node):
+        x = self.acts[node.inputs[0]]
+        y = self._feature(node.outputs[0])
+        part = None
+        pixels = y.shape[0] * y.shape[1] * y.shape[2]
+        if node.attrs.emit_stats:
+            tiles = self.L.bnff_sum_tiles(pixels)
+            part = self._empty((tiles, 2, y.shape[3]), torch.float32)
+        self._emit(self.L.bnff_avgpool_fwd, self.dcode, view_of(x), view_of(y), node.attrs.k,
+                   _ptr(part), what="avgpool")
+        if node.attrs.emit_stats:
+            st = self._stats_for(node.outputs[0], y.shape[3], pixels)
+            self._emit_stats_finalize(part, tiles, y.shape[3], pixels, st)
+            self.stats[node.outputs[1]] = st
+
+    # --------------------------------------------------------------- backward
+    def _compile_backward(self):
+        self._cur = self.bwd
+        g = self.g
+        self.loss_grad = {}
+        self.grads: dict = {}
+        for sid in g.outputs:
+            n, c, h, w = g.slots[sid].shape
+            t = self._zeros((n, h, w, c))
+            self.loss_grad[sid] = t
+            self.grads[sid] = Plain(t)
+        # shared split-K workspace (kernels run in stream order)
+        ws = 1
+        for node in g.nodes:
+            conv = getattr(node.attrs, "conv", None)
+            if conv is None:
+                continue
+            xs = g.slots[node.inputs[0]].shape
+            oh, ow = conv.out_hw(xs[2], xs[3])
+            cin_s = self._store_c(xs[1])
+            ws = max(ws, self.L.bnff_wgrad_workspace(xs[0], oh, ow, conv.kh, conv.kw, cin_s,
+                                                    conv.out_c, 0))
+        self.wg_ws = self._empty((ws,), torch.float32)
+        for node in reversed(g.nodes):
+            try:
+                getattr(self, "_b_" + node.kind)(node)
+            except ShapeError as e:
+                raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
+        self.input_grads = {}
+        for sid in g.inputs:
+            gv = self.grads.get(sid)
+            self.input_grads[sid] = self._resolve(gv) if (gv is not None and self.input_grad) else None
+        self.launch_counts["bwd"] = len(self.bwd)
+
+    def _fresh_like(self, t):
+        return self._empty(tuple(t.shape))
+
+    def _resolve(self, gv) -> torch.Tensor:
+        """Materialise a deferred package (DeferredBNGrad.materialize, execute.py:123-126)."""
+        if isinstance(gv, Plain):
+            return gv.t
+        out = self._fresh_like(gv.dt1)
+        term = _lib.GradTerm(view_of(gv.dt1), view_of(gv.x), 1, gv.coef())
+        self._keep.append(term)
+        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, C.byref(term), 1,
+                   what="bn_dx")
+        return out
+
+    def _incoming(self, sid) -> torch.Tensor:
+        gv = self.grads.get(sid)
+        if gv is None:
+            raise StateError(f"no gradient arrived at slot {sid}")
+        return self._resolve(gv)
+
+    def _add_grad(self, sid, gv):
+        cur = self.grads.get(sid)
+        if cur is None:
+            self.grads[sid] = gv
+            return
+        if isinstance(cur, Deferred) or isinstance(gv, Deferred):
+            raise StateError(f"slot {sid}: deferred gradient cannot be accumulated")
+        out = self._fresh_like(cur.t)
+        terms = (_lib.GradTerm * 2)(_lib.GradTerm(view_of(cur.t), view_of(cur.t), 0, coef_of()),
+                                    _lib.GradTerm(view_of(gv.t), view_of(gv.t), 0, coef_of()))
+        self._keep.append(terms)
+        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, 2, what="grad_add")
+        self.grads[sid] = Plain(out)
+
+    def _wants_dx(self, sid):
+        return self.input_grad or sid not in self.g.inputs
+
+    def _conv_backward(self, node, conv, x, dy_gv, x_pro, x_tables, dgrad_epi, dgrad_tables):
+        """dgrad (+ epilogue) and wgrad of one conv; returns the dx tensor (or None)."""
+        cin_store = x.shape[3]
+        wp, wt, _, _ = self._pack(conv, cin_store)
+        if isinstance(dy_gv, Deferred):
+            dy, dy_x, dy_pro, dy_coef = dy_gv.dt1, dy_gv.x, _lib.PRO_BN_DX, dy_gv.coef()
+        else:
+            dy, dy_x, dy_pro, dy_coef = dy_gv.t, dy_gv.t, _lib.PRO_NONE, coef_of()
+        dx, part = None, None
+        if self._wants_dx(node.inputs[0]):
+            dx = self._empty(tuple(x.shape))
+            ecoef = coef_of()
+            if dgrad_epi == _lib.DG_NRC:
+                mt = (x.shape[0] * x.shape[1] * x.shape[2] + 127) // 128
+                part = self._empty((mt, 2, x.shape[3]), torch.float32)
+                m32, s32, b32, i32 = dgrad_tables
+                ecoef = coef_of(m32, s32, b32, i32)
+            da = _lib.DgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(dy),
+                                view_of(dy_x), dy_pro, dy_coef, view_of(dx), view_of(x), _ptr(wt),
+                                dgrad_epi, ecoef, _ptr(part))
+            self._keep.append(da)
+            self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}")
+        xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
+        wa = _lib.WgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x), x_pro,
+                            xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
+                            _ptr(self.grad(f"{conv.name}.weight")), conv.in_c,
+                            _ptr(self.grad(f"{conv.name}.bias")))
+        self._keep.append(wa)
+        self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}")
+        return dx, part
+
+    def _b_Conv2D(self, node):
+        at = node.attrs
+        raw = self.grads.get(node.outputs[0])
+        if raw is None:
+            raise StateError(f"no gradient arrived at slot {node.outputs[0]}")
+        x = self.acts[node.inputs[0]]
+        epi = _lib.DG_CLIP if at.clip_input else _lib.DG_PLAIN
+        pro = _lib.PRO_RELU if at.clip_input else _lib.PRO_NONE
+        dx, _ = self._conv_backward(node, at.conv, x, raw, pro, None, epi, None)
+        if dx is not None:
+            self._add_grad(node.inputs[0], Plain(dx))
+
+    _b_FusedConvStats = _b_Conv2D
+
+    def _dx_coeffs(self, part, tiles, c, count, st: Stats, bn, tag):
+        k1, k2, gg, m32, i32 = (self._zeros((c,), torch.float32) for _ in range(5))
+        dg64, db64 = self._zeros((c,), torch.float64), self._zeros((c,), torch.float64)
+        self._emit(self.L.bnff_dx_coeffs, c, _ptr(part), tiles, count, _ptr(st.mean), _ptr(st.var),
+                   _ptr(self.param(f"{bn.name}.gamma")), C.c_float(bn.eps), _ptr(dg64), _ptr(db64),
+                   _ptr(k1), _ptr(k2), _ptr(gg), _ptr(m32), _ptr(i32),
+                   _ptr(self.grad(f"{bn.name}.gamma")), _ptr(self.grad(f"{bn.name}.beta")),
+                   what=f"dx_coeffs {tag}")
+        return m32, i32, k1, k2, gg
+
+    def _bn_grad_sums(self, x, dy, tables, st, bn, tag):
+        """dbeta = sum dy, dgamma = sum dy*xhat (ops.py:271-274) -> backward table."""
+        pixels = x.shape[0] * x.shape[1] * x.shape[2]
+        tiles = self.L.bnff_sum_tiles(pixels)
+        part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+        m32, _, _, i32 = tables
+        self._emit(self.L.bnff_channel_sums, self.dcode, 1, view_of(x), view_of(dy),
+                   coef_of(m32, i32), _ptr(part), what=f"bn_bwd_sums {tag}")
+        return self._dx_coeffs(part, tiles, x.shape[3], pixels, st, bn, tag)
+
+    def _b_BatchNorm(self, node):
+        st = self.node_stats.get(node.id)
+        if st is None:
+            raise StateError(f"node {node.id}: backward before forward (no saved statistics)")
+        dy = self._incoming(node.outputs[0])
+        x = self.acts[node.inputs[0]]
+        m32, i32, k1, k2, gg = self._bn_grad_sums(x, dy, self.node_tables[node.id], st,
+                                                  node.attrs.bn, node.name)
+        self._add_grad(node.inputs[0], Plain(self._resolve(Deferred(dy, x, m32, i32, k1, k2, gg))))
+
+    def _b_ReLU(self, node):
+        dy = self._incoming(node.outputs[0])
+        x = self.acts[node.inputs[0]]
+        dx = self._fresh_like(x)
+        self._emit(self.L.bnff_relu_bwd, self.dcode, view_of(x), view_of(dy), view_of(dx),
+                   what="relu_bwd")
+        self._add_grad(node.inputs[0], Plain(dx))
+
+    def _b_FissionSubBN1(self, node):
+        if node.attrs.defer_backward:
+            return
+        pending = self.grads.get(node.inputs[0])
+        if isinstance(pending, Deferred):
+            self.grads[node.inputs[0]] = Plain(self._resolve(pending))
+
+    def _b_FissionSubBN2(self, node):
+        dy = self._incoming(node.outputs[0])
+        x = self.acts[node.inputs[0]]
+        st = self.stats[node.inputs[1]]
+        m32, i32, k1, k2, gg = self._bn_grad_sums(x, dy, self.node_tables[node.id], st,
+                                                  node.attrs.bn, node.name)
+        self._add_grad(node.inputs[0], Deferred(dy, x, m32, i32, k1, k2, gg))
+
+    def _b_FusedNormReluConv(self, node):
+        at = node.attrs
+        gv = self.grads.get(node.outputs[0])
+        if gv is None:
+            raise StateError(f"no gradient arrived at slot {node.outputs[0]}")
+        x = self.acts[node.inputs[0]]
+        st = self.stats[node.inputs[1]]
+        tb = self.node_tables[node.id]
+        if not self._wants_dx(node.inputs[0]):
+            raise StateError("FusedNormReluConv directly on the graph input is not supported")
+        dt1, part = self._conv_backward(node, at.conv, x, gv, _lib.PRO_BN_RELU, tb, _lib.DG_NRC, tb)
+        mt = part.shape[0]
+        m32, i32, k1, k2, gg = self._dx_coeffs(part, mt, x.shape[3], st.count, st, at.bn, node.name)
+        self._add_grad(node.inputs[0], Deferred(dt1, x, m32, i32, k1, k2, gg))
+
+    def _b_Concat(self, node):
+        gv = self.grads.get(node.outputs[0])
+        if gv is None:
+            raise StateError(f"no gradient arrived at concat output {node.outputs[0]}")
+        physical = node.kind == G.CONCAT and node.attrs.physical
+        off = 0
+        for s in (s for s in node.inputs if self.g.slots[s].kind == "feature"):
+            c = self.g.slots[s].shape[1]
+            if isinstance(gv, Deferred):
+                piece = gv.slice(off, off + c)
+            else:
+                sl = gv.t[..., off:off + c]
+                if physical:  # the reference copies each piece (execute.py:438)
+                    cp = self._empty(tuple(sl.shape))
+                    self._emit(self.L.bnff_copy, self.dcode, view_of(sl), view_of(cp),
+                               what="concat_bwd_copy")
+                    sl = cp
+                piece = Plain(sl)
+            self._add_grad(s, piece)
+            off += c
+
+    _b_FusedConcatStats = _b_Concat
+
+    def _b_Split(self, node):
+        branches = []
+        for o in node.outputs:
+            gv = self.grads.get(o)
+            if gv is None:
+                raise StateError(f"no gradient arrived at split branch {o}")
+            branches.append(gv)
+        # in place into a plain branch's storage when one exists (block gradient buffer)
+        out = next((b.t for b in branches if isinstance(b, Plain)), None)
+        if out is None:
+            out = self._fresh_like(branches[0].dt1)
+        terms = (_lib.GradTerm * len(branches))()
+        for i, b in enumerate(branches):
+            if isinstance(b, Plain):
+                terms[i] = _lib.GradTerm(view_of(b.t), view_of(b.t), 0, coef_of())
+            else:
+                terms[i] = _lib.GradTerm(view_of(b.dt1), view_of(b.x), 1, b.coef())
+        self._keep.append(terms)
+        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, len(branches),
+                   what="split_bwd")
+        self._add_grad(node.inputs[0], Plain(out))
+
+    def _b_EltwiseSum(self, node):
+        dy = self._incoming(node.outputs[0])
+        self._add_grad(node.inputs[0], Plain(dy))
+        cb = self.g.slots[node.inputs[1]].shape[1]
+        self._add_grad(node.inputs[1], Plain(dy[..., :cb] if node.attrs.pad_channels else dy))
+
+    def _b_AvgPool(self, node):
+        dy = self._incoming(node.outputs[0])
+        x = self.acts[node.inputs[0]]
+        if not self._wants_dx(node.inputs[0]):
+            return
+        dx = self._fresh_like(x)
+        self._emit(self.L.bnff_avgpool_bwd, self.dcode, view_of(dy), view_of(dx), node.attrs.k,
+                   what="avgpool_bwd")
+        self._add_grad(node.inputs[0], Plain(dx))
+
+    # -------------------------------------------------------------- optimizer
+    def _compile_optimizer(self):
+        self._cur = self.opt
+        if self.lr != 0.0:
+            self._emit(self.L.bnff_sgd, _ptr(self.wflat), _ptr(self.gflat), self.wflat.numel(),
+                       C.c_float(self.lr), what="sgd")
+        self.repack = []
+        self._cur = self.repack
+        for name, (wp, wt, cin_s, conv) in self.packs.items():
+            self._emit(self.L.bnff_pack_weights, self.dcode, _ptr(self.param(f"{name}.weight")),
+                       conv.out_c, conv.in_c, cin_s, conv.kh, conv.kw, _ptr(wp), _ptr(wt),
+                       what="pack_weights")
+        self._cur = None
+        self.launch_counts["opt"] = len(self.opt) + len(self.repack)
+        # initial packing of the current weights
+        self._run(self.repack)
+
+    # -------------------------------------------------------------------- run
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def _run(self, thunks):
+        s = self._stream()
+        for t in thunks:
+            t(s)
+
+    def set_input(self, x):
+        """Graph input: NCHW fp32 (numpy or torch, host or device) -> padded NHWC."""
+        sid = self.g.inputs[0]
+        n, c, h, w = self.g.slots[sid].shape
+        xt = torch.as_tensor(x)
+        if tuple(xt.shape) != (n, c, h, w):
+            raise ShapeError(f"input slot {sid}: shape {tuple(xt.shape)} != declared {(n, c, h, w)}")
+        xt = xt.to(self.dev, torch.float32, non_blocking=True).contiguous()
+        _lib.check(self.L.bnff_nchw_to_nhwc(self.dcode, _ptr(xt), n, c, h, w,
+                                            view_of(self.acts[sid]), self._stream()), "input")
+        self._keep_input = xt
+
+    def set_loss_grad(self, dy):
+        sid = self.g.outputs[0]
+        n, c, h, w = self.g.slots[sid].shape
+        dt = torch.as_tensor(dy).to(self.dev, torch.float32).contiguous()
+        if tuple(dt.shape) != (n, c, h, w):
+            raise ShapeError(f"loss grad slot {sid}: shape {tuple(dt.shape)} != {(n, c, h, w)}")
+        _lib.check(self.L.bnff_nchw_to_nhwc(self.dcode, _ptr(dt), n, c, h, w,
+                                            view_of(self.loss_grad[sid]), self._stream()), "dy")
+        self._keep_dy = dt
+
+    def forward(self):
+        self._run(self.fwd)
+
+    def backward(self):
+        self._run(self.bwd)
+
+    def optimizer_step(self):
+        self._run(self.opt)
+        self._run(self.repack)
+
+    def step(self):
+        """One training iteration: forward, backward, SGD (+ weight repack)."""
+        if self.graph_exec is not None:
+            self.graph_exec.replay()
+            return
+        self.forward()
+        self.backward()
+        self.optimizer_step()
+
+    def capture(self):
+        """Capture forward+backward+optimizer as one CUDA graph (replayed by step())."""
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self.forward()
+            self.backward()  # warm: first launches set kernel attributes
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            self.forward()
+            self.backward()
+            self._run(self.opt)
+            self._run(self.repack)
+        self.graph_exec = gr
+        return gr
+
+    def num_launches(self) -> int:
+        return (self.launch_counts["fwd"] + self.launch_counts["bwd"] + self.launch_counts["opt"])
+
+    # --------------------------------------------------------------- readback
+    def to_nchw(self, t: torch.Tensor, c_real: int | None = None) -> np.ndarray:
+        a = t.float().permute(0, 3, 1, 2)
+        if c_real is not None:
+            a = a[:, :c_real]
+        return a.contiguous().cpu().numpy()
+
+    def output(self, sid=None) -> np.ndarray:
+        sid = self.g.outputs[0] if sid is None else sid
+        return self.to_nchw(self.acts[sid])
+
+    def act(self, sid) -> np.ndarray:
+        return self.to_nchw(self.acts[sid], self.g.slots[sid].shape[1])
+
+    def input_grad_nchw(self, sid=None):
+        sid = self.g.inputs[0] if sid is None else sid
+        t = self.input_grads.get(sid)
+        return None if t is None else self.to_nchw(t, self.input_c[sid])
+
+    def param_grads(self) -> dict:
+        host = self.gflat.cpu().numpy()
+        out = {}
+        for k in self.param_names:
+            o, n = self.poff[k]
+            out[k] = host[o:o + n].reshape(np.asarray(self.g.params[k]).shape)
+        return out
+
+    def params_now(self) -> dict:
+        host = self.wflat.cpu().numpy()
+        return {k: host[o:o + n].reshape(np.asarray(self.g.params[k]).shape)
+                for k, (o, n) in self.poff.items()}
+
+    def stats_of(self, stats_sid):
+        st = self.stats[stats_sid]
+        return {k: getattr(st, k).cpu().numpy() for k in ("sum", "sumsq", "mean", "var")}

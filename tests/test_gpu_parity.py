@@ -1,0 +1,209 @@
+"""GPU parity: libbnff (through the device engine / C ABI) vs the CPU oracle.
+
+Tolerances (stated per the north star):
+  * fp32 mode (3xTF32 tcgen05): max|gpu - ref| <= 1e-4 * max|ref| for activations,
+    BN statistics, gradients and post-step weights -- compared against the fp64
+    oracle run so the fp32 CPU path's own rounding does not count against us.
+  * bf16 mode (bf16 storage + bf16 tcgen05): max|gpu - ref| <= 3e-2 * max|ref|
+    for activations, 8e-2 for gradients (bf16 has an 8-bit mantissa; errors
+    compound through BN backward).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import executor as OX  # noqa: E402
+from paper_1807_01702_b200 import fusion  # noqa: E402
+from paper_1807_01702_b200 import graph as G  # noqa: E402
+from paper_1807_01702_b200.tensor import Rng  # noqa: E402
+
+TOL = {"f32": (1e-4, 1e-4), "bf16": (3e-2, 8e-2)}
+
+
+def scaled(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-30))
+
+
+def _engine():
+    from paper_1807_01702_b200.engine import Engine
+    return Engine
+
+
+def run_both(g0, level, dtype, seed=1):
+    g, _ = fusion.plan(g0, fusion.parse_level(level))
+    rng = Rng(seed)
+    x = rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0)
+    dy = rng.normal(g.slots[g.outputs[0]].shape)
+    # fp64 oracle on the same (fp32-valued) inputs and parameters
+    g64 = g
+    res = OX.forward(g64, {g.inputs[0]: x.astype(np.float64)})
+    ref = OX.backward(g64, res, {g.outputs[0]: dy.astype(np.float64)})
+    eng = _engine()(g, dtype=dtype, input_grad=True)
+    eng.set_input(x)
+    eng.set_loss_grad(dy)
+    eng.forward()
+    eng.backward()
+    torch.cuda.synchronize()
+    return g, eng, res, ref
+
+
+def check(g, eng, res, ref, dtype, skip_bias=False):
+    ta, tg = TOL[dtype]
+    out = eng.output()
+    assert scaled(out, res.vals[g.outputs[0]]) < ta, "output"
+    grads = eng.param_grads()
+    for k, v in ref.params.items():
+        if skip_bias and k.endswith(".bias"):
+            continue
+        e = scaled(grads[k], v)
+        assert e < tg, f"{k}: {e:.3e}"
+    dx = eng.input_grad_nchw()
+    assert scaled(dx, ref.inputs[g.inputs[0]]) < tg, "input grad"
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("level", ["baseline", "rcf", "rcf+mvf", "bnff", "bnff+icf"])
+def test_block_c1_all_levels(dtype, level):
+    """BASELINE config C1: conv3x3-BN-ReLU-conv1x1, N=8 C=64 32x32."""
+    g0 = G.build_block(8, 64, 32, seed=0, dtype=np.float64 if False else np.float32)
+    g, eng, res, ref = run_both(g0, level, dtype)
+    # conv1 bias gradient is ~0 analytically (BN follows) -> compare absolutely below
+    check(g, eng, res, ref, dtype, skip_bias=True)
+    gb = eng.param_grads()["conv1.bias"]
+    scale = np.max(np.abs(ref.params["mid.conv.bias"]))
+    assert np.max(np.abs(gb - ref.params["conv1.bias"])) < TOL[dtype][1] * scale
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_block_stats_match(dtype):
+    g0 = G.build_block(8, 64, 32, seed=0)
+    g, eng, res, ref = run_both(g0, "bnff", dtype)
+    fcs = next(n for n in g.nodes if n.kind == G.FUSED_CONV_STATS)
+    st = eng.stats_of(fcs.outputs[1])
+    want = res.vals[fcs.outputs[1]]
+    assert scaled(st["mean"], want.mean) < TOL[dtype][0] * 10
+    assert scaled(st["var"], want.var) < TOL[dtype][0] * 10
+
+
+def aligned_densenet(batch=2):
+    return G.ModelSpec("densenet", (3, 3), 16, 4, (batch, 32, 16, 16), "micro", "conv3",
+                       name="densenet-micro-aligned")
+
+
+def tiny_full():
+    return G.ModelSpec("densenet", (2, 2), 8, 4, (2, 3, 32, 32), "full", "conv7-pool", 16,
+                       name="densenet-tiny-full")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("level", ["baseline", "bnff", "bnff+icf"])
+def test_densenet_micro_aligned(dtype, level):
+    g0 = G.build_model(aligned_densenet(), seed=0)
+    g, eng, res, ref = run_both(g0, level, dtype)
+    check(g, eng, res, ref, dtype, skip_bias=True)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("level", ["baseline", "bnff", "bnff+icf"])
+def test_densenet_tiny_full(dtype, level):
+    """7x7/s2 stem (3-channel input padded on device), stem BN/ReLU/pool, transition, head."""
+    g0 = G.build_model(tiny_full(), seed=0)
+    g, eng, res, ref = run_both(g0, level, dtype)
+    check(g, eng, res, ref, dtype, skip_bias=True)
+
+
+@pytest.mark.parametrize("level", ["baseline", "bnff", "bnff+icf"])
+def test_resnet_tiny_strided_f32(level):
+    spec = G.ModelSpec("resnet", (1, 1), input_dims=(2, 8, 8, 8), scale="micro", stem="conv3",
+                       base_channels=16, resnet_stages=((1, 4, 16, 1), (1, 8, 32, 2)))
+    g0 = G.build_model(spec, seed=0)
+    g, eng, res, ref = run_both(g0, level, "f32")
+    check(g, eng, res, ref, "f32", skip_bias=True)
+
+
+def test_reference_golden_direct_f32(golden_dir):
+    """Compare the GPU fp32 path directly with reference-produced fixtures."""
+    import os
+    ref = np.load(os.path.join(golden_dir, "model_densenet-tiny-full_bnff_f32.npz"))
+    g0 = G.build_model(tiny_full(), seed=0)
+    g, _ = fusion.plan(g0, fusion.FusionLevel.BNFF)
+    from paper_1807_01702_b200.engine import Engine
+    eng = Engine(g, dtype="f32", input_grad=True)
+    eng.set_input(ref["x"])
+    eng.set_loss_grad(ref[f"dy_{g.outputs[0]}"])
+    eng.forward()
+    eng.backward()
+    torch.cuda.synchronize()
+    assert scaled(eng.output(), ref[f"out_{g.outputs[0]}"]) < 1e-4
+    grads = eng.param_grads()
+    for key in ref.files:
+        if key.startswith("grad::") and not key.endswith(".bias"):
+            assert scaled(grads[key[6:]], ref[key]) < 1e-4, key
+
+
+def test_sgd_post_step_weights():
+    g0 = G.build_block(2, 64, 16, seed=0)
+    g, _ = fusion.plan(g0, fusion.FusionLevel.BNFF)
+    rng = Rng(1)
+    x = rng.uniform((2, 64, 16, 16), -1.0, 1.0)
+    dy = rng.normal((2, 64, 16, 16))
+    res = OX.forward(g, {g.inputs[0]: x.astype(np.float64)})
+    ref = OX.backward(g, res, {g.outputs[0]: dy.astype(np.float64)})
+    want = OX.sgd({k: np.asarray(v, np.float64) for k, v in g.params.items()}, ref.params, 0.1)
+    from paper_1807_01702_b200.engine import Engine
+    eng = Engine(g, dtype="f32", lr=0.1)
+    eng.set_input(x)
+    eng.set_loss_grad(dy)
+    eng.step()
+    torch.cuda.synchronize()
+    got = eng.params_now()
+    for k in want:
+        if k.endswith(".bias"):
+            continue
+        assert scaled(got[k], want[k]) < 1e-4, k
+
+
+def test_deterministic_bitwise():
+    g0 = G.build_model(aligned_densenet(), seed=0)
+    g, _ = fusion.plan(g0, fusion.FusionLevel.BNFF)
+    rng = Rng(1)
+    x = rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0)
+    dy = rng.normal(g.slots[g.outputs[0]].shape)
+    from paper_1807_01702_b200.engine import Engine
+    outs = []
+    for _ in range(2):
+        eng = Engine(g, dtype="bf16")
+        eng.set_input(x)
+        eng.set_loss_grad(dy)
+        eng.forward()
+        eng.backward()
+        torch.cuda.synchronize()
+        outs.append((eng.output(), eng.gflat.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_cuda_graph_replay_matches_eager():
+    g0 = G.build_block(2, 64, 16, seed=0)
+    g, _ = fusion.plan(g0, fusion.FusionLevel.BNFF)
+    rng = Rng(1)
+    x = rng.uniform((2, 64, 16, 16), -1.0, 1.0)
+    dy = rng.normal((2, 64, 16, 16))
+    from paper_1807_01702_b200.engine import Engine
+    eng = Engine(g, dtype="bf16")
+    eng.set_input(x)
+    eng.set_loss_grad(dy)
+    eng.forward()
+    eng.backward()
+    torch.cuda.synchronize()
+    want = eng.gflat.cpu().numpy().copy()
+    eng.capture()
+    eng.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(eng.gflat.cpu().numpy(), want)

@@ -37,6 +37,14 @@ __device__ uint32_t op_off(const ProbeCfg& c, int mn_major, int mn, int k, int r
   uint32_t atom = mnbyte >> 7;
   uint32_t inb = mnbyte & 127;
   uint32_t atom_bytes = c.K * 128;
+  if (c.layout_mn == kLayoutSW64 || c.layout_mn == kLayoutSW32) {
+    uint32_t rowb = c.layout_mn == kLayoutSW64 ? 64 : 32;
+    uint32_t atomb = rowb * c.K;  // one atom holds all K rows
+    uint32_t a2 = mnbyte / rowb, in2 = mnbyte % rowb;
+    uint32_t off = a2 * atomb + k * rowb + in2;
+    uint32_t mask = c.layout_mn == kLayoutSW64 ? 3 : 1;
+    return off ^ (((off >> 7) & mask) << 4);
+  }
   if (c.layout_mn == kLayoutSW128Base32) {
     // Swizzle<2,5,2>: 32B chunk index ^= (row & 3)
     uint32_t chunk = ((inb >> 5) ^ (k & 3)) & 3;
@@ -77,7 +85,7 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
   }
   fence_proxy_async_smem();
   if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
-  if (tid < 32) tmem_alloc<128>(&tmem_base);
+  if (tid < 32) tmem_alloc<256>(&tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -107,8 +115,9 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
         uint32_t addr = smem_u32(sb) + kb * c.N * 128 + (k0 % kb_elems) * c.esize;
         bd = make_sdesc(addr, 16, 1024, kLayoutSW128);
       } else {
-        uint32_t addr = smem_u32(sb) + k0 * 128;
-        uint32_t lbo = c.K * 128, sbo = c.mn_kgroup * 128;
+        uint32_t rowb = c.layout_mn == kLayoutSW64 ? 64 : (c.layout_mn == kLayoutSW32 ? 32 : 128);
+        uint32_t addr = smem_u32(sb) + k0 * rowb;
+        uint32_t lbo = c.K * rowb, sbo = c.mn_kgroup * rowb;
         if (c.swap_lbo_sbo) { uint32_t t = lbo; lbo = sbo; sbo = t; }
         bd = make_sdesc(addr, lbo, sbo, c.layout_mn);
       }
@@ -129,7 +138,7 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
   }
   tc_fence_before();
   __syncthreads();
-  if (tid < 32) tmem_dealloc<128>(tmem);
+  if (tid < 32) tmem_dealloc<256>(tmem);
 }
 
 static float round_op(float x, int esize) {
@@ -212,5 +221,12 @@ int main() {
     run(nm, {2, 0, 0, 64, 64, 2, 8, 0, s, 1});
   }
   run("bf16 K/K rowshift 8 bo=0", {2, 0, 0, 64, 64, 2, 8, 0, 8, 0});
+  run("bf16 K/MN N32 sw64 (B)", {2, 0, 1, 32, 64, 4, 8, 0, -1, 0});
+  run("bf16 K/MN N32 sw32 (B)", {2, 0, 1, 32, 64, 6, 8, 0, -1, 0});
+  run("bf16 K/MN N16 sw32 (B)", {2, 0, 1, 16, 64, 6, 8, 0, -1, 0});
+  run("tf32 K/MN N32 base32 (B)", {4, 0, 1, 32, 32, 1, 4, 0, -1, 0});
+  run("tf32 MN/MN N128 K64 base32", {4, 1, 1, 128, 64, 1, 4, 0, -1, 0});
+  run("bf16 MN/MN N256 K64", {2, 1, 1, 256, 64, 2, 8, 0, -1, 0});
+  run("bf16 K/K N256 K64", {2, 0, 0, 256, 64, 2, 8, 0, -1, 0});
   return 0;
 }

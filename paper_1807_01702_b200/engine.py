@@ -142,6 +142,7 @@ class Engine:
         self.launch_counts = {"fwd": 0, "bwd": 0, "opt": 0}
         self._cur = None
         self._keep: list = []  # ctypes structs referenced by thunks
+        self._bufs: list = []  # device buffers referenced by thunks
         self._alloc_params()
         self._alloc_acts()
         self._compile_forward()
@@ -150,11 +151,17 @@ class Engine:
         self.graph_exec = None
 
     # ------------------------------------------------------------------ alloc
+    # every device buffer is owned by the engine: thunks hold raw pointers, so a
+    # buffer must never return to the caching allocator while the engine lives
     def _empty(self, shape, dtype=None):
-        return torch.empty(shape, dtype=dtype or self.tdt, device=self.dev)
+        t = torch.empty(shape, dtype=dtype or self.tdt, device=self.dev)
+        self._bufs.append(t)
+        return t
 
     def _zeros(self, shape, dtype=None):
-        return torch.zeros(shape, dtype=dtype or self.tdt, device=self.dev)
+        t = torch.zeros(shape, dtype=dtype or self.tdt, device=self.dev)
+        self._bufs.append(t)
+        return t
 
     def _alloc_params(self):
         g = self.g
@@ -165,7 +172,7 @@ class Engine:
         host = np.concatenate([np.asarray(g.params[k], np.float32).reshape(-1)
                                for k in self.param_names]) if total else np.zeros(0, np.float32)
         self.wflat = torch.from_numpy(host).to(self.dev)
-        self.gflat = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        self.gflat = self._zeros((total,), torch.float32)
         self.poff = {k: (int(offs[i]), int(sizes[i])) for i, k in enumerate(self.param_names)}
         self.packs = {}  # conv name -> (wpack, wpack_t, cin_store)
 
@@ -378,9 +385,10 @@ class Engine:
 
     def _f_Concat(self, node):
         y = self._feature(node.outputs[0])
+        feats = [s for s in node.inputs if self.g.slots[s].kind == "feature"]
         if node.attrs.physical:
             off = 0
-            for s in node.inputs:
+            for s in feats:
                 piece = self.acts[s]
                 c = piece.shape[3]
                 self._emit(self.L.bnff_copy, self.dcode, view_of(piece), view_of(y[..., off:off + c]),
@@ -388,7 +396,7 @@ class Engine:
                 off += c
         else:
             off = 0
-            for s in node.inputs:  # view mode: producers already wrote in place
+            for s in feats:  # view mode: producers already wrote in place
                 piece = self.acts[s]
                 if piece.data_ptr() != y[..., off:].data_ptr():
                     raise StateError(f"{node.name}: view-concat piece {s} not in the block buffer")

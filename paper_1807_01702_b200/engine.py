@@ -57,6 +57,11 @@ def coef_of(a=None, b=None, c=None, d=None, e=None) -> _lib.Coef:
     return _lib.Coef(_ptr(a), _ptr(b), _ptr(c), _ptr(d), _ptr(e))
 
 
+def _nb(*ts) -> int:
+    """bytes of the logical elements of NHWC views (channel slices count their own channels)."""
+    return sum(int(t.numel()) * t.element_size() for t in ts if t is not None)
+
+
 def _vec_of(dtype_code: int) -> int:
     return 8 if dtype_code == _lib.BF16 else 4
 
@@ -233,20 +238,25 @@ class Engine:
         return Stats(*arrs, count=count)
 
     # ------------------------------------------------------------ emit helpers
-    def _emit(self, fn, *args, what=""):
-        """Append a launch thunk calling fn(*args, stream)."""
-        L = self.L
+    def _emit(self, fn, *args, what="", nbytes=0, flops=0, launches=1):
+        """Append a launch thunk calling fn(*args, stream).  ``nbytes``/``flops`` are the
+        launch's ALGORITHMIC HBM bytes / FLOPs (each tensor counted once), used by the
+        live roofline in bench.py."""
         check = _lib.check
         self._keep.append(args)
-        cur = self._cur
 
         def thunk(stream):
             check(fn(*args, stream), what)
-        cur.append(thunk)
+        thunk.what = what
+        thunk.kind = what.split(" ")[0]
+        thunk.nbytes = int(nbytes)
+        thunk.flops = int(flops)
+        thunk.launches = launches  # kernels this C-ABI call launches
+        self._cur.append(thunk)
 
     def _emit_stats_finalize(self, part, tiles, c, count, st: Stats):
         self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
-                   _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize")
+                   _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize", launches=3)
 
     def _pack(self, conv, cin_store):
         key = conv.name
@@ -272,7 +282,7 @@ class Engine:
         tiles = self.L.bnff_sum_tiles(pixels)
         part = self._empty((tiles, 2, x.shape[3]), torch.float32)
         self._emit(self.L.bnff_channel_sums, self.dcode, 0, view_of(x), view_of(x), coef_of(),
-                   _ptr(part), what=f"channel_sums {tag}")
+                   _ptr(part), what=f"channel_sums {tag}", nbytes=_nb(x))
         self._emit_stats_finalize(part, tiles, x.shape[3], pixels, st)
 
     # ---------------------------------------------------------------- forward
@@ -298,7 +308,10 @@ class Engine:
         args = _lib.FpropArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x),
                               view_of(y), _ptr(wp), _ptr(self.param(f"{conv.name}.bias")), pro, cf,
                               _ptr(stat_part))
-        self._emit(self.L.bnff_conv_fprop, C.byref(args), what=f"fprop {node.name}")
+        n_, oh_, ow_, co_ = y.shape
+        flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
+        self._emit(self.L.bnff_conv_fprop, C.byref(args), what=f"fprop {node.name}",
+                   nbytes=_nb(x, y, wp), flops=flops)
         self._keep.append(args)
 
     def _f_Conv2D(self, node):
@@ -329,19 +342,20 @@ class Engine:
             tiles = self.L.bnff_sum_tiles(pixels)
             part = self._empty((tiles, 2, c), torch.float32)
             self._emit(self.L.bnff_centered_var, self.dcode, view_of(x), _ptr(st.mean), _ptr(part),
-                       what="centered_var")
+                       what="centered_var", nbytes=_nb(x))
             self._emit(self.L.bnff_var_finalize, _ptr(part), tiles, c, pixels, _ptr(st.var),
-                       what="var_finalize")
+                       what="var_finalize", launches=2)
         self.node_stats[node.id] = st
         tb = self._bn_tables(st, node.attrs.bn, node.name)
         self.node_tables[node.id] = tb
         self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(y),
-                   coef_of(tb[0], tb[1], tb[2]), 0, what="bn_apply")
+                   coef_of(tb[0], tb[1], tb[2]), 0, what="bn_apply", nbytes=_nb(x, y))
 
     def _f_ReLU(self, node):
         x = self.acts[node.inputs[0]]
         y = self._feature(node.outputs[0])
-        self._emit(self.L.bnff_relu_fwd, self.dcode, view_of(x), view_of(y), what="relu_fwd")
+        self._emit(self.L.bnff_relu_fwd, self.dcode, view_of(x), view_of(y), what="relu_fwd",
+                   nbytes=_nb(x, y))
 
     def _f_FissionSubBN1(self, node):
         x = self.acts[node.inputs[0]]
@@ -358,7 +372,7 @@ class Engine:
         tb = self._bn_tables(st, node.attrs.bn, node.name)
         self.node_tables[node.id] = tb
         self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(y),
-                   coef_of(tb[0], tb[1], tb[2]), 0, what="subbn2")
+                   coef_of(tb[0], tb[1], tb[2]), 0, what="subbn2", nbytes=_nb(x, y))
 
     def _f_FusedNormReluConv(self, node):
         at = node.attrs
@@ -372,7 +386,7 @@ class Engine:
         if self.save_postrelu:
             saved = self._feature(node.outputs[1])
             self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(saved),
-                       coef_of(tb[0], tb[1], tb[2]), 1, what="saved_postrelu")
+                       coef_of(tb[0], tb[1], tb[2]), 1, what="saved_postrelu", nbytes=_nb(x, saved))
         part = None
         if at.emit_stats:
             mt = (y.shape[0] * y.shape[1] * y.shape[2] + 127) // 128
@@ -392,7 +406,7 @@ class Engine:
                 piece = self.acts[s]
                 c = piece.shape[3]
                 self._emit(self.L.bnff_copy, self.dcode, view_of(piece), view_of(y[..., off:off + c]),
-                           what="concat_copy")
+                           what="concat_copy", nbytes=2 * _nb(piece))
                 off += c
         else:
             off = 0
@@ -416,7 +430,10 @@ class Engine:
                             (piece.sum, piece.sumsq, piece.mean, piece.var)):
                 if a[off:off + c].data_ptr() != b.data_ptr():  # not in place: copy (ops.py:128-143)
                     dst = a[off:off + c]
-                    self._cur.append(lambda stream, d=dst, s=b: d.copy_(s))
+                    def _cp(stream, d=dst, s=b):
+                        d.copy_(s)
+                    _cp.what, _cp.kind, _cp.nbytes, _cp.flops = "stats_copy", "stats_copy", 0, 0
+                    self._cur.append(_cp)
             off += c
         self.stats[node.outputs[1]] = st
 
@@ -430,7 +447,8 @@ class Engine:
         y = self._feature(node.outputs[0])
         if not node.attrs.pad_channels and a.shape != b.shape:
             raise ShapeError(f"EltwiseSum operands {tuple(a.shape)} vs {tuple(b.shape)}")
-        self._emit(self.L.bnff_ews_fwd, self.dcode, view_of(a), view_of(b), view_of(y), what="ews")
+        self._emit(self.L.bnff_ews_fwd, self.dcode, view_of(a), view_of(b), view_of(y), what="ews",
+                   nbytes=_nb(a, b, y))
 
     def _f_AvgPool(self, node):
         x = self.acts[node.inputs[0]]
@@ -441,7 +459,7 @@ class Engine:
             tiles = self.L.bnff_sum_tiles(pixels)
             part = self._empty((tiles, 2, y.shape[3]), torch.float32)
         self._emit(self.L.bnff_avgpool_fwd, self.dcode, view_of(x), view_of(y), node.attrs.k,
-                   _ptr(part), what="avgpool")
+                   _ptr(part), what="avgpool", nbytes=_nb(x, y))
         if node.attrs.emit_stats:
             st = self._stats_for(node.outputs[0], y.shape[3], pixels)
             self._emit_stats_finalize(part, tiles, y.shape[3], pixels, st)
@@ -492,7 +510,7 @@ class Engine:
         term = _lib.GradTerm(view_of(gv.dt1), view_of(gv.x), 1, gv.coef())
         self._keep.append(term)
         self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, C.byref(term), 1,
-                   what="bn_dx")
+                   what="bn_dx", nbytes=_nb(gv.dt1, gv.x, out))
         return out
 
     def _incoming(self, sid) -> torch.Tensor:
@@ -512,7 +530,8 @@ class Engine:
         terms = (_lib.GradTerm * 2)(_lib.GradTerm(view_of(cur.t), view_of(cur.t), 0, coef_of()),
                                     _lib.GradTerm(view_of(gv.t), view_of(gv.t), 0, coef_of()))
         self._keep.append(terms)
-        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, 2, what="grad_add")
+        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, 2, what="grad_add",
+                   nbytes=_nb(cur.t, gv.t, out))
         self.grads[sid] = Plain(out)
 
     def _wants_dx(self, sid):
@@ -539,14 +558,24 @@ class Engine:
                                 view_of(dy_x), dy_pro, dy_coef, view_of(dx), view_of(x), _ptr(wt),
                                 dgrad_epi, ecoef, _ptr(part))
             self._keep.append(da)
-            self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}")
+            n_, h_, w_, ci_ = dx.shape
+            flops = 2 * n_ * h_ * w_ * ci_ * conv.kh * conv.kw * dy.shape[3]
+            extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
+            extra += _nb(x) if dgrad_epi != _lib.DG_PLAIN else 0
+            self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
+                       nbytes=_nb(dy, dx, wt) + extra, flops=flops)
         xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
         wa = _lib.WgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x), x_pro,
                             xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
                             _ptr(self.grad(f"{conv.name}.weight")), conv.in_c,
                             _ptr(self.grad(f"{conv.name}.bias")))
         self._keep.append(wa)
-        self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}")
+        n_, oh_, ow_, co_ = dy.shape
+        flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
+        extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
+        self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}",
+                   nbytes=_nb(x, dy) + extra + 4 * conv.out_c * conv.in_c * conv.kh * conv.kw,
+                   flops=flops, launches=4)
         return dx, part
 
     def _b_Conv2D(self, node):
@@ -570,7 +599,7 @@ class Engine:
                    _ptr(self.param(f"{bn.name}.gamma")), C.c_float(bn.eps), _ptr(dg64), _ptr(db64),
                    _ptr(k1), _ptr(k2), _ptr(gg), _ptr(m32), _ptr(i32),
                    _ptr(self.grad(f"{bn.name}.gamma")), _ptr(self.grad(f"{bn.name}.beta")),
-                   what=f"dx_coeffs {tag}")
+                   what=f"dx_coeffs {tag}", launches=3)
         return m32, i32, k1, k2, gg
 
     def _bn_grad_sums(self, x, dy, tables, st, bn, tag):
@@ -580,7 +609,7 @@ class Engine:
         part = self._empty((tiles, 2, x.shape[3]), torch.float32)
         m32, _, _, i32 = tables
         self._emit(self.L.bnff_channel_sums, self.dcode, 1, view_of(x), view_of(dy),
-                   coef_of(m32, i32), _ptr(part), what=f"bn_bwd_sums {tag}")
+                   coef_of(m32, i32), _ptr(part), what=f"bn_bwd_sums {tag}", nbytes=_nb(x, dy))
         return self._dx_coeffs(part, tiles, x.shape[3], pixels, st, bn, tag)
 
     def _b_BatchNorm(self, node):
@@ -598,7 +627,7 @@ class Engine:
         x = self.acts[node.inputs[0]]
         dx = self._fresh_like(x)
         self._emit(self.L.bnff_relu_bwd, self.dcode, view_of(x), view_of(dy), view_of(dx),
-                   what="relu_bwd")
+                   what="relu_bwd", nbytes=_nb(x, dy, dx))
         self._add_grad(node.inputs[0], Plain(dx))
 
     def _b_FissionSubBN1(self, node):
@@ -646,7 +675,7 @@ class Engine:
                 if physical:  # the reference copies each piece (execute.py:438)
                     cp = self._empty(tuple(sl.shape))
                     self._emit(self.L.bnff_copy, self.dcode, view_of(sl), view_of(cp),
-                               what="concat_bwd_copy")
+                               what="concat_bwd_copy", nbytes=2 * _nb(sl))
                     sl = cp
                 piece = Plain(sl)
             self._add_grad(s, piece)
@@ -672,8 +701,9 @@ class Engine:
             else:
                 terms[i] = _lib.GradTerm(view_of(b.dt1), view_of(b.x), 1, b.coef())
         self._keep.append(terms)
+        nb = _nb(out) + sum(_nb(b.t) if isinstance(b, Plain) else _nb(b.dt1, b.x) for b in branches)
         self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, len(branches),
-                   what="split_bwd")
+                   what="split_bwd", nbytes=nb)
         self._add_grad(node.inputs[0], Plain(out))
 
     def _b_EltwiseSum(self, node):
@@ -689,7 +719,7 @@ class Engine:
             return
         dx = self._fresh_like(x)
         self._emit(self.L.bnff_avgpool_bwd, self.dcode, view_of(dy), view_of(dx), node.attrs.k,
-                   what="avgpool_bwd")
+                   what="avgpool_bwd", nbytes=_nb(dy, dx))
         self._add_grad(node.inputs[0], Plain(dx))
 
     # -------------------------------------------------------------- optimizer
@@ -697,7 +727,7 @@ class Engine:
         self._cur = self.opt
         if self.lr != 0.0:
             self._emit(self.L.bnff_sgd, _ptr(self.wflat), _ptr(self.gflat), self.wflat.numel(),
-                       C.c_float(self.lr), what="sgd")
+                       C.c_float(self.lr), what="sgd", nbytes=12 * self.wflat.numel())
         self.repack = []
         self._cur = self.repack
         for name, (wp, wt, cin_s, conv) in self.packs.items():
@@ -759,8 +789,10 @@ class Engine:
         self.backward()
         self.optimizer_step()
 
-    def capture(self):
-        """Capture forward+backward+optimizer as one CUDA graph (replayed by step())."""
+    def capture(self, split: bool = False):
+        """Capture the step as CUDA graph(s).  split=False: one graph forward+backward+
+        SGD+repack (replayed by step()).  split=True: (fwd+bwd graph, optimizer graph),
+        so a data-parallel wrapper can all-reduce the gradient buffer in between."""
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
@@ -768,6 +800,16 @@ class Engine:
             self.backward()  # warm: first launches set kernel attributes
         torch.cuda.current_stream(self.dev).wait_stream(s)
         torch.cuda.synchronize(self.dev)
+        if split:
+            g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1):
+                self.forward()
+                self.backward()
+            with torch.cuda.graph(g2):
+                self._run(self.opt)
+                self._run(self.repack)
+            self.graph_parts = (g1, g2)
+            return g1, g2
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
             self.forward()
@@ -776,6 +818,28 @@ class Engine:
             self._run(self.repack)
         self.graph_exec = gr
         return gr
+
+    def all_thunks(self):
+        return list(self.fwd) + list(self.bwd) + list(self.opt) + list(self.repack)
+
+    def profile_launches(self, reps: int = 3):
+        """Per-launch device time: CUDA events recorded on the launching stream between
+        consecutive launches (a separate pass, not the timed region).  Returns
+        [(thunk, mean_ms)] in launch order."""
+        thunks = self.all_thunks()
+        s = self._stream()
+        stream = torch.cuda.current_stream(self.dev)
+        acc = [0.0] * len(thunks)
+        for _ in range(reps):
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(thunks) + 1)]
+            evs[0].record(stream)
+            for i, t in enumerate(thunks):
+                t(s)
+                evs[i + 1].record(stream)
+            torch.cuda.synchronize(self.dev)
+            for i in range(len(thunks)):
+                acc[i] += evs[i].elapsed_time(evs[i + 1])
+        return [(t, a / reps) for t, a in zip(thunks, acc)]
 
     def num_launches(self) -> int:
         return (self.launch_counts["fwd"] + self.launch_counts["bwd"] + self.launch_counts["opt"])

@@ -73,7 +73,7 @@ typedef struct {
   const float* bias;  /* c_out, nullable */
   int32_t x_pro;      /* BNFF_PRO_NONE / RELU / BN_RELU */
   bnff_coef x_coef;
-  float* stat_part;   /* nullable: sum/sumsq partials [m_tiles][2][c_out] of the stored y */
+  float* stat_part;   /* nullable: sum/sumsq partials [bnff_stat_rows()][2][c_out] of the stored y */
 } bnff_fprop_args;
 
 typedef struct {
@@ -88,7 +88,7 @@ typedef struct {
   const void* wpack_t;/* packed transposed weights [c_in][kh*kw*c_out (padded)] */
   int32_t epi;        /* BNFF_DG_* */
   bnff_coef x_coef;   /* NRC: a = mean, b = scale, c = beta, d = invstd */
-  float* stat_part;   /* NRC: partials [m_tiles][2][c_in] of (sum dt1, sum dt1*xhat) */
+  float* stat_part;   /* NRC: partials [bnff_stat_rows()][2][c_in] of (sum dt1, sum dt1*xhat) */
 } bnff_dgrad_args;
 
 typedef struct {
@@ -111,6 +111,11 @@ typedef struct {
 const char* bnff_last_error(void);
 int bnff_version(void);
 int bnff_device_ok(void); /* 1 if device 0 is sm_100 */
+
+/* Rows of the per-CTA statistics partial buffers written by bnff_conv_fprop /
+ * bnff_conv_dgrad (= number of SMs; one persistent CTA per SM).  The buffer
+ * [rows][2][c] must be zero-initialised once; rows a launch does not use stay 0. */
+int32_t bnff_stat_rows(void);
 
 /* K1: conv2d_fwd (ops.py:151-175), fused_conv_stats_fwd (fused.py:79-100),
  *     fused_norm_relu_conv_fwd (fused.py:103-154), RCF clipped conv (execute.py:167-179) */

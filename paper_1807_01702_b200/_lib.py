@@ -63,6 +63,7 @@ SIGNATURES = {
     "bnff_last_error": (C.c_char_p, []),
     "bnff_version": (C.c_int, []),
     "bnff_device_ok": (C.c_int, []),
+    "bnff_stat_rows": (_I32, []),
     "bnff_conv_fprop": (C.c_int, [C.POINTER(FpropArgs), _P]),
     "bnff_conv_dgrad": (C.c_int, [C.POINTER(DgradArgs), _P]),
     "bnff_wgrad_workspace": (_I64, [_I32] * 8),

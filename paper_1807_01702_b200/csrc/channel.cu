@@ -762,11 +762,20 @@ extern "C" int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, i
 // caller's partial buffer [tiles][2][C] placed after the wgrad workspace.
 namespace bnff {
 __global__ void parts_to_f32_kernel(const float* part, int tiles, int C, float* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0.0;
-  for (int t = 0; t < tiles; ++t) s += (double)part[(long long)t * 2 * C + c];
-  out[c] = (float)s;
+  // 256 threads per 32 channels; 8 warps split the tiles, combined in fixed order
+  __shared__ double sh[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  double acc = 0.0;
+  if (c < C)
+    for (int t = ty; t < tiles; t += 8) acc += (double)part[(long long)t * 2 * C + c];
+  sh[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < C) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += sh[k][tx];
+    out[c] = (float)s;
+  }
 }
 }  // namespace bnff
 
@@ -777,7 +786,7 @@ extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, i
   int rc = bnff_channel_sums(dtype, 2, dy_x, dy, cf, scratch, stream);
   if (rc) return rc;
   const long long pixels = dy.n * dy.h * dy.w;
-  parts_to_f32_kernel<<<(int)((dy.c + 127) / 128), 128, 0, (cudaStream_t)stream>>>(scratch, sum_tiles(pixels),
-                                                                                   (int)dy.c, dbias);
+  parts_to_f32_kernel<<<(int)((dy.c + 31) / 32), 256, 0, (cudaStream_t)stream>>>(scratch, sum_tiles(pixels),
+                                                                                (int)dy.c, dbias);
   return check_launch("dbias");
 }

@@ -34,10 +34,12 @@ enum { MODE_FPROP = 0, MODE_DGRAD = 1, MODE_WGRAD = 2 };
 struct IgParams {
   int M, N;             // GEMM extents
   int nkb;              // total k-blocks
-  int kb_per_split;     // k-blocks per split (blockIdx.z)
+  int kpt;              // k-blocks per tile (WGRAD: per split)
+  int mtiles, ntiles, splits, ntiles_total;
   // geometry (conv input h,w; output oh,ow)
-  int n, h, w, cin, oh, ow, cout, kh, kw, stride, pad;
-  int kred;             // reduction channel count for the K index (fprop: cin, dgrad: cout)
+  int n, h, w, cin, oh, ow, cout, kh, kw, stride, pad, taps;
+  int kred;             // reduction channel count of the K index (fprop: cin, dgrad: cout)
+  FastDiv fd_kred, fd_kw, fd_ohow, fd_ow, fd_hw, fd_w, fd_cin;
   // A operand source
   const void* a_ptr; long long a_rs;
   const void* a_xptr; long long a_xrs;
@@ -171,46 +173,53 @@ __device__ __forceinline__ void warp_colsum16(float (&v)[16], int lane) {
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-template <int MODE, int BN, typename T>
+template <int MODE, int BN, typename T, bool HASX>
 struct IgCfg {
   static constexpr int ESZ = sizeof(T);
-  static constexpr int V = 16 / ESZ;           // elements per chunk
+  static constexpr int V = 16 / ESZ;           // elements per 16-byte chunk
   static constexpr int KB = 128 / ESZ;         // K elements per stage
   static constexpr bool F32 = ESZ == 4;
-  static constexpr int PLANES = F32 ? 2 : 1;
+  static constexpr int PLANES = F32 ? 2 : 1;   // 3xTF32: hi / lo planes
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
-  static constexpr int BUDGET = (F32 ? 200 : 100) * 1024;
+  static constexpr int X_BYTES = HASX ? (MODE == MODE_WGRAD ? B_BYTES : A_BYTES) : 0;
+  static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES) + X_BYTES;
+  static constexpr int BUDGET = 176 * 1024;
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW < 2 ? 2 : (STAGES_RAW > 4 ? 4 : STAGES_RAW);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
-  static constexpr int TCOLS = BN < 32 ? 32 : BN;
-  static constexpr int B_PER = BN / 16;        // B chunks per producer thread
+  static constexpr int STAGES = STAGES_RAW < 2 ? 2 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+  static constexpr int LAG = STAGES >= 4 ? STAGES - 2 : STAGES - 1;  // cp.async groups in flight
+  static constexpr int TCOLS = 2 * BN;         // double-buffered fp32 accumulators
+  static constexpr int B_PER = BN / 16;        // B chunks per producer thread per stage
+  static constexpr int META_BYTES = 2 * STAGES * 128 * 4;
+  static constexpr int SMEM_FIXED = STAGES * STAGE_BYTES + META_BYTES + 1024;
+  static constexpr int THREADS = 288;          // 4 producer, 1 MMA, 4 epilogue warps
 };
 
-template <int MODE, int BN, typename T>
-__global__ void __launch_bounds__(160, 1) igemm_kernel(const IgParams p) {
-  using C = IgCfg<MODE, BN, T>;
-  constexpr int V = C::V, KB = C::KB, STAGES = C::STAGES;
+template <int MODE, int BN, typename T, bool HASX>
+__global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
+  using C = IgCfg<MODE, BN, T, HASX>;
+  constexpr int V = C::V, KB = C::KB, STAGES = C::STAGES, LAG = C::LAG;
   extern __shared__ uint8_t dsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], acc_bar;
+  uint32_t* meta_a = reinterpret_cast<uint32_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint32_t* meta_b = meta_a + STAGES * 128;
+  float* sacc = reinterpret_cast<float*>(meta_b + STAGES * 128);  // [2][stat_ld]
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], accf_bar[2], acce_bar[2];
   __shared__ uint32_t tmem_sh;
   __shared__ float red[4][2][BN];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
-  const int kb0 = blockIdx.z * p.kb_per_split;
-  const int kb1 = min(p.nkb, kb0 + p.kb_per_split);
-  const int nk = kb1 - kb0;
+  const int ntl = (p.ntiles_total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const bool do_stats = MODE != MODE_WGRAD && p.stat_part != nullptr;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 128); mbar_init(&empty_bar[s], 1); }
-    mbar_init(&acc_bar, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], 128); }
     fence_mbar_init();
   }
+  if (do_stats)
+    for (int i = tid; i < 2 * p.stat_ld; i += blockDim.x) sacc[i] = 0.f;
   if (warp == 4) tmem_alloc<C::TCOLS>(&tmem_sh);
   tc_fence_before();
   __syncthreads();
@@ -221,345 +230,394 @@ __global__ void __launch_bounds__(160, 1) igemm_kernel(const IgParams p) {
   auto stage_b = [&](int s, int plane) {
     return smem + s * C::STAGE_BYTES + C::PLANES * C::A_BYTES + plane * C::B_BYTES;
   };
+  auto stage_x = [&](int s) { return smem + s * C::STAGE_BYTES + C::PLANES * (C::A_BYTES + C::B_BYTES); };
 
-  if (warp < 4) {
-    // ===================== producers =====================
-    const int taps = p.kh * p.kw;
-    if constexpr (MODE != MODE_WGRAD) {
-      // A: K-major [128 rows][128B]; thread -> chunk column j, rows r0 + 16*i
-      const int j = tid & 7, r0 = tid >> 3;
-      int pbase[8], ph[8], pw[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = m0 + r0 + 16 * i;
-        if (m < p.M) {
-          if constexpr (MODE == MODE_FPROP) {
-            const int img = m / (p.oh * p.ow), rem = m - img * (p.oh * p.ow);
-            const int oy = rem / p.ow, ox = rem - oy * p.ow;
-            pbase[i] = img * p.h * p.w;
-            ph[i] = oy * p.stride - p.pad;
-            pw[i] = ox * p.stride - p.pad;
-          } else {
-            const int img = m / (p.h * p.w), rem = m - img * (p.h * p.w);
-            const int y = rem / p.w, x = rem - y * p.w;
-            pbase[i] = img * p.oh * p.ow;
-            ph[i] = y + p.pad;
-            pw[i] = x + p.pad;
-          }
-        } else {
-          pbase[i] = -1; ph[i] = 0; pw[i] = 0;
-        }
-      }
-      const int bj = tid & 7, br0 = tid >> 3;
-      for (int it = 0; it < nk; ++it) {
-        const int kb = kb0 + it, s = it % STAGES;
-        // ---- gather A ----
-        const int kidx = kb * KB + j * V;
-        const int tap = kidx / p.kred, cc = kidx - tap * p.kred;
-        const int ty = tap / p.kw, tx = tap - ty * p.kw;
-        const bool kval = tap < taps;
-        Chunk<T> ra[8], rx[8];
-        unsigned okmask = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          bool ok = kval && pbase[i] >= 0;
-          long long pix = 0;
-          if constexpr (MODE == MODE_FPROP) {
-            const int iy = ph[i] + ty, ix = pw[i] + tx;
-            ok = ok && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-            pix = (long long)pbase[i] + (long long)iy * p.w + ix;
-          } else {
-            int ay = ph[i] - ty, ax = pw[i] - tx;
-            if (p.stride > 1) {
-              ok = ok && ay >= 0 && ax >= 0 && (ay % p.stride) == 0 && (ax % p.stride) == 0;
-              ay /= p.stride;
-              ax /= p.stride;
-            }
-            ok = ok && ay >= 0 && ay < p.oh && ax >= 0 && ax < p.ow;
-            pix = (long long)pbase[i] + (long long)ay * p.ow + ax;
-          }
-          if (ok) {
-            ra[i].load(reinterpret_cast<const T*>(p.a_ptr) + pix * p.a_rs + cc);
-            if (p.a_pro == BNFF_PRO_BN_DX)
-              rx[i].load(reinterpret_cast<const T*>(p.a_xptr) + pix * p.a_xrs + cc);
-          } else {
-            ra[i].zero();
-            rx[i].raw = ra[i].raw;
-          }
-          okmask |= (ok ? 1u : 0u) << i;
-        }
-        // ---- gather B (packed weights, K-major rows of b_rs elements) ----
-        Chunk<T> rb[C::B_PER];
-#pragma unroll
-        for (int i = 0; i < C::B_PER; ++i) {
-          const int row = n0 + br0 + 16 * i;
-          if (row < p.N)
-            rb[i].load(reinterpret_cast<const T*>(p.b_ptr) + (long long)row * p.b_rs + kb * KB + bj * V);
-          else
-            rb[i].zero();
-        }
-        if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-        uint8_t* a0 = stage_a(s, 0);
-        uint8_t* a1 = stage_a(s, 1);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float f[V], xf[V];
-          ra[i].to_float(f);
-          if (p.a_pro == BNFF_PRO_BN_DX) rx[i].to_float(xf);
-          if ((okmask >> i) & 1u) {
-            apply_pro<V>(p.a_pro, f, xf, cc, p.a_coef);
-          } else {
-#pragma unroll
-            for (int q = 0; q < V; ++q) f[q] = 0.f;
-          }
-          st_chunk<T, V>(a0, a1, kmajor_sw128_off(r0 + 16 * i, j * 16), f);
-        }
-        uint8_t* b0 = stage_b(s, 0);
-        uint8_t* b1 = stage_b(s, 1);
-#pragma unroll
-        for (int i = 0; i < C::B_PER; ++i) {
-          float f[V];
-          rb[i].to_float(f);
-          st_chunk<T, V>(b0, b1, kmajor_sw128_off(br0 + 16 * i, bj * 16), f);
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&full_bar[s]);
-      }
+  // tile index -> (m0, n0, kb0)
+  auto tile_of = [&](int lt, int& m0, int& n0, int& kb0) {
+    const int t = (int)blockIdx.x + lt * (int)gridDim.x;
+    const int mt = t % p.mtiles;
+    const int r = t / p.mtiles;
+    m0 = mt * 128;
+    if (MODE == MODE_WGRAD) {
+      n0 = (r % p.ntiles) * BN;
+      kb0 = (r / p.ntiles) * p.kpt;
     } else {
-      // ===================== WGRAD producers (MN-major) =====================
-      // A: KB pixel rows x 128 (tap,ci) elements; thread -> M chunk column ja
-      constexpr int CPR_A = 128 / V;            // chunks per K-row (16 bf16 / 32 f32)
-      constexpr int RSTEP_A = 128 / CPR_A;      // 8 / 4
-      const int ja = tid % CPR_A, ra0 = tid / CPR_A;
-      const int midx = m0 + ja * V;
-      const int a_tap = midx / p.cin, a_ci = midx - a_tap * p.cin;
-      const int a_ty = a_tap / p.kw, a_tx = a_tap - a_ty * p.kw;
-      const bool a_mval = midx < p.M;
-      constexpr int CPR_B = BN / V;
-      constexpr int RSTEP_B = 128 / CPR_B;
-      const int jb = tid % CPR_B, rb0 = tid / CPR_B;
-      const int co = n0 + jb * V;
-      const bool b_nval = co < p.N;
-      const int npix = p.n * p.oh * p.ow;
-      for (int it = 0; it < nk; ++it) {
-        const int kb = kb0 + it, s = it % STAGES;
-        Chunk<T> ra[8];
-        unsigned okmask = 0;
+      n0 = r * BN;
+      kb0 = 0;
+    }
+  };
+
+  if (warp < 4) {
+    // ======================= producers (cp.async) =======================
+    const int G = ntl * p.kpt;
+    // per-tile state
+    int pbase[8], ph[8], pw[8];
+    int cur_lt = -1, m0 = 0, n0 = 0, kb0 = 0;
+    // WGRAD fixed per-tile operand columns
+    constexpr int CPR_A = 128 / V, RSTEP_A = 128 / CPR_A;
+    constexpr int CPR_B = BN / V, RSTEP_B = 128 / CPR_B;
+    const int ja = tid % CPR_A, ra0 = tid / CPR_A;
+    const int jb = tid % CPR_B, rb0 = tid / CPR_B;
+    int a_ci = 0, a_ty = 0, a_tx = 0;
+    bool a_mval = false;
+    const int j = tid & 7, r0 = tid >> 3;  // K-major mapping (FPROP/DGRAD A, B weights)
+    const uint32_t npix = (uint32_t)(p.n * p.oh * p.ow);
+    const bool xa = HASX && MODE == MODE_DGRAD && p.a_pro == BNFF_PRO_BN_DX;
+    const bool xb = HASX && MODE == MODE_WGRAD && p.b_pro == BNFF_PRO_BN_DX;
+    const bool need_ta = C::F32 || p.a_pro != BNFF_PRO_NONE;
+    const bool need_tb = C::F32 || (MODE == MODE_WGRAD && p.b_pro != BNFF_PRO_NONE);
+
+    for (int g = 0; g < G + LAG; ++g) {
+      if (g < G) {
+        const int lt = g / p.kpt, kk = g - lt * p.kpt;
+        const int s = g % STAGES;
+        if (lt != cur_lt) {
+          cur_lt = lt;
+          tile_of(lt, m0, n0, kb0);
+          if constexpr (MODE != MODE_WGRAD) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int pix = kb * KB + ra0 + RSTEP_A * i;
-          bool ok = a_mval && pix < npix;
-          long long src = 0;
-          if (ok) {
-            const int img = pix / (p.oh * p.ow), rem = pix - img * (p.oh * p.ow);
-            const int oy = rem / p.ow, ox = rem - oy * p.ow;
-            const int iy = oy * p.stride - p.pad + a_ty, ix = ox * p.stride - p.pad + a_tx;
-            ok = iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-            src = ((long long)img * p.h + iy) * p.w + ix;
-          }
-          if (ok) ra[i].load(reinterpret_cast<const T*>(p.a_ptr) + src * p.a_rs + a_ci);
-          else ra[i].zero();
-          okmask |= (ok ? 1u : 0u) << i;
-        }
-        Chunk<T> rb[C::B_PER], rbx[C::B_PER];
-#pragma unroll
-        for (int i = 0; i < C::B_PER; ++i) {
-          const int pix = kb * KB + rb0 + RSTEP_B * i;
-          if (b_nval && pix < npix) {
-            rb[i].load(reinterpret_cast<const T*>(p.b_ptr) + (long long)pix * p.b_rs + co);
-            if (p.b_pro == BNFF_PRO_BN_DX)
-              rbx[i].load(reinterpret_cast<const T*>(p.b_xptr) + (long long)pix * p.b_xrs + co);
+            for (int i = 0; i < 8; ++i) {
+              const int m = m0 + r0 + 16 * i;
+              if (m < p.M) {
+                if constexpr (MODE == MODE_FPROP) {
+                  const uint32_t img = fdiv(m, p.fd_ohow), rem = m - img * (p.oh * p.ow);
+                  const uint32_t oy = fdiv(rem, p.fd_ow), ox = rem - oy * p.ow;
+                  pbase[i] = img * p.h * p.w;
+                  ph[i] = oy * p.stride - p.pad;
+                  pw[i] = ox * p.stride - p.pad;
+                } else {
+                  const uint32_t img = fdiv(m, p.fd_hw), rem = m - img * (p.h * p.w);
+                  const uint32_t y = fdiv(rem, p.fd_w), x = rem - y * p.w;
+                  pbase[i] = img * p.oh * p.ow;
+                  ph[i] = y + p.pad;
+                  pw[i] = x + p.pad;
+                }
+              } else {
+                pbase[i] = -1; ph[i] = 0; pw[i] = 0;
+              }
+            }
           } else {
-            rb[i].zero();
-            rbx[i].raw = rb[i].raw;
+            const int midx = m0 + ja * V;
+            a_mval = midx < p.M;
+            const int tap = fdiv(midx, p.fd_cin);
+            a_ci = midx - tap * p.cin;
+            a_ty = fdiv(tap, p.fd_kw);
+            a_tx = tap - a_ty * p.kw;
           }
         }
-        if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-        uint8_t* a0 = stage_a(s, 0);
-        uint8_t* a1 = stage_a(s, 1);
+        if (g >= STAGES) mbar_wait(&empty_bar[s], ((g / STAGES) - 1) & 1);
+        const int kb = kb0 + kk;
+        const uint32_t abase = smem_u32(stage_a(s, 0)), bbase = smem_u32(stage_b(s, 0));
+        const uint32_t xbase = smem_u32(stage_x(s));
+        if constexpr (MODE != MODE_WGRAD) {
+          const int kidx = kb * KB + j * V;
+          const int tap = fdiv(kidx, p.fd_kred), cc = kidx - tap * p.kred;
+          const int ty = fdiv(tap, p.fd_kw), tx = tap - ty * p.kw;
+          const bool kval = tap < p.taps;
+          uint32_t mask = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float f[V], xf[V];
-          ra[i].to_float(f);
-          if ((okmask >> i) & 1u) {
-            apply_pro<V>(p.a_pro, f, xf, a_ci, p.a_coef);
-          } else {
-#pragma unroll
-            for (int q = 0; q < V; ++q) f[q] = 0.f;
+          for (int i = 0; i < 8; ++i) {
+            bool ok = kval && pbase[i] >= 0;
+            long long pix = 0;
+            if constexpr (MODE == MODE_FPROP) {
+              const int iy = ph[i] + ty, ix = pw[i] + tx;
+              ok = ok && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
+              pix = (long long)pbase[i] + (long long)iy * p.w + ix;
+            } else {
+              int ay = ph[i] - ty, ax = pw[i] - tx;
+              if (p.stride > 1) {
+                ok = ok && ay >= 0 && ax >= 0 && (ay % p.stride) == 0 && (ax % p.stride) == 0;
+                ay /= p.stride;
+                ax /= p.stride;
+              }
+              ok = ok && ay >= 0 && ay < p.oh && ax >= 0 && ax < p.ow;
+              pix = (long long)pbase[i] + (long long)ay * p.ow + ax;
+            }
+            const uint32_t off = kmajor_sw128_off(r0 + 16 * i, j * 16);
+            const T* src = reinterpret_cast<const T*>(p.a_ptr) + (ok ? pix * p.a_rs + cc : 0);
+            cp_async16(abase + off, src, ok ? 16u : 0u);
+            if (xa) {
+              const T* xs = reinterpret_cast<const T*>(p.a_xptr) + (ok ? pix * p.a_xrs + cc : 0);
+              cp_async16(xbase + off, xs, ok ? 16u : 0u);
+            }
+            mask |= (ok ? 1u : 0u) << i;
           }
-          st_chunk<T, V>(a0, a1, mn_off<T, 128, KB>(ra0 + RSTEP_A * i, ja * V), f);
+          meta_a[s * 128 + tid] = ((uint32_t)cc << 8) | mask;
+#pragma unroll
+          for (int i = 0; i < C::B_PER; ++i) {
+            const int row = n0 + r0 + 16 * i;
+            const bool ok = row < p.N;
+            const T* src = reinterpret_cast<const T*>(p.b_ptr) +
+                           (ok ? (long long)row * p.b_rs + kb * KB + j * V : 0);
+            cp_async16(bbase + kmajor_sw128_off(r0 + 16 * i, j * 16), src, ok ? 16u : 0u);
+          }
+        } else {
+          uint32_t mask = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t pix = (uint32_t)(kb * KB + ra0 + RSTEP_A * i);
+            bool ok = a_mval && pix < npix && kb < p.nkb;
+            long long src = 0;
+            if (ok) {
+              const uint32_t img = fdiv(pix, p.fd_ohow), rem = pix - img * (p.oh * p.ow);
+              const uint32_t oy = fdiv(rem, p.fd_ow), ox = rem - oy * p.ow;
+              const int iy = (int)oy * p.stride - p.pad + a_ty, ix = (int)ox * p.stride - p.pad + a_tx;
+              ok = iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
+              src = ((long long)img * p.h + iy) * p.w + ix;
+            }
+            const T* sp = reinterpret_cast<const T*>(p.a_ptr) + (ok ? src * p.a_rs + a_ci : 0);
+            cp_async16(abase + mn_off<T, 128, KB>(ra0 + RSTEP_A * i, ja * V), sp, ok ? 16u : 0u);
+            mask |= (ok ? 1u : 0u) << i;
+          }
+          meta_a[s * 128 + tid] = ((uint32_t)a_ci << 8) | mask;
+          const int co = n0 + jb * V;
+          uint32_t maskb = 0;
+#pragma unroll
+          for (int i = 0; i < C::B_PER; ++i) {
+            const uint32_t pix = (uint32_t)(kb * KB + rb0 + RSTEP_B * i);
+            const bool ok = co < p.N && pix < npix && kb < p.nkb;
+            const uint32_t off = mn_off<T, BN, KB>(rb0 + RSTEP_B * i, jb * V);
+            const T* sp = reinterpret_cast<const T*>(p.b_ptr) + (ok ? (long long)pix * p.b_rs + co : 0);
+            cp_async16(bbase + off, sp, ok ? 16u : 0u);
+            if (xb) {
+              const T* xs = reinterpret_cast<const T*>(p.b_xptr) + (ok ? (long long)pix * p.b_xrs + co : 0);
+              cp_async16(xbase + off, xs, ok ? 16u : 0u);
+            }
+            maskb |= (ok ? 1u : 0u) << i;
+          }
+          meta_b[s * 128 + tid] = ((uint32_t)co << 8) | maskb;
         }
-        uint8_t* b0 = stage_b(s, 0);
-        uint8_t* b1 = stage_b(s, 1);
+      }
+      cp_async_commit();
+      if (g >= LAG) {
+        const int gg = g - LAG;
+        const int s2 = gg % STAGES;
+        cp_async_wait<LAG>();
+        if (need_ta) {
+          const uint32_t ma = meta_a[s2 * 128 + tid];
+          const int cc = (int)(ma >> 8);
+          uint8_t* a0 = stage_a(s2, 0);
+          uint8_t* a1 = stage_a(s2, 1);
+          uint8_t* xs = stage_x(s2);
 #pragma unroll
-        for (int i = 0; i < C::B_PER; ++i) {
-          const int pix = kb * KB + rb0 + RSTEP_B * i;
-          float f[V], xf[V];
-          rb[i].to_float(f);
-          if (p.b_pro == BNFF_PRO_BN_DX) rbx[i].to_float(xf);
-          if (b_nval && pix < npix) {
-            apply_pro<V>(p.b_pro, f, xf, co, p.b_coef);
-          } else {
-#pragma unroll
-            for (int q = 0; q < V; ++q) f[q] = 0.f;
+          for (int i = 0; i < 8; ++i) {
+            uint32_t off;
+            if constexpr (MODE == MODE_WGRAD) off = mn_off<T, 128, KB>(ra0 + RSTEP_A * i, ja * V);
+            else off = kmajor_sw128_off(r0 + 16 * i, j * 16);
+            Chunk<T> ch, cx;
+            ch.raw = *reinterpret_cast<const decltype(ch.raw)*>(a0 + off);
+            float f[V], xf[V];
+            ch.to_float(f);
+            if (xa) {
+              cx.raw = *reinterpret_cast<const decltype(cx.raw)*>(xs + off);
+              cx.to_float(xf);
+            }
+            if ((ma >> i) & 1u) apply_pro<V>(p.a_pro, f, xf, cc, p.a_coef);
+            st_chunk<T, V>(a0, a1, off, f);
           }
-          st_chunk<T, V>(b0, b1, mn_off<T, BN, KB>(rb0 + RSTEP_B * i, jb * V), f);
+        }
+        if (need_tb) {
+          uint8_t* b0 = stage_b(s2, 0);
+          uint8_t* b1 = stage_b(s2, 1);
+          uint8_t* xs = stage_x(s2);
+          const uint32_t mb = MODE == MODE_WGRAD ? meta_b[s2 * 128 + tid] : 0u;
+          const int co = (int)(mb >> 8);
+#pragma unroll
+          for (int i = 0; i < C::B_PER; ++i) {
+            uint32_t off;
+            if constexpr (MODE == MODE_WGRAD) off = mn_off<T, BN, KB>(rb0 + RSTEP_B * i, jb * V);
+            else off = kmajor_sw128_off(r0 + 16 * i, j * 16);
+            Chunk<T> ch, cx;
+            ch.raw = *reinterpret_cast<const decltype(ch.raw)*>(b0 + off);
+            float f[V], xf[V];
+            ch.to_float(f);
+            if (MODE == MODE_WGRAD && ((mb >> i) & 1u)) {
+              if (xb) {
+                cx.raw = *reinterpret_cast<const decltype(cx.raw)*>(xs + off);
+                cx.to_float(xf);
+              }
+              apply_pro<V>(p.b_pro, f, xf, co, p.b_coef);
+            }
+            st_chunk<T, V>(b0, b1, off, f);
+          }
         }
         fence_proxy_async_smem();
-        mbar_arrive(&full_bar[s]);
+        mbar_arrive(&full_bar[s2]);
       }
     }
-  } else if (lane == 0) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t fmt = C::F32 ? kFmtTF32 : kFmtBF16;
-    constexpr uint32_t mn = MODE == MODE_WGRAD ? 1u : 0u;
-    constexpr uint32_t idesc = make_idesc(128, BN, fmt, mn, mn);
-    for (int it = 0; it < nk; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full_bar[s], (it / STAGES) & 1);
-      tc_fence_after();
-      const uint32_t abase0 = smem_u32(stage_a(s, 0)), bbase0 = smem_u32(stage_b(s, 0));
-      const uint32_t abase1 = smem_u32(stage_a(s, 1)), bbase1 = smem_u32(stage_b(s, 1));
+  } else if (warp == 4) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t fmt = C::F32 ? kFmtTF32 : kFmtBF16;
+      constexpr uint32_t mn = MODE == MODE_WGRAD ? 1u : 0u;
+      constexpr uint32_t idesc = make_idesc(128, BN, fmt, mn, mn);
+      int g = 0;
+      for (int lt = 0; lt < ntl; ++lt) {
+        const int slot = lt & 1;
+        if (lt >= 2) mbar_wait(&acce_bar[slot], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + slot * BN;
+        for (int kk = 0; kk < p.kpt; ++kk, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full_bar[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(stage_a(s, 0)), b0 = smem_u32(stage_b(s, 0));
+          const uint32_t a1 = smem_u32(stage_a(s, 1)), b1 = smem_u32(stage_b(s, 1));
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        uint64_t ad0, bd0, ad1, bd1;
-        if constexpr (MODE == MODE_WGRAD) {
-          ad0 = mn_desc<T, 128, KB>(abase0, kk);
-          bd0 = mn_desc<T, BN, KB>(bbase0, kk);
-          ad1 = mn_desc<T, 128, KB>(abase1, kk);
-          bd1 = mn_desc<T, BN, KB>(bbase1, kk);
-        } else {
-          ad0 = make_sdesc(abase0 + kk * 32, 16, 1024, kLayoutSW128);
-          bd0 = make_sdesc(bbase0 + kk * 32, 16, 1024, kLayoutSW128);
-          ad1 = make_sdesc(abase1 + kk * 32, 16, 1024, kLayoutSW128);
-          bd1 = make_sdesc(bbase1 + kk * 32, 16, 1024, kLayoutSW128);
-        }
-        const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-        if constexpr (C::F32) {
-          umma_tf32(tmem, ad0, bd0, idesc, acc);  // hi*hi
-          umma_tf32(tmem, ad0, bd1, idesc, 1u);   // hi*lo
-          umma_tf32(tmem, ad1, bd0, idesc, 1u);   // lo*hi
-        } else {
-          umma_f16(tmem, ad0, bd0, idesc, acc);
-        }
-      }
-      umma_commit(&empty_bar[s]);
-    }
-    umma_commit(&acc_bar);
-  }
-  __syncwarp();
-
-  // ===================== epilogue (warps 0-3) =====================
-  if (warp < 4) {
-    mbar_wait(&acc_bar, 0);
-    tc_fence_after();
-    const int row = warp * 32 + lane;
-    const int gm = m0 + row;
-    const bool rval = gm < p.M;
-    const bool do_stats = p.stat_part != nullptr;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-      tmem_ld_wait();
-      const int gc0 = n0 + c0;
-      if constexpr (MODE == MODE_WGRAD) {
-        if (rval) {
-          float* dst = reinterpret_cast<float*>(p.c_ptr) +
-                       ((long long)blockIdx.z * p.M + gm) * (long long)p.c_rs + gc0;
-#pragma unroll
-          for (int q = 0; q < 16; q += 4) {
-            if (gc0 + q < p.N)
-              *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
-          }
-        }
-      } else {
-        float s1[16], s2[16];
-        float xv[16];
-        const bool need_x = MODE == MODE_DGRAD && p.epi != BNFF_DG_PLAIN;
-        if (need_x) {
-#pragma unroll
-          for (int q = 0; q < 16; q += V) {
-            Chunk<T> ch;
-            if (rval && gc0 + q < p.N)
-              ch.load(reinterpret_cast<const T*>(p.e_xptr) + (long long)gm * p.e_xrs + gc0 + q);
-            else
-              ch.zero();
-            float f[V];
-            ch.to_float(f);
-#pragma unroll
-            for (int u = 0; u < V; ++u) xv[q + u] = f[u];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int gc = gc0 + q;
-          const bool cval = gc < p.N;
-          float val = v[q];
-          if constexpr (MODE == MODE_FPROP) {
-            if (p.bias != nullptr && cval) val = __fadd_rn(val, __ldg(p.bias + gc));
-          } else {
-            if (p.epi == BNFF_DG_CLIP) {
-              val = xv[q] > 0.f ? val : 0.f;
-            } else if (p.epi == BNFF_DG_NRC && cval) {
-              float t = __fmul_rn(__fsub_rn(xv[q], __ldg(p.e_coef.a + gc)), __ldg(p.e_coef.b + gc));
-              t = __fadd_rn(t, __ldg(p.e_coef.c + gc));
-              val = t > 0.f ? val : 0.f;
+          for (int q = 0; q < 4; ++q) {
+            uint64_t ad0, bd0, ad1, bd1;
+            if constexpr (MODE == MODE_WGRAD) {
+              ad0 = mn_desc<T, 128, KB>(a0, q);
+              bd0 = mn_desc<T, BN, KB>(b0, q);
+              ad1 = mn_desc<T, 128, KB>(a1, q);
+              bd1 = mn_desc<T, BN, KB>(b1, q);
+            } else {
+              ad0 = make_sdesc(a0 + q * 32, 16, 1024, kLayoutSW128);
+              bd0 = make_sdesc(b0 + q * 32, 16, 1024, kLayoutSW128);
+              ad1 = make_sdesc(a1 + q * 32, 16, 1024, kLayoutSW128);
+              bd1 = make_sdesc(b1 + q * 32, 16, 1024, kLayoutSW128);
+            }
+            const uint32_t acc = (kk > 0 || q > 0) ? 1u : 0u;
+            if constexpr (C::F32) {
+              umma_tf32(dt, ad0, bd0, idesc, acc);
+              umma_tf32(dt, ad0, bd1, idesc, 1u);
+              umma_tf32(dt, ad1, bd0, idesc, 1u);
+            } else {
+              umma_f16(dt, ad0, bd0, idesc, acc);
             }
           }
-          // round to storage precision; statistics use the stored value
-          float r;
-          if constexpr (sizeof(T) == 2) r = __bfloat162float(__float2bfloat16_rn(val));
-          else r = val;
-          v[q] = r;
-          const bool sv = rval && cval;
-          if constexpr (MODE == MODE_FPROP) {
-            s1[q] = sv ? r : 0.f;
-            s2[q] = sv ? r * r : 0.f;
-          } else {
-            float xh = 0.f;
-            if (p.epi == BNFF_DG_NRC && cval)
-              xh = __fmul_rn(__fsub_rn(xv[q], __ldg(p.e_coef.a + gc)), __ldg(p.e_coef.d + gc));
-            s1[q] = sv ? r : 0.f;
-            s2[q] = sv ? r * xh : 0.f;
-          }
+          umma_commit(&empty_bar[s]);
         }
-        if (rval) {
-          T* dst = reinterpret_cast<T*>(p.c_ptr) + (long long)gm * p.c_rs + gc0;
+        umma_commit(&accf_bar[slot]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= epilogue (warps 5-8) =======================
+    const int ew = warp - 5;          // epilogue warp index 0..3
+    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+    const int et = tid - 160;         // 0..127
+    for (int lt = 0; lt < ntl; ++lt) {
+      const int slot = lt & 1;
+      int m0, n0, kb0;
+      tile_of(lt, m0, n0, kb0);
+      mbar_wait(&accf_bar[slot], (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = quad * 32 + lane;
+      const int gm = m0 + row;
+      const bool rval = gm < p.M;
+      const uint32_t tbase = tmem + slot * BN + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + c0, v);
+        tmem_ld_wait();
+        const int gc0 = n0 + c0;
+        if constexpr (MODE == MODE_WGRAD) {
+          if (rval) {
+            const int split = kb0 / p.kpt;
+            float* dst = reinterpret_cast<float*>(p.c_ptr) +
+                         ((long long)split * p.M + gm) * (long long)p.c_rs + gc0;
 #pragma unroll
-          for (int q = 0; q < 16; q += V) {
-            if (gc0 + q < p.N) {
-              if constexpr (sizeof(T) == 2) {
-                uint4 o;
-                o.x = pack_bf16(v[q], v[q + 1]); o.y = pack_bf16(v[q + 2], v[q + 3]);
-                o.z = pack_bf16(v[q + 4], v[q + 5]); o.w = pack_bf16(v[q + 6], v[q + 7]);
-                *reinterpret_cast<uint4*>(dst + q) = o;
-              } else {
+            for (int q = 0; q < 16; q += 4)
+              if (gc0 + q < p.N)
                 *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+          }
+        } else {
+          float s1[16], s2[16], xv[16];
+          const bool need_x = MODE == MODE_DGRAD && p.epi != BNFF_DG_PLAIN;
+          if (need_x) {
+#pragma unroll
+            for (int q = 0; q < 16; q += V) {
+              Chunk<T> ch;
+              if (rval && gc0 + q < p.N)
+                ch.load(reinterpret_cast<const T*>(p.e_xptr) + (long long)gm * p.e_xrs + gc0 + q);
+              else
+                ch.zero();
+              float f[V];
+              ch.to_float(f);
+#pragma unroll
+              for (int u = 0; u < V; ++u) xv[q + u] = f[u];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int gc = gc0 + q;
+            const bool cval = gc < p.N;
+            float val = v[q];
+            if constexpr (MODE == MODE_FPROP) {
+              if (p.bias != nullptr && cval) val = __fadd_rn(val, __ldg(p.bias + gc));
+            } else {
+              if (p.epi == BNFF_DG_CLIP) {
+                val = xv[q] > 0.f ? val : 0.f;
+              } else if (p.epi == BNFF_DG_NRC && cval) {
+                float t = __fmul_rn(__fsub_rn(xv[q], __ldg(p.e_coef.a + gc)), __ldg(p.e_coef.b + gc));
+                t = __fadd_rn(t, __ldg(p.e_coef.c + gc));
+                val = t > 0.f ? val : 0.f;
+              }
+            }
+            float r;
+            if constexpr (sizeof(T) == 2) r = __bfloat162float(__float2bfloat16_rn(val));
+            else r = val;
+            v[q] = r;
+            const bool sv = rval && cval;
+            if constexpr (MODE == MODE_FPROP) {
+              s1[q] = sv ? r : 0.f;
+              s2[q] = sv ? r * r : 0.f;
+            } else {
+              float xh = 0.f;
+              if (p.epi == BNFF_DG_NRC && cval)
+                xh = __fmul_rn(__fsub_rn(xv[q], __ldg(p.e_coef.a + gc)), __ldg(p.e_coef.d + gc));
+              s1[q] = sv ? r : 0.f;
+              s2[q] = sv ? r * xh : 0.f;
+            }
+          }
+          if (rval) {
+            T* dst = reinterpret_cast<T*>(p.c_ptr) + (long long)gm * p.c_rs + gc0;
+#pragma unroll
+            for (int q = 0; q < 16; q += V) {
+              if (gc0 + q < p.N) {
+                if constexpr (sizeof(T) == 2) {
+                  uint4 o;
+                  o.x = pack_bf16(v[q], v[q + 1]); o.y = pack_bf16(v[q + 2], v[q + 3]);
+                  o.z = pack_bf16(v[q + 4], v[q + 5]); o.w = pack_bf16(v[q + 6], v[q + 7]);
+                  *reinterpret_cast<uint4*>(dst + q) = o;
+                } else {
+                  *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+                }
               }
             }
           }
-        }
-        if (do_stats) {
-          warp_colsum16(s1, lane);
-          warp_colsum16(s2, lane);
-          if ((lane & 1) == 0) {
-            red[warp][0][c0 + (lane >> 1)] = s1[0];
-            red[warp][1][c0 + (lane >> 1)] = s2[0];
+          if (do_stats) {
+            warp_colsum16(s1, lane);
+            warp_colsum16(s2, lane);
+            if ((lane & 1) == 0) {
+              red[ew][0][c0 + (lane >> 1)] = s1[0];
+              red[ew][1][c0 + (lane >> 1)] = s2[0];
+            }
           }
         }
       }
-    }
-    if (MODE != MODE_WGRAD && do_stats) {
-      named_bar(1, 128);
-      for (int c = tid; c < BN; c += 128) {
-        const int gc = n0 + c;
-        if (gc < p.N) {
-          const float a = ((red[0][0][c] + red[1][0][c]) + red[2][0][c]) + red[3][0][c];
-          const float b = ((red[0][1][c] + red[1][1][c]) + red[2][1][c]) + red[3][1][c];
-          p.stat_part[((long long)blockIdx.x * 2 + 0) * p.stat_ld + gc] = a;
-          p.stat_part[((long long)blockIdx.x * 2 + 1) * p.stat_ld + gc] = b;
+      // accumulator slot drained -> MMA may reuse it
+      tc_fence_before();
+      mbar_arrive(&acce_bar[slot]);
+      if (do_stats) {
+        named_bar(1, 128);
+        for (int c = et; c < BN; c += 128) {
+          const int gc = n0 + c;
+          if (gc < p.N) {
+            sacc[gc] += ((red[0][0][c] + red[1][0][c]) + red[2][0][c]) + red[3][0][c];
+            sacc[p.stat_ld + gc] += ((red[0][1][c] + red[1][1][c]) + red[2][1][c]) + red[3][1][c];
+          }
         }
+        named_bar(2, 128);
+      }
+    }
+    if (do_stats) {
+      // one partial row per CTA (fixed tile->CTA assignment => deterministic)
+      for (int c = et; c < p.stat_ld; c += 128) {
+        p.stat_part[((long long)blockIdx.x * 2 + 0) * p.stat_ld + c] = sacc[c];
+        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.stat_ld + c] = sacc[p.stat_ld + c];
       }
     }
   }
@@ -571,35 +629,62 @@ __global__ void __launch_bounds__(160, 1) igemm_kernel(const IgParams p) {
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
-template <int MODE, int BN, typename T>
-static int launch_ig(const IgParams& p, int splits, cudaStream_t st) {
-  using C = IgCfg<MODE, BN, T>;
-  auto kern = igemm_kernel<MODE, BN, T>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(igemm)");
-    attr_set = true;
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
   }
-  dim3 grid((p.M + 127) / 128, (p.N + BN - 1) / BN, splits);
-  kern<<<grid, 160, C::SMEM, st>>>(p);
+  return n;
+}
+
+template <int MODE, int BN, typename T, bool HASX>
+static int launch_ig(IgParams p, cudaStream_t st) {
+  using C = IgCfg<MODE, BN, T, HASX>;
+  auto kern = igemm_kernel<MODE, BN, T, HASX>;
+  const int smem = C::SMEM_FIXED + (MODE != MODE_WGRAD && p.stat_part ? 2 * p.stat_ld * 4 : 0);
+  static int attr_smem = 0;  // per instantiation
+  if (smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(igemm)");
+    attr_smem = smem;
+  }
+  p.mtiles = (p.M + 127) / 128;
+  p.ntiles = (p.N + BN - 1) / BN;
+  p.ntiles_total = p.mtiles * p.ntiles * p.splits;
+  p.fd_kred = make_fastdiv(p.kred > 0 ? p.kred : 1);
+  p.fd_kw = make_fastdiv(p.kw);
+  p.fd_ohow = make_fastdiv(p.oh * p.ow);
+  p.fd_ow = make_fastdiv(p.ow);
+  p.fd_hw = make_fastdiv(p.h * p.w);
+  p.fd_w = make_fastdiv(p.w);
+  p.fd_cin = make_fastdiv(p.cin);
+  p.taps = p.kh * p.kw;
+  const int grid = p.ntiles_total < num_sms() ? p.ntiles_total : num_sms();
+  kern<<<grid, C::THREADS, smem, st>>>(p);
   return check_launch("igemm");
 }
 
-template <int MODE, typename T>
-static int dispatch_bn(const IgParams& p, int bn, int splits, cudaStream_t st) {
+template <int MODE, typename T, bool HASX>
+static int dispatch_bn(const IgParams& p, int bn, cudaStream_t st) {
   switch (bn) {
-    case 32: return launch_ig<MODE, 32, T>(p, splits, st);
-    case 64: return launch_ig<MODE, 64, T>(p, splits, st);
-    case 128: return launch_ig<MODE, 128, T>(p, splits, st);
-    default: return launch_ig<MODE, 256, T>(p, splits, st);
+    case 32: return launch_ig<MODE, 32, T, HASX>(p, st);
+    case 64: return launch_ig<MODE, 64, T, HASX>(p, st);
+    case 128: return launch_ig<MODE, 128, T, HASX>(p, st);
+    default: return launch_ig<MODE, 256, T, HASX>(p, st);
   }
 }
 
 template <int MODE>
-static int dispatch(int dtype, const IgParams& p, int bn, int splits, cudaStream_t st) {
-  if (dtype == BNFF_BF16) return dispatch_bn<MODE, __nv_bfloat16>(p, bn, splits, st);
-  return dispatch_bn<MODE, float>(p, bn, splits, st);
+static int dispatch(int dtype, const IgParams& p, int bn, bool hasx, cudaStream_t st) {
+  if (dtype == BNFF_BF16) {
+    if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, __nv_bfloat16, true>(p, bn, st);
+    return dispatch_bn<MODE, __nv_bfloat16, false>(p, bn, st);
+  }
+  if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, float, true>(p, bn, st);
+  return dispatch_bn<MODE, float, false>(p, bn, st);
 }
 
 static int pick_bn(int n) {
@@ -608,8 +693,6 @@ static int pick_bn(int n) {
   if (n <= 128) return 128;
   return 256;
 }
-
-static inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace bnff
 
@@ -655,14 +738,15 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
   const int K = p.kh * p.kw * p.cin;
   const int kb = a->dtype == BNFF_BF16 ? 64 : 32;
   p.nkb = (K + kb - 1) / kb;
-  p.kb_per_split = p.nkb;
+  p.kpt = p.nkb;
+  p.splits = 1;
   p.a_ptr = a->x.ptr; p.a_rs = a->x.row_stride; p.a_pro = a->x_pro; p.a_coef = a->x_coef;
   p.b_ptr = a->wpack; p.b_rs = kpad_elems(a->dtype, K);
   p.c_ptr = a->y.ptr; p.c_rs = a->y.row_stride;
   p.bias = a->bias;
   p.stat_part = a->stat_part;
   p.stat_ld = p.cout;
-  return dispatch<MODE_FPROP>(a->dtype, p, pick_bn(p.N), 1, (cudaStream_t)stream);
+  return dispatch<MODE_FPROP>(a->dtype, p, pick_bn(p.N), false, (cudaStream_t)stream);
 }
 
 extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
@@ -683,7 +767,8 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   const int K = p.kh * p.kw * p.cout;
   const int kb = a->dtype == BNFF_BF16 ? 64 : 32;
   p.nkb = (K + kb - 1) / kb;
-  p.kb_per_split = p.nkb;
+  p.kpt = p.nkb;
+  p.splits = 1;
   p.a_ptr = a->dy.ptr; p.a_rs = a->dy.row_stride; p.a_pro = a->dy_pro; p.a_coef = a->dy_coef;
   p.a_xptr = a->dy_x.ptr; p.a_xrs = a->dy_x.row_stride;
   p.b_ptr = a->wpack_t; p.b_rs = kpad_elems(a->dtype, K);
@@ -692,16 +777,19 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   p.e_xptr = a->x.ptr; p.e_xrs = a->x.row_stride; p.e_coef = a->x_coef;
   p.stat_part = a->epi == BNFF_DG_NRC ? a->stat_part : nullptr;
   p.stat_ld = p.cin;
-  return dispatch<MODE_DGRAD>(a->dtype, p, pick_bn(p.N), 1, (cudaStream_t)stream);
+  return dispatch<MODE_DGRAD>(a->dtype, p, pick_bn(p.N), a->dy_pro == BNFF_PRO_BN_DX,
+                              (cudaStream_t)stream);
 }
+
+extern "C" int32_t bnff_stat_rows(void) { return num_sms(); }
 
 extern "C" int32_t bnff_wgrad_default_splits(int32_t n, int32_t oh, int32_t ow, int32_t kh,
                                              int32_t kw, int32_t c_in, int32_t c_out) {
   const long long npix = (long long)n * oh * ow;
   const int nkb = (int)((npix + 63) / 64);
   const int tiles = ((kh * kw * c_in + 127) / 128) * ((c_out + pick_bn(c_out) - 1) / pick_bn(c_out));
-  int splits = (2 * 148 + tiles - 1) / tiles;
-  const int max_splits = nkb / 4 > 0 ? nkb / 4 : 1;  // >= 4 k-blocks per split
+  int splits = (num_sms() + tiles - 1) / tiles;
+  const int max_splits = nkb / 8 > 0 ? nkb / 8 : 1;  // >= 8 k-blocks per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   return splits;
@@ -753,14 +841,15 @@ extern "C" int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream) {
   int splits = a->splits > 0 ? a->splits
                              : bnff_wgrad_default_splits(p.n, p.oh, p.ow, p.kh, p.kw, p.cin, p.cout);
   if (splits > p.nkb) splits = p.nkb;
-  p.kb_per_split = (p.nkb + splits - 1) / splits;
-  splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;  // no empty splits
+  p.kpt = (p.nkb + splits - 1) / splits;
+  splits = (p.nkb + p.kpt - 1) / p.kpt;  // no empty splits (the last may be partial)
+  p.splits = splits;
   p.a_ptr = a->x.ptr; p.a_rs = a->x.row_stride; p.a_pro = a->x_pro; p.a_coef = a->x_coef;
   p.b_ptr = a->dy.ptr; p.b_rs = a->dy.row_stride; p.b_pro = a->dy_pro; p.b_coef = a->dy_coef;
   p.b_xptr = a->dy_x.ptr; p.b_xrs = a->dy_x.row_stride;
   p.c_ptr = a->workspace; p.c_rs = p.N;
   cudaStream_t st = (cudaStream_t)stream;
-  rc = dispatch<MODE_WGRAD>(a->dtype, p, pick_bn(p.N), splits, st);
+  rc = dispatch<MODE_WGRAD>(a->dtype, p, pick_bn(p.N), a->dy_pro == BNFF_PRO_BN_DX, st);
   if (rc) return rc;
   const long long total = (long long)p.M * p.N;
   const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);

@@ -191,3 +191,43 @@ __device__ __forceinline__ float tf32_hi(float x) {
 }
 
 }  // namespace bnff
+
+namespace bnff {
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS): 16-byte global->shared copies with zero-fill
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// exact unsigned division by a runtime constant (Granlund-Montgomery, n < 2^32)
+struct FastDiv {
+  uint32_t d;
+  uint64_t m;
+  uint32_t s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{};
+  f.d = d;
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  f.s = s;
+  f.m = ((1ull << (32 + s)) + d - 1) / d;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  // m < 2^33: (n*m) >> 32 = ((n*m_lo) >> 32) + n*m_hi, exact in 64 bits
+  uint64_t t = ((uint64_t)n * (uint32_t)f.m) >> 32;
+  t += (uint64_t)n * (uint32_t)(f.m >> 32);
+  return (uint32_t)(t >> f.s);
+}
+}  // namespace bnff

@@ -320,8 +320,8 @@ class Engine:
         y = self._feature(node.outputs[0])
         pro = _lib.PRO_RELU if at.clip_input else _lib.PRO_NONE
         if node.kind == G.FUSED_CONV_STATS:
-            mt = (y.shape[0] * y.shape[1] * y.shape[2] + 127) // 128
-            part = self._empty((mt, 2, y.shape[3]), torch.float32)
+            mt = self.L.bnff_stat_rows()
+            part = self._zeros((mt, 2, y.shape[3]), torch.float32)
             self._conv_fprop(node, x, y, at.conv, pro, None, part)
             st = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
             self._emit_stats_finalize(part, mt, y.shape[3], st.count, st)
@@ -389,8 +389,8 @@ class Engine:
                        coef_of(tb[0], tb[1], tb[2]), 1, what="saved_postrelu", nbytes=_nb(x, saved))
         part = None
         if at.emit_stats:
-            mt = (y.shape[0] * y.shape[1] * y.shape[2] + 127) // 128
-            part = self._empty((mt, 2, y.shape[3]), torch.float32)
+            mt = self.L.bnff_stat_rows()
+            part = self._zeros((mt, 2, y.shape[3]), torch.float32)
         self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
         if at.emit_stats:
             ost = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
@@ -550,8 +550,7 @@ class Engine:
             dx = self._empty(tuple(x.shape))
             ecoef = coef_of()
             if dgrad_epi == _lib.DG_NRC:
-                mt = (x.shape[0] * x.shape[1] * x.shape[2] + 127) // 128
-                part = self._empty((mt, 2, x.shape[3]), torch.float32)
+                part = self._zeros((self.L.bnff_stat_rows(), 2, x.shape[3]), torch.float32)
                 m32, s32, b32, i32 = dgrad_tables
                 ecoef = coef_of(m32, s32, b32, i32)
             da = _lib.DgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(dy),

@@ -357,8 +357,8 @@ def fused_conv_stats_fwd(x, conv, out, budget: int = DEFAULT_BUDGET, workers: in
     if x.shape[3] < pc.p.in_c:
         raise ShapeError(f"{pc.p.name}: input has {x.shape[3]} channels, expected {pc.p.in_c}")
     out = _out_like(x, pc.p, out)
-    mt = (_pixels(out) + 127) // 128
-    part = torch.empty((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
+    mt = _L().bnff_stat_rows()
+    part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
     _fprop(x, pc, out, _lib.PRO_NONE, None, part)
     st = _new_stats(pc.p.out_c, _pixels(out), x.device)
     _finalize(part, mt, st)
@@ -385,8 +385,8 @@ def fused_norm_relu_conv_fwd(x, stats: DevStats, bn: BNParams, conv, out, saved_
     out = _out_like(x, pc.p, out)
     part, mt = None, 0
     if emit_stats:
-        mt = (_pixels(out) + 127) // 128
-        part = torch.empty((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
+        mt = _L().bnff_stat_rows()
+        part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
     _fprop(x, pc, out, _lib.PRO_BN_RELU, tb[:3], part)
     if emit_stats:
         st = _new_stats(pc.p.out_c, _pixels(out), x.device)
@@ -404,8 +404,8 @@ def fused_nrc_bwd(x, saved_postrelu, stats: DevStats, bn: BNParams, conv, dy, dy
     pc = _packed(conv, x)
     tb = _tables(stats, bn, x.device)
     n, h, w, c = x.shape
-    mt = (n * h * w + 127) // 128
-    part = torch.empty((mt, 2, c), dtype=torch.float32, device=x.device)
+    mt = _L().bnff_stat_rows()
+    part = torch.zeros((mt, 2, c), dtype=torch.float32, device=x.device)
     dt1 = _dgrad(dy, pc, x, _lib.DG_NRC, x, (tb[0], tb[1], tb[2], tb[3]), part, dy_pkg)
     dw, db = _wgrad(x, dy, pc, _lib.PRO_BN_RELU, tb[:3], dy_pkg)
     table, dg64, db64 = _dx_table(part, mt, stats, bn.gamma, bn.eps, x.device)

@@ -74,6 +74,8 @@ typedef struct {
   int32_t x_pro;      /* BNFF_PRO_NONE / RELU / BN_RELU */
   bnff_coef x_coef;
   float* stat_part;   /* nullable: sum/sumsq partials [bnff_stat_rows()][2][c_out] of the stored y */
+  const void* wwin;   /* nullable: window-layout weights (bnff_pack_window, fwd); selects the
+                         window-shift kernel when bnff_window_ok() */
 } bnff_fprop_args;
 
 typedef struct {
@@ -89,6 +91,7 @@ typedef struct {
   int32_t epi;        /* BNFF_DG_* */
   bnff_coef x_coef;   /* NRC: a = mean, b = scale, c = beta, d = invstd */
   float* stat_part;   /* NRC: partials [bnff_stat_rows()][2][c_in] of (sum dt1, sum dt1*xhat) */
+  const void* wwin;   /* nullable: window-layout weights (bnff_pack_window, dgrad) */
 } bnff_dgrad_args;
 
 typedef struct {
@@ -101,7 +104,8 @@ typedef struct {
   bnff_view dy_x;
   int32_t dy_pro;     /* NONE / BN_DX */
   bnff_coef dy_coef;
-  int32_t splits;     /* split-K factor (0 = choose); see bnff_wgrad_workspace */
+  int32_t splits;     /* split-K factor (0 = choose; < 0 forces the generic kernel); see
+                         bnff_wgrad_workspace */
   float* workspace;   /* splits * (kh*kw*c_in) * c_out floats */
   float* dw;          /* output (c_out, dw_cin, kh, kw) fp32, reference layout */
   int32_t dw_cin;     /* real input channels (<= x.c when the input is channel-padded); 0 = x.c */
@@ -138,6 +142,27 @@ int64_t bnff_pack_size(int32_t dtype, int32_t c_out, int32_t c_in_store, int32_t
 int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, int32_t c_in,
                       int32_t c_in_store, int32_t kh, int32_t kw, void* wpack, void* wpack_t,
                       void* stream);
+
+/* Window-shift tcgen05 kernels (csrc/wconv.cu) for stride-1 1x1/p0 and 3x3/p1 convs in
+ * bf16: each input element is transformed once per tile and every 3x3 tap reads a
+ * row-shifted window of it.  bnff_window_ok() says whether a conv qualifies; the
+ * pre-swizzled weight layout is [slab][tap][n_pad][64B|128B row] (fwd: n = c_out,
+ * reduction over c_in; dgrad: n = c_in, reduction over c_out, taps flipped).        */
+int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
+                   int32_t stride, int32_t pad, int32_t h, int32_t w);
+int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
+                              int32_t dgrad); /* elements */
+int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t kh,
+                     int32_t kw, void* wfwd, void* wdgrad, void* stream);
+int64_t bnff_window_wgrad_ws(int32_t n, int32_t h, int32_t w, int32_t kh, int32_t c_in,
+                             int32_t c_out); /* floats of split partials */
+int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
+                      int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, float* dw,
+                      int32_t dw_cin, void* stream);
+int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
+                     int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
+                     const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
+                     float* stat_part, void* stream);
 
 /* K5: channel sums over an NHWC view -> partials [tiles][2][c]:
  *   mode 0: (x, x^2)                         -- bn_stats_onepass (ops.py:231-237)

@@ -35,14 +35,15 @@ class FpropArgs(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32),
                 ("pad", C.c_int32), ("x", View), ("y", View), ("wpack", C.c_void_p),
                 ("bias", C.c_void_p), ("x_pro", C.c_int32), ("x_coef", Coef),
-                ("stat_part", C.c_void_p)]
+                ("stat_part", C.c_void_p), ("wwin", C.c_void_p)]
 
 
 class DgradArgs(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32),
                 ("pad", C.c_int32), ("dy", View), ("dy_x", View), ("dy_pro", C.c_int32),
                 ("dy_coef", Coef), ("dx", View), ("x", View), ("wpack_t", C.c_void_p),
-                ("epi", C.c_int32), ("x_coef", Coef), ("stat_part", C.c_void_p)]
+                ("epi", C.c_int32), ("x_coef", Coef), ("stat_part", C.c_void_p),
+                ("wwin", C.c_void_p)]
 
 
 class WgradArgs(C.Structure):
@@ -71,6 +72,14 @@ SIGNATURES = {
     "bnff_wgrad_default_splits": (_I32, [_I32] * 7),
     "bnff_pack_size": (_I64, [_I32] * 5),
     "bnff_pack_weights": (C.c_int, [_I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
+    "bnff_window_ok": (C.c_int, [_I32] * 9),
+    "bnff_window_pack_size": (_I64, [_I32] * 6),
+    "bnff_pack_window": (C.c_int, [_I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
+    "bnff_window_conv": (C.c_int, [_I32, _I32, _I32, View, View, _I32, Coef, View, _P, _P, _I32,
+                                   View, Coef, _P, _P]),
+    "bnff_window_wgrad_ws": (_I64, [_I32] * 6),
+    "bnff_window_wgrad": (C.c_int, [View, _I32, Coef, View, View, _I32, Coef, _I32, _P, _P, _I32,
+                                    _P]),
     "bnff_sum_tiles": (_I32, [_I64]),
     "bnff_channel_sums": (C.c_int, [_I32, _I32, View, View, Coef, _P, _P]),
     "bnff_stats_finalize": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P]),

@@ -732,6 +732,11 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
   if (a->x_pro == BNFF_PRO_BN_DX) return set_error(BNFF_ERR_UNSUPPORTED, "fprop: BN_DX prologue");
   if (a->x_pro == BNFF_PRO_BN_RELU && (!a->x_coef.a || !a->x_coef.b || !a->x_coef.c))
     return set_error(BNFF_ERR_STATE, "fprop: missing statistics for the normalize prologue");
+  if (a->wwin && bnff_window_ok(a->dtype, (int)a->x.c, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+    bnff_view none{};
+    return bnff_window_conv(0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin, a->bias,
+                            0, none, bnff_coef{}, a->stat_part, stream);
+  }
   p.M = p.n * p.oh * p.ow;
   p.N = p.cout;
   p.kred = p.cin;
@@ -761,6 +766,13 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
     return set_error(BNFF_ERR_SHAPE, "dgrad: dy spatial dims inconsistent with dx");
   if (a->dy_pro == BNFF_PRO_BN_DX && (rc = check_common(a->dtype, a->dy_x, "dgrad dy_x"))) return rc;
   if (a->epi != BNFF_DG_PLAIN && (rc = check_common(a->dtype, a->x, "dgrad x"))) return rc;
+  if (a->wwin && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+    if (a->dy_pro == BNFF_PRO_BN_DX && (!a->dy_coef.a || !a->dy_coef.e))
+      return set_error(BNFF_ERR_STATE, "dgrad: missing deferred-gradient coefficients");
+    return bnff_window_conv(1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx, a->wwin,
+                            nullptr, a->epi, a->x, a->x_coef,
+                            a->epi == BNFF_DG_NRC ? a->stat_part : nullptr, stream);
+  }
   p.M = p.n * p.h * p.w;
   p.N = p.cin;
   p.kred = p.cout;
@@ -800,7 +812,12 @@ extern "C" int64_t bnff_wgrad_workspace(int32_t n, int32_t oh, int32_t ow, int32
   if (splits <= 0) splits = bnff_wgrad_default_splits(n, oh, ow, kh, kw, c_in, c_out);
   const long long npix = (long long)n * oh * ow;
   // split-K partial tiles + dbias channel partials [tiles][2][c_out]
-  return (int64_t)splits * kh * kw * c_in * c_out + (int64_t)bnff_sum_tiles(npix) * 2 * c_out;
+  long long part = (long long)splits * kh * kw * c_in * c_out;
+  if (kh == kw && (kh == 1 || kh == 3)) {  // the window kernel may plan more splits (stride 1: oh = h)
+    const long long wwin = bnff_window_wgrad_ws(n, oh, ow, kh, c_in, c_out);
+    if (wwin > part) part = wwin;
+  }
+  return (int64_t)part + (int64_t)bnff_sum_tiles(npix) * 2 * c_out;
 }
 
 namespace bnff {
@@ -832,6 +849,18 @@ extern "C" int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream) {
   p.oh = (int)a->dy.h; p.ow = (int)a->dy.w; p.cout = (int)a->dy.c;
   if ((p.h + 2 * p.pad - p.kh) / p.stride + 1 != p.oh || (p.w + 2 * p.pad - p.kw) / p.stride + 1 != p.ow)
     return set_error(BNFF_ERR_SHAPE, "wgrad: dy spatial dims inconsistent with x");
+  if (a->splits >= 0 && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+    // window-shift kernel (splits < 0 forces the generic path)
+    int rc2 = bnff_window_wgrad(a->x, a->x_pro, a->x_coef, a->dy, a->dy_x, a->dy_pro, a->dy_coef, p.kh,
+                                a->workspace, a->dw, a->dw_cin, stream);
+    if (rc2) return rc2;
+    if (a->dbias != nullptr) {
+      const long long used = bnff_window_wgrad_ws(p.n, p.h, p.w, p.kh, p.cin, p.cout);
+      return bnff_dbias_scratch(a->dtype, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->workspace + used,
+                                a->dbias, stream);
+    }
+    return BNFF_OK;
+  }
   const int taps = p.kh * p.kw;
   p.M = taps * p.cin;
   p.N = p.cout;

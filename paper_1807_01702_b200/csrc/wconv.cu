@@ -1,0 +1,1268 @@
+// wconv.cu -- window-shift implicit-GEMM convolutions on tcgen05 / TMEM (sm_100a, bf16).
+//
+// Stride-1 "same" convolutions (1x1 pad 0, 3x3 pad 1) are run on a PADDED GRID of
+// output positions q = (img, py, px), py < h+2p, px < w+2p.  With the normalized
+// input laid out on the same grid (zero border), every filter tap (ty, tx) of output
+// q reads grid row q + ty*wp + tx: a pure row shift.  A CTA therefore loads and
+// transforms each input element ONCE per tile into a shared-memory window of
+// 128 + 2*wp + 2 rows (K-major, 128B/64B swizzled rows) and the MMA warp issues all
+// 9 taps as UMMAs whose A descriptors start at shifted rows of that window
+// (row-shifted swizzled descriptors validated by tools/umma_probe.cu).  Positions in
+// the padding columns/rows are computed and discarded (7% at 56x56).
+//
+// FPROP  y[q, co] = sum_tap,ci  pro(x)[q + s_tap, ci] * W[co, ci, tap]
+//        pro: NONE | RELU | BN_RELU (sub-BN2 + ReLU, fused.py:133-135)
+//        epilogue: +bias, bf16 store into a channel-offset NHWC view (in-place concat),
+//                  per-channel sum / sum^2 of the STORED values (sub-BN1 + MVF)
+// DGRAD  dx[q, ci] = sum_tap,co pro(dy)[q + s_tap, co] * W[co, ci, flip(tap)]
+//        pro: NONE | BN_DX (deferred sub-BN1' dx, ops.py:283-298)
+//        epilogue: PLAIN | CLIP (x>0) | NRC (mask relu(bn(x))>0, sum dt1, sum dt1*xhat,
+//                  fused.py:176-188)
+//
+// CTA = 13 warps: 8 loader warps (LDG -> transform in fp32 -> packed bf16 -> swizzled
+// STS), 1 MMA warp (TMEM owner, one elected lane issues tcgen05.mma), 4 epilogue warps
+// (TMEM -> registers -> smem staging -> coalesced stores; column statistics from the
+// staged tile).  Persistent grid, double-buffered TMEM accumulators, mbarrier rings.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "sm100.cuh"
+#include "common.cuh"
+
+namespace bnff {
+namespace wc {
+
+enum { M_FPROP = 0, M_DGRAD = 1 };
+constexpr int NLW = 8;                  // loader warps
+constexpr int LT = NLW * 32;            // loader threads
+constexpr int THREADS = (NLW + 1 + 4) * 32;
+constexpr int RMAX = 256;               // max window rows (wp <= 63 for 3x3)
+constexpr int SMEM_BUDGET = 225 * 1024;
+
+struct WcParams {
+  int n, h, w, hp, wp, pad, Q, mtiles, ntiles, tiles, R, stages;
+  FastDiv fd_hpwp, fd_wp;
+  int ci, nslab, N, npad;
+  const __nv_bfloat16* src; long long src_rs;
+  const __nv_bfloat16* srcx; long long srcx_rs;
+  int pro;
+  bnff_coef pcoef;
+  const uint8_t* wpk;
+  __nv_bfloat16* out; long long out_rs;
+  const float* bias;
+  int epi;
+  const __nv_bfloat16* ex; long long ex_rs;
+  bnff_coef ecoef;
+  float* stat_part;
+};
+
+__host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+template <int BN, int RB, int TAPS, int MODE>
+struct Layout {
+  static constexpr int SLABW = RB / 2;               // channels per slab row
+  static constexpr int CPR = RB / 16;                // 16B chunks per row
+  static constexpr int RS = LT / CPR;                // loader row step
+  static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
+  static constexpr bool WRES = TAPS == 9;            // weights resident in smem
+  static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
+  static constexpr int CW = MODE == M_DGRAD ? 32 : (BN < 64 ? BN : 64);  // epilogue column chunk
+  static constexpr int SROWB = CW * 2 + 16;          // staging row pitch (bytes)
+  static constexpr int STG = 128 * SROWB;
+  static constexpr int NSTG = MODE == M_DGRAD ? 4 : 1;  // dgrad: dt1, dt1*xhat, x[2]
+  static constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr uint32_t LAY = RB == 128 ? kLayoutSW128 : kLayoutSW64;
+  static constexpr uint32_t SBO = 8 * RB;
+};
+
+// byte offsets of the dynamic shared memory carve-up (identical on host and device)
+struct Carve {
+  int wres, stage0, stage_bytes, a_bytes, stg, ptab, etab, sacc, red, rowtab, rowpix, meta, total;
+};
+
+template <int BN, int RB, int TAPS, int MODE>
+__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages) {
+  using L = Layout<BN, RB, TAPS, MODE>;
+  Carve c{};
+  int off = 0;
+  c.wres = off;
+  if (L::WRES) off += align_up(nslab * TAPS * BN * RB, 1024);
+  c.a_bytes = align_up(R * RB, 1024);
+  c.stage_bytes = c.a_bytes * (L::XOP ? 2 : 1) + (L::WRES ? 0 : BN * RB);
+  c.stage0 = off;
+  off += stages * c.stage_bytes;
+  c.stg = off;
+  off += L::NSTG * L::STG;
+  c.ptab = off;
+  off += 3 * nslab * L::SLABW * 4;
+  c.etab = off;
+  off += 4 * npad * 4;
+  c.sacc = off;
+  off += 2 * npad * 4;
+  c.red = off;
+  off += 4 * 128 * 4;
+  c.rowtab = off;
+  off += 2 * RMAX * 4;
+  c.rowpix = off;
+  off += 128 * 4;
+  c.meta = off;
+  off += 8 * LT * 4;
+  c.total = off + 1024;  // + alignment slack
+  return c;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& r, float* f) {
+  f[0] = bf16lo(r.x); f[1] = bf16hi(r.x); f[2] = bf16lo(r.y); f[3] = bf16hi(r.y);
+  f[4] = bf16lo(r.z); f[5] = bf16hi(r.z); f[6] = bf16lo(r.w); f[7] = bf16hi(r.w);
+}
+__device__ __forceinline__ uint4 pack8(const float* f, bool relu) {
+  uint4 o;
+  if (relu) {
+    o.x = pack_bf16_relu(f[0], f[1]); o.y = pack_bf16_relu(f[2], f[3]);
+    o.z = pack_bf16_relu(f[4], f[5]); o.w = pack_bf16_relu(f[6], f[7]);
+  } else {
+    o.x = pack_bf16_rn(f[0], f[1]); o.y = pack_bf16_rn(f[2], f[3]);
+    o.z = pack_bf16_rn(f[4], f[5]); o.w = pack_bf16_rn(f[6], f[7]);
+  }
+  return o;
+}
+__device__ __forceinline__ void ld16f(const float* p, float* v) {  // 16 floats, 16B aligned
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 t = reinterpret_cast<const float4*>(p)[i];
+    v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+  }
+}
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    default: cp_async_wait<7>(); break;
+  }
+}
+
+template <int BN, int RB, int TAPS, int MODE>
+__global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
+  using L = Layout<BN, RB, TAPS, MODE>;
+  constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], w_bar;
+  __shared__ uint32_t tmem_sh;
+  const Carve cv = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, p.stages);
+  const int ST = p.stages;
+  float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
+  float* etab = reinterpret_cast<float*>(smem + cv.etab);
+  float* sacc = reinterpret_cast<float*>(smem + cv.sacc);
+  float* red = reinterpret_cast<float*>(smem + cv.red);
+  int* rowtab = reinterpret_cast<int*>(smem + cv.rowtab);
+  int* rowpix = reinterpret_cast<int*>(smem + cv.rowpix);
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + cv.meta);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntl = (p.tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const bool do_stats = p.stat_part != nullptr;
+  const int kpad = p.nslab * SLABW;
+
+  // ---- setup: barriers, TMEM, coefficient tables
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full_bar[s], LT + (L::WRES ? 0 : 1));
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], 128); }
+    mbar_init(&w_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
+  // window-operand tables: BN_RELU: (scale, beta - mean*scale); BN_DX: (g, -g*k2*inv, g*(k2*inv*mean-k1))
+  for (int c = tid; c < kpad; c += THREADS) {
+    float t0 = 1.f, t1 = 0.f, t2 = 0.f;
+    if (c < p.ci) {
+      if (p.pro == BNFF_PRO_BN_RELU) {
+        const float m = p.pcoef.a[c], s = p.pcoef.b[c], b = p.pcoef.c[c];
+        t0 = s;
+        t1 = b - m * s;
+      } else if (p.pro == BNFF_PRO_BN_DX) {
+        const float m = p.pcoef.a[c], inv = p.pcoef.b[c], k1 = p.pcoef.c[c], k2 = p.pcoef.d[c],
+                    g = p.pcoef.e[c];
+        t0 = g;
+        t1 = -g * k2 * inv;
+        t2 = g * (k2 * inv * m - k1);
+      }
+    }
+    ptab[c] = t0;
+    ptab[kpad + c] = t1;
+    ptab[2 * kpad + c] = t2;
+  }
+  // epilogue tables: FPROP: bias; DGRAD NRC: (scale, beta-mean*scale, inv, -mean*inv)
+  for (int c = tid; c < p.npad; c += THREADS) {
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    if (c < p.N) {
+      if (MODE == M_FPROP) {
+        t0 = p.bias ? p.bias[c] : 0.f;
+      } else if (p.epi == BNFF_DG_NRC) {
+        const float m = p.ecoef.a[c], s = p.ecoef.b[c], b = p.ecoef.c[c], inv = p.ecoef.d[c];
+        t0 = s;
+        t1 = b - m * s;
+        t2 = inv;
+        t3 = -m * inv;
+      }
+    }
+    etab[c] = t0;
+    etab[p.npad + c] = t1;
+    etab[2 * p.npad + c] = t2;
+    etab[3 * p.npad + c] = t3;
+    sacc[c] = 0.f;
+    sacc[p.npad + c] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  auto stage_a = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes; };
+  auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes; };
+  auto stage_b = [&](int s) {
+    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (L::XOP ? 2 : 1);
+  };
+  auto tile_of = [&](int it, int& q0, int& n0) {
+    const int t = (int)blockIdx.x + it * (int)gridDim.x;
+    q0 = (t / p.ntiles) * 128;
+    n0 = (t % p.ntiles) * BN;
+  };
+
+  if (warp < NLW) {
+    // =============================== loaders ===============================
+    // issue (cp.async, zero-fill for padding rows) runs LAG stages ahead of the in-place
+    // transform; the MMA consumes a stage once the transform has arrived on full_bar.
+    const int j = tid % CPR, r0 = tid / CPR;
+    if (L::WRES && tid == 0) {
+      const uint32_t wb = p.nslab * TAPS * BN * RB;
+      mbar_arrive_expect_tx(&w_bar, wb);
+      bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
+    }
+    const int hpwp = p.hp * p.wp;
+    const int G = ntl * p.nslab;
+    // loads in flight vs transformed stages waiting for / inside the MMA: split the ring
+    const int LAG = ST / 2 > 1 ? ST / 2 : 1;
+    const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
+    const bool need_t = p.pro != BNFF_PRO_NONE;
+    for (int g = 0; g < G + LAG; ++g) {
+      if (g < G) {
+        const int it = g / p.nslab, s = g - it * p.nslab;
+        int q0, n0;
+        tile_of(it, q0, n0);
+        int* rt = rowtab + (it & 1) * RMAX;
+        if (s == 0) {
+          for (int r = tid; r < p.R; r += LT) {
+            const int q = q0 + r;
+            int src = -1;
+            if (q < p.Q) {
+              const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
+              const int rem = q - img * hpwp;
+              const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
+              const int px = rem - py * p.wp;
+              const int iy = py - p.pad, ix = px - p.pad;
+              if (iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) src = (img * p.h + iy) * p.w + ix;
+            }
+            rt[r] = src;
+          }
+          named_bar_sync(1, LT);
+        }
+        const int st = g % ST;
+        if (g >= ST) mbar_wait(&empty_bar[st], ((g / ST) - 1) & 1);
+        if (!L::WRES && tid == 0) {
+          mbar_arrive_expect_tx(&full_bar[st], BN * RB);
+          bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
+                   &full_bar[st]);
+        }
+        const int cs = min(SLABW, p.ci - s * SLABW);
+        const int c0 = s * SLABW + j * 8;
+        uint32_t mask = 0;
+        if (j * 8 < cs) {
+          const uint32_t abase = smem_u32(stage_a(st)), xbase = smem_u32(stage_x(st));
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int r = r0 + u * RS;
+            if (r < p.R) {
+              const int src = rt[r];
+              const bool ok = src >= 0;
+              uint32_t off;
+              if constexpr (RB == 128) off = r * 128 + ((j ^ (r & 7)) << 4);
+              else off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+              cp_async16(abase + off, p.src + (ok ? (long long)src * p.src_rs + c0 : 0), ok ? 16u : 0u);
+              if (xop)
+                cp_async16(xbase + off, p.srcx + (ok ? (long long)src * p.srcx_rs + c0 : 0),
+                           ok ? 16u : 0u);
+              mask |= (ok ? 1u : 0u) << u;
+            }
+          }
+        }
+        meta[st * LT + tid] = mask;
+      }
+      cp_async_commit();
+      if (g >= LAG) {
+        const int gg = g - LAG;
+        const int st = gg % ST;
+        const int it = gg / p.nslab, s = gg - it * p.nslab;
+        cp_async_wait_dyn(LAG);
+        const int cs = min(SLABW, p.ci - s * SLABW);
+        if (need_t && j * 8 < cs) {
+          const int c0 = s * SLABW + j * 8;
+          float t0[8], t1[8], t2[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            t0[i] = ptab[c0 + i];
+            t1[i] = ptab[kpad + c0 + i];
+            t2[i] = ptab[2 * kpad + c0 + i];
+          }
+          const uint32_t mask = meta[st * LT + tid];
+          uint8_t* A = stage_a(st);
+          uint8_t* X = stage_x(st);
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int r = r0 + u * RS;
+            if (r >= p.R || !((mask >> u) & 1u)) continue;  // padding rows stay zero
+            uint32_t off;
+            if constexpr (RB == 128) off = r * 128 + ((j ^ (r & 7)) << 4);
+            else off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(A + off), f);
+            uint4 o;
+            if (p.pro == BNFF_PRO_RELU) {
+              o = pack8(f, true);
+            } else if (p.pro == BNFF_PRO_BN_RELU) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], t1[i]);
+              o = pack8(f, true);
+            } else {
+              float xf[8];
+              unpack8(*reinterpret_cast<const uint4*>(X + off), xf);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], fmaf(xf[i], t1[i], t2[i]));
+              o = pack8(f, false);
+            }
+            *reinterpret_cast<uint4*>(A + off) = o;
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&full_bar[st]);
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == NLW) {
+    // =============================== MMA issuer ===============================
+    if (lane == 0) {
+      if (L::WRES) mbar_wait(&w_bar, 0);
+      constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 0, 0);
+      const uint32_t wres = smem_u32(smem + cv.wres);
+      int g = 0;
+      for (int it = 0; it < ntl; ++it) {
+        const int buf = it & 1;
+        if (it >= 2) mbar_wait(&acce_bar[buf], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN;
+        uint32_t acc = 0;
+        for (int s = 0; s < p.nslab; ++s, ++g) {
+          const int st = g % ST;
+          mbar_wait(&full_bar[st], (g / ST) & 1);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(stage_a(st));
+          const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB : smem_u32(stage_b(st));
+          const int ks = min(SLABW, p.ci - s * SLABW) / 16;
+#pragma unroll 1
+          for (int u = 0; u < TAPS; ++u) {
+            const int shift = TAPS == 9 ? (u / 3) * p.wp + (u % 3) : 0;
+            for (int kk = 0; kk < ks; ++kk) {
+              const uint64_t ad = make_sdesc(abase + shift * RB + kk * 32, 16, L::SBO, L::LAY);
+              const uint64_t bd = make_sdesc(bbase + u * BN * RB + kk * 32, 16, L::SBO, L::LAY);
+              umma_f16(d, ad, bd, idesc, acc);
+              acc = 1;
+            }
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        umma_commit(&accf_bar[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue ===============================
+    const int quad = warp & 3;
+    const int et = tid - (NLW + 1) * 32;  // 0..127
+    const int row = quad * 32 + lane;
+    uint8_t* stg = smem + cv.stg;
+    uint8_t* stg2 = stg + L::STG;
+    uint8_t* xs0 = stg + 2 * L::STG;       // dgrad: double-buffered x chunk (own row)
+    const int hpwp = p.hp * p.wp;
+    constexpr int HALF = CW / 2;             // column pairs per chunk
+    constexpr int RG = 128 / HALF;           // row groups in the column pass
+    constexpr int NCH = BN / CW;             // column chunks per tile
+    const int cp = et % HALF, rg = et / HALF;
+    const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
+    const bool nrc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC;
+    // x chunk prefetch (own row, CW channels) into xs[buf]
+    auto fetch_x = [&](int pix, int n0, int cc, int b) {
+      const uint32_t dst = smem_u32(xs0 + b * L::STG + row * L::SROWB);
+      const int col = n0 + cc;
+      const bool ok = pix >= 0 && col < p.N;
+#pragma unroll
+      for (int i = 0; i < CW / 8; ++i)
+        cp_async16(dst + i * 16, p.ex + (ok ? (long long)pix * p.ex_rs + col + i * 8 : 0), ok ? 16u : 0u);
+      cp_async_commit();
+    };
+    for (int it = 0; it < ntl; ++it) {
+      const int buf = it & 1;
+      int q0, n0;
+      tile_of(it, q0, n0);
+      int pix = -1;
+      {
+        // output positions are the UNPADDED coordinates of the grid: (img, py, px), py<h, px<w
+        const int q = q0 + row;
+        if (q < p.Q) {
+          const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
+          const int rem = q - img * hpwp;
+          const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
+          const int px = rem - py * p.wp;
+          if (py < p.h && px < p.w) pix = (img * p.h + py) * p.w + px;
+        }
+      }
+      rowpix[row] = pix;
+      if (need_x) fetch_x(pix, n0, 0, 0);
+      mbar_wait(&accf_bar[buf], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ci = 0; ci < NCH; ++ci) {
+        const int cc = ci * CW;
+        if (need_x) {
+          if (ci + 1 < NCH) {
+            fetch_x(pix, n0, cc + CW, (ci + 1) & 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+        }
+        const uint8_t* xrow = xs0 + (ci & 1) * L::STG + row * L::SROWB;
+        // ---- row pass: TMEM -> fp32 -> epilogue math -> bf16 staging
+#pragma unroll
+        for (int c16 = 0; c16 < CW; c16 += 16) {
+          float v[16];
+          tmem_ld16(tmem + buf * BN + cc + c16 + ((uint32_t)(quad * 32) << 16), v);
+          tmem_ld_wait();
+          const int gc = n0 + cc + c16;
+          float xh[16];
+          if (MODE == M_FPROP) {
+            float bv[16];
+            ld16f(etab + gc, bv);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = pix >= 0 ? v[i] + bv[i] : 0.f;
+          } else {
+            if (need_x) {
+              float xv[16];
+              unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2), xv);
+              unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2 + 16), xv + 8);
+              if (p.epi == BNFF_DG_CLIP) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = xv[i] > 0.f ? v[i] : 0.f;
+              } else {
+                float e0[16], e1[16], e2[16], e3[16];
+                ld16f(etab + gc, e0);
+                ld16f(etab + p.npad + gc, e1);
+                ld16f(etab + 2 * p.npad + gc, e2);
+                ld16f(etab + 3 * p.npad + gc, e3);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float t = fmaf(xv[i], e0[i], e1[i]);
+                  v[i] = t > 0.f ? v[i] : 0.f;
+                  xh[i] = fmaf(xv[i], e2[i], e3[i]);
+                }
+              }
+            }
+            if (pix < 0) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+          }
+          const uint4 o0 = pack8(v, false), o1 = pack8(v + 8, false);
+          uint4* sp = reinterpret_cast<uint4*>(stg + row * L::SROWB + c16 * 2);
+          sp[0] = o0;
+          sp[1] = o1;
+          if (nrc) {
+            float r[16];
+            unpack8(o0, r);
+            unpack8(o1, r + 8);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] *= xh[i];
+            uint4* sp2 = reinterpret_cast<uint4*>(stg2 + row * L::SROWB + c16 * 2);
+            sp2[0] = pack8(r, false);
+            sp2[1] = pack8(r + 8, false);
+          }
+        }
+        if (ci == NCH - 1) {
+          tc_fence_before();
+          mbar_arrive(&acce_bar[buf]);  // accumulator slot drained
+        }
+        named_bar_sync(2, 128);
+        // ---- column pass: per-channel sums of the staged (stored) values
+        if (do_stats && (MODE == M_FPROP || nrc)) {
+          float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+          const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
+          const uint32_t* s32b = reinterpret_cast<const uint32_t*>(stg2);
+#pragma unroll 4
+          for (int r = rg; r < 128; r += RG) {
+            const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
+            const float lo = bf16lo(wv), hi = bf16hi(wv);
+            a0 += lo;
+            a1 += hi;
+            if (MODE == M_FPROP) {
+              b0 = fmaf(lo, lo, b0);
+              b1 = fmaf(hi, hi, b1);
+            } else {
+              const uint32_t w2 = s32b[r * (L::SROWB / 4) + cp];
+              b0 += bf16lo(w2);
+              b1 += bf16hi(w2);
+            }
+          }
+          red[(rg * 4 + 0) * HALF + cp] = a0;
+          red[(rg * 4 + 1) * HALF + cp] = a1;
+          red[(rg * 4 + 2) * HALF + cp] = b0;
+          red[(rg * 4 + 3) * HALF + cp] = b1;
+          named_bar_sync(2, 128);
+          if (et < CW) {
+            const int c = et, pc = c >> 1, odd = c & 1;
+            float s1 = 0.f, s2 = 0.f;
+            for (int k = 0; k < RG; ++k) {
+              s1 += red[(k * 4 + odd) * HALF + pc];
+              s2 += red[(k * 4 + 2 + odd) * HALF + pc];
+            }
+            const int gcol = n0 + cc + c;
+            if (gcol < p.N) {
+              sacc[gcol] += s1;
+              sacc[p.npad + gcol] += s2;
+            }
+          }
+        }
+        // ---- store pass: staged rows -> NHWC view (coalesced 16B stores)
+        constexpr int CPO = CW / 8;  // 16B chunks per staged row
+        for (int k = et; k < 128 * CPO; k += 128) {
+          const int r = k / CPO, ch = k - r * CPO;
+          const int px = rowpix[r];
+          const int col = n0 + cc + ch * 8;
+          if (px >= 0 && col < p.N) {
+            const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
+            *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
+          }
+        }
+        named_bar_sync(2, 128);
+      }
+    }
+    if (do_stats) {
+      for (int c = et; c < p.N; c += 128) {
+        p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + c] = sacc[c];
+        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + c] = sacc[p.npad + c];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NLW) tmem_dealloc<L::TCOLS>(tmem);
+}
+
+// ===========================================================================
+// WGRAD on the padded grid:  dW[tap][ci][co] = sum_q  P_x[q + s_tap, ci] * G[q, co]
+// A = P_x (MN-major: each grid position is a 128B row of 64 channels per atom; one
+// window of KB + 2*wp + 2 rows serves all 9 taps through K-shifted descriptors),
+// B = G = pro(dy) at output positions (zero elsewhere), MN-major.  A CTA owns one
+// work unit (m-group of MT*128 input channels, N tile, K split) at a time and keeps
+// TAPS*MT accumulators of BN columns in TMEM; fp32 partials go to a workspace
+// reduced in fixed split order (deterministic).
+// ===========================================================================
+int num_sms_wc();
+
+struct WgParams {
+  int n, h, w, hp, wp, pad, Q;
+  FastDiv fd_hpwp, fd_wp;
+  int cin, cout, KB, RA, nkb, kpt, splits, MG, NT, units, stages;
+  const __nv_bfloat16* x; long long x_rs;
+  int x_pro;
+  bnff_coef x_coef;
+  const __nv_bfloat16* dy; long long dy_rs;
+  const __nv_bfloat16* dyx; long long dyx_rs;
+  int dy_pro;
+  bnff_coef dy_coef;
+  float* ws;
+};
+
+template <int BN, int MT, int TAPS, int KB>
+struct WgL {
+  static constexpr int BRB = BN * 2 >= 128 ? 128 : BN * 2;  // B row bytes per atom
+  static constexpr int NBA = BN * 2 / BRB;                   // B atoms
+  static constexpr int BCPR = BRB / 16;                      // B chunks per row per atom
+  static constexpr int BCH = NBA * BCPR;                     // B chunks per row
+  static constexpr int RAMAX = TAPS == 9 ? KB + 128 : KB;    // A rows (wp <= 63)
+  static constexpr int AAT = 2 * MT;                         // A atoms
+  static constexpr int UAR = RAMAX / 32;                     // A rows per thread per atom
+  static constexpr int UB = KB * BCH / LT;                   // B chunks per thread
+  static constexpr uint32_t BLAY = BRB == 128 ? kLayoutSW128 : kLayoutSW64;
+  static constexpr int NACC = TAPS * MT;
+  static constexpr int TCOLS = NACC * BN <= 32 ? 32 : (NACC * BN <= 64 ? 64 : (NACC * BN <= 128 ? 128 : (NACC * BN <= 256 ? 256 : 512)));
+  static_assert(NACC * BN <= 512, "TMEM");
+  static_assert(KB * BCH % LT == 0, "B mapping");
+};
+
+struct WgCarve {
+  int stage_bytes, a_bytes, b_bytes, ptab, qtab, rowx, rowg, meta, total;
+};
+template <int BN, int MT, int TAPS, int KB>
+__host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int stages) {
+  using L = WgL<BN, MT, TAPS, KB>;
+  WgCarve c{};
+  c.a_bytes = L::AAT * RA * 128;
+  c.b_bytes = L::NBA * KB * L::BRB;
+  c.stage_bytes = align_up(c.a_bytes + 2 * c.b_bytes, 1024);  // A | B | X(dy_x)
+  int off = stages * c.stage_bytes;
+  c.ptab = off;
+  off += 2 * cin_pad * 4;
+  c.qtab = off;
+  off += 3 * npad * 4;
+  c.rowx = off;
+  off += 2 * L::RAMAX * 4;
+  c.rowg = off;
+  off += 2 * KB * 4;
+  c.meta = off;
+  off += 8 * LT * 4;
+  c.total = off + 1024;
+  return c;
+}
+
+template <int BN, int MT, int TAPS, int KB>
+__global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
+  using L = WgL<BN, MT, TAPS, KB>;
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar, acce_bar;
+  __shared__ uint32_t tmem_sh;
+  const int cin_pad = p.MG * MT * 128, npad = p.NT * BN;
+  const WgCarve cv = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, p.stages);
+  const int ST = p.stages;
+  float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
+  float* qtab = reinterpret_cast<float*>(smem + cv.qtab);
+  int* rowx = reinterpret_cast<int*>(smem + cv.rowx);
+  int* rowg = reinterpret_cast<int*>(smem + cv.rowg);
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + cv.meta);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nun = (p.units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { mbar_init(&full_bar[s], LT); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&accf_bar, 1);
+    mbar_init(&acce_bar, 128);
+    fence_mbar_init();
+  }
+  if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
+  for (int c = tid; c < cin_pad; c += THREADS) {  // x prologue: (scale, beta - mean*scale)
+    float t0 = 1.f, t1 = 0.f;
+    if (c < p.cin && p.x_pro == BNFF_PRO_BN_RELU) {
+      t0 = p.x_coef.b[c];
+      t1 = p.x_coef.c[c] - p.x_coef.a[c] * t0;
+    }
+    ptab[c] = t0;
+    ptab[cin_pad + c] = t1;
+  }
+  for (int c = tid; c < npad; c += THREADS) {  // dy prologue (BN_DX)
+    float t0 = 1.f, t1 = 0.f, t2 = 0.f;
+    if (c < p.cout && p.dy_pro == BNFF_PRO_BN_DX) {
+      const float m = p.dy_coef.a[c], inv = p.dy_coef.b[c], k1 = p.dy_coef.c[c],
+                  k2 = p.dy_coef.d[c], g = p.dy_coef.e[c];
+      t0 = g;
+      t1 = -g * k2 * inv;
+      t2 = g * (k2 * inv * m - k1);
+    }
+    qtab[c] = t0;
+    qtab[npad + c] = t1;
+    qtab[2 * npad + c] = t2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  auto unit_of = [&](int ui, int& mg, int& nt, int& sp) {
+    const int u = (int)blockIdx.x + ui * (int)gridDim.x;
+    sp = u % p.splits;
+    const int r = u / p.splits;
+    nt = r % p.NT;
+    mg = r / p.NT;
+  };
+  auto stage_a = [&](int s) { return smem + s * cv.stage_bytes; };
+  auto stage_b = [&](int s) { return smem + s * cv.stage_bytes + cv.a_bytes; };
+  auto stage_x = [&](int s) { return smem + s * cv.stage_bytes + cv.a_bytes + cv.b_bytes; };
+  auto kb_count = [&](int sp) { return min(p.kpt, p.nkb - sp * p.kpt); };
+
+  if (warp < NLW) {
+    // =============================== loaders ===============================
+    const int ja = tid & 7, ra0 = tid >> 3;                 // A: chunk column, first row
+    const int jb = tid % L::BCH, rb0 = tid / L::BCH;        // B: chunk column, first row
+    constexpr int RBS = LT / L::BCH;                        // B row step
+    const int hpwp = p.hp * p.wp;
+    const bool xb = p.dy_pro == BNFF_PRO_BN_DX;
+    int G = 0;
+    for (int ui = 0; ui < nun; ++ui) {
+      int mg, nt, sp;
+      unit_of(ui, mg, nt, sp);
+      G += kb_count(sp);
+    }
+    const int LAG = ST / 2 > 1 ? ST / 2 : 1;
+    // issue-side cursor
+    int iu = 0, ik = 0, imgi = 0, inti = 0, isp = 0, icnt = 0;
+    if (nun > 0) { unit_of(0, imgi, inti, isp); icnt = kb_count(isp); }
+    // transform-side cursor
+    int tu = 0, tk = 0, tmg = 0, tnt = 0, tsp = 0, tcnt = 0;
+    if (nun > 0) { unit_of(0, tmg, tnt, tsp); tcnt = kb_count(tsp); }
+    (void)tu; (void)tk; (void)tsp;
+    for (int g = 0; g < G + LAG; ++g) {
+      if (g < G) {
+        const int kb = isp * p.kpt + ik;
+        const int q0 = kb * KB;
+        int* rx = rowx + (g & 1) * L::RAMAX;
+        int* rg = rowg + (g & 1) * KB;
+        for (int r = tid; r < p.RA; r += LT) {
+          const int q = q0 + r;
+          int src = -1;
+          if (q < p.Q) {
+            const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
+            const int rem = q - img * hpwp;
+            const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
+            const int px = rem - py * p.wp;
+            const int iy = py - p.pad, ix = px - p.pad;
+            if (iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) src = (img * p.h + iy) * p.w + ix;
+            if (r < KB) rg[r] = (py < p.h && px < p.w) ? (img * p.h + py) * p.w + px : -1;
+          } else if (r < KB) {
+            rg[r] = -1;
+          }
+          rx[r] = src;
+        }
+        named_bar_sync(1, LT);
+        const int st = g % ST;
+        if (g >= ST) mbar_wait(&empty_bar[st], ((g / ST) - 1) & 1);
+        uint32_t mask = 0;
+        const uint32_t abase = smem_u32(stage_a(st));
+#pragma unroll
+        for (int a = 0; a < L::AAT; ++a) {
+          const int c0 = imgi * MT * 128 + a * 64 + ja * 8;
+#pragma unroll
+          for (int k = 0; k < L::UAR; ++k) {
+            const int r = ra0 + 32 * k;
+            if (r < p.RA && c0 < p.cin) {
+              const int src = rx[r];
+              const bool ok = src >= 0;
+              const uint32_t off = a * p.RA * 128 + r * 128 + ((ja ^ (r & 7)) << 4);
+              cp_async16(abase + off, p.x + (ok ? (long long)src * p.x_rs + c0 : 0), ok ? 16u : 0u);
+              mask |= (ok ? 1u : 0u) << (a * L::UAR + k);
+            }
+          }
+        }
+        const uint32_t bbase = smem_u32(stage_b(st)), xbase = smem_u32(stage_x(st));
+        const int co0 = inti * BN + jb * 8;
+#pragma unroll
+        for (int k = 0; k < L::UB; ++k) {
+          const int r = rb0 + RBS * k;
+          if (co0 < p.cout) {
+            const int src = rg[r];
+            const bool ok = src >= 0;
+            const int b = jb / L::BCPR, jj = jb % L::BCPR;
+            uint32_t off = b * KB * L::BRB + r * L::BRB;
+            if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
+            else off += (jj ^ ((r >> 1) & 3)) << 4;
+            cp_async16(bbase + off, p.dy + (ok ? (long long)src * p.dy_rs + co0 : 0), ok ? 16u : 0u);
+            if (xb)
+              cp_async16(xbase + off, p.dyx + (ok ? (long long)src * p.dyx_rs + co0 : 0), ok ? 16u : 0u);
+            mask |= (ok ? 1u : 0u) << (24 + k);
+          }
+        }
+        meta[st * LT + tid] = mask;
+        if (++ik == icnt) {
+          ik = 0;
+          if (++iu < nun) { unit_of(iu, imgi, inti, isp); icnt = kb_count(isp); }
+        }
+      }
+      cp_async_commit();
+      if (g >= LAG) {
+        const int gg = g - LAG;
+        const int st = gg % ST;
+        cp_async_wait_dyn(LAG);
+        const uint32_t mask = meta[st * LT + tid];
+        if (p.x_pro != BNFF_PRO_NONE) {
+          uint8_t* A = stage_a(st);
+#pragma unroll
+          for (int a = 0; a < L::AAT; ++a) {
+            const int c0 = tmg * MT * 128 + a * 64 + ja * 8;
+            if (c0 >= p.cin) continue;
+            float t0[8], t1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { t0[i] = ptab[c0 + i]; t1[i] = ptab[cin_pad + c0 + i]; }
+#pragma unroll
+            for (int k = 0; k < L::UAR; ++k) {
+              if (!((mask >> (a * L::UAR + k)) & 1u)) continue;
+              const int r = ra0 + 32 * k;
+              const uint32_t off = a * p.RA * 128 + r * 128 + ((ja ^ (r & 7)) << 4);
+              float f[8];
+              unpack8(*reinterpret_cast<const uint4*>(A + off), f);
+              if (p.x_pro == BNFF_PRO_BN_RELU) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], t1[i]);
+              }
+              *reinterpret_cast<uint4*>(A + off) = pack8(f, true);
+            }
+          }
+        }
+        if (xb) {
+          const int co0 = tnt * BN + jb * 8;
+          if (co0 < p.cout) {
+            uint8_t* B = stage_b(st);
+            const uint8_t* X = stage_x(st);
+            float t0[8], t1[8], t2[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              t0[i] = qtab[co0 + i]; t1[i] = qtab[npad + co0 + i]; t2[i] = qtab[2 * npad + co0 + i];
+            }
+#pragma unroll
+            for (int k = 0; k < L::UB; ++k) {
+              if (!((mask >> (24 + k)) & 1u)) continue;
+              const int r = rb0 + RBS * k;
+              const int b = jb / L::BCPR, jj = jb % L::BCPR;
+              uint32_t off = b * KB * L::BRB + r * L::BRB;
+              if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
+              else off += (jj ^ ((r >> 1) & 3)) << 4;
+              float f[8], xf[8];
+              unpack8(*reinterpret_cast<const uint4*>(B + off), f);
+              unpack8(*reinterpret_cast<const uint4*>(X + off), xf);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], fmaf(xf[i], t1[i], t2[i]));
+              *reinterpret_cast<uint4*>(B + off) = pack8(f, false);
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&full_bar[st]);
+        if (++tk == tcnt) {
+          tk = 0;
+          if (++tu < nun) { unit_of(tu, tmg, tnt, tsp); tcnt = kb_count(tsp); }
+        }
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == NLW) {
+    // =============================== MMA issuer ===============================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 1, 1);
+      int g = 0;
+      for (int ui = 0; ui < nun; ++ui) {
+        int mg, nt, sp;
+        unit_of(ui, mg, nt, sp);
+        const int cnt = kb_count(sp);
+        if (ui >= 1) mbar_wait(&acce_bar, (ui - 1) & 1);
+        tc_fence_after();
+        for (int k = 0; k < cnt; ++k, ++g) {
+          const int st = g % ST;
+          mbar_wait(&full_bar[st], (g / ST) & 1);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(stage_a(st)), bbase = smem_u32(stage_b(st));
+#pragma unroll 1
+          for (int u = 0; u < TAPS; ++u) {
+            const int shift = TAPS == 9 ? (u / 3) * p.wp + (u % 3) : 0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+              for (int kk = 0; kk < KB / 16; ++kk) {
+                const uint64_t ad = make_sdesc(abase + 2 * mt * p.RA * 128 + (shift + kk * 16) * 128,
+                                               p.RA * 128, 1024, kLayoutSW128);
+                const uint64_t bd = make_sdesc(bbase + kk * 16 * L::BRB, KB * L::BRB, 8 * L::BRB, L::BLAY);
+                umma_f16(tmem + (u * MT + mt) * BN, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        umma_commit(&accf_bar);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue ===============================
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    for (int ui = 0; ui < nun; ++ui) {
+      int mg, nt, sp;
+      unit_of(ui, mg, nt, sp);
+      mbar_wait(&accf_bar, ui & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int u = 0; u < TAPS; ++u) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int ci = (mg * MT + mt) * 128 + row;
+          float* dst = p.ws + (((long long)sp * TAPS + u) * p.cin + ci) * p.cout + nt * BN;
+#pragma unroll 1
+          for (int c16 = 0; c16 < BN; c16 += 16) {
+            float v[16];
+            tmem_ld16(tmem + (u * MT + mt) * BN + c16 + ((uint32_t)(quad * 32) << 16), v);
+            tmem_ld_wait();
+            if (ci < p.cin && nt * BN + c16 < p.cout) {
+#pragma unroll
+              for (int q = 0; q < 16; q += 4)
+                *reinterpret_cast<float4*>(dst + c16 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acce_bar);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NLW) tmem_dealloc<L::TCOLS>(tmem);
+}
+
+// dW[co][ci][tap] = sum_s ws[s][tap*cin + ci][co]  (fixed split order), float4 over co
+__global__ void wg_reduce_kernel(const float* __restrict__ ws, int splits, int taps, int cin,
+                                 int cout, int cin_real, float* __restrict__ dw) {
+  const int M = taps * cin;
+  const int n4 = cout >> 2;
+  const int total = M * n4;
+  const long long sstride = (long long)M * cout;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int m = i / n4, c4 = (i - m * n4) * 4;
+    const float* src = ws + (long long)m * cout + c4;
+    float4 acc = *reinterpret_cast<const float4*>(src);
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = *reinterpret_cast<const float4*>(src + s * sstride);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const int tap = m / cin, ci = m - tap * cin;
+    if (ci < cin_real) {
+      const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dw[((long long)(c4 + q) * cin_real + ci) * taps + tap] = a[q];
+    }
+  }
+}
+
+template <int BN, int MT, int TAPS, int KB>
+static int launch_wg(WgParams p, cudaStream_t st) {
+  auto kern = wgrad_kernel<BN, MT, TAPS, KB>;
+  const int cin_pad = p.MG * MT * 128, npad = p.NT * BN;
+  int stages = 8;
+  WgCarve c{};
+  for (; stages >= 2; --stages) {
+    c = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, stages);
+    if (c.total <= SMEM_BUDGET) break;
+  }
+  if (stages < 2) return set_error(BNFF_ERR_UNSUPPORTED, "wgrad window: does not fit shared memory");
+  p.stages = stages;
+  static int attr = 0;
+  if (c.total > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c.total);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(wgrad window)");
+    attr = c.total;
+  }
+  const int grid = p.units < num_sms_wc() ? p.units : num_sms_wc();
+  kern<<<grid, THREADS, c.total, st>>>(p);
+  return check_launch("wgrad window");
+}
+
+// ---------------------------------------------------------------------------
+// weight packing: fp32 (co, ci, kh, kw) -> pre-swizzled bf16 blocks [slab][tap][npad][RB]
+// ---------------------------------------------------------------------------
+__global__ void pack_window_kernel(const float* __restrict__ w, int co_n, int ci_n, int kh, int kw,
+                                   int dgrad, int CI, int N, int npad, int RB, int nslab,
+                                   __nv_bfloat16* __restrict__ out) {
+  const int taps = kh * kw;
+  const int slabw = RB / 2;
+  const long long total = (long long)nslab * taps * npad * slabw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % slabw);
+    long long t = i / slabw;
+    const int n = (int)(t % npad);
+    t /= npad;
+    const int u = (int)(t % taps);
+    const int s = (int)(t / taps);
+    const int ch = s * slabw + k;  // reduction channel
+    float v = 0.f;
+    if (n < N && ch < CI) {
+      int ky = u / kw, kx = u % kw;
+      int co, ci;
+      if (dgrad) { ky = kh - 1 - ky; kx = kw - 1 - kx; co = ch; ci = n; }
+      else { co = n; ci = ch; }
+      v = w[(((long long)co * ci_n + ci) * kh + ky) * kw + kx];
+    }
+    const int kb = k * 2;
+    int chunk = kb >> 4;
+    chunk ^= RB == 128 ? (n & 7) : ((n >> 1) & 3);
+    const long long byte = (((long long)s * taps + u) * npad + n) * RB + chunk * 16 + (kb & 15);
+    out[byte / 2] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int num_sms_wc() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+// GEMM N tile for an output-channel count
+inline int pick_bn(int N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
+inline int pick_rb(int CI) { return CI <= 32 ? 64 : 128; }
+
+struct Geo {
+  int taps, RB, BN, ntiles, npad, nslab;
+};
+inline Geo geo(int CI, int N, int kh, int kw) {
+  Geo g{};
+  g.taps = kh * kw;
+  g.RB = pick_rb(CI);
+  g.BN = pick_bn(N);
+  g.ntiles = (N + g.BN - 1) / g.BN;
+  g.npad = g.ntiles * g.BN;
+  g.nslab = (CI + g.RB / 2 - 1) / (g.RB / 2);
+  return g;
+}
+
+template <int BN, int RB, int TAPS, int MODE>
+static int launch_t(WcParams p, cudaStream_t st) {
+  auto kern = wconv_kernel<BN, RB, TAPS, MODE>;
+  int stages = 8;
+  Carve c{};
+  for (; stages >= 2; --stages) {
+    c = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, stages);
+    if (c.total <= SMEM_BUDGET) break;
+  }
+  if (stages < 2) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: shape does not fit shared memory");
+  p.stages = stages;
+  static int attr = 0;
+  if (c.total > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c.total);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(wconv)");
+    attr = c.total;
+  }
+  const int grid = p.tiles < num_sms_wc() ? p.tiles : num_sms_wc();
+  kern<<<grid, THREADS, c.total, st>>>(p);
+  return check_launch("wconv");
+}
+
+template <int MODE, int TAPS>
+static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st) {
+  if (RB == 64) {
+    switch (BN) {
+      case 32: return launch_t<32, 64, TAPS, MODE>(p, st);
+      case 64: return launch_t<64, 64, TAPS, MODE>(p, st);
+      case 128: return launch_t<128, 64, TAPS, MODE>(p, st);
+      default: return launch_t<256, 64, TAPS, MODE>(p, st);
+    }
+  }
+  switch (BN) {
+    case 32: return launch_t<32, 128, TAPS, MODE>(p, st);
+    case 64: return launch_t<64, 128, TAPS, MODE>(p, st);
+    case 128: return launch_t<128, 128, TAPS, MODE>(p, st);
+    default: return launch_t<256, 128, TAPS, MODE>(p, st);
+  }
+}
+
+}  // namespace wc
+}  // namespace bnff
+
+using namespace bnff;
+
+// eligibility of the window kernels for a conv (bf16, stride 1, 1x1/p0 or 3x3/p1)
+extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
+                              int32_t stride, int32_t pad, int32_t h, int32_t w) {
+  if (dtype != BNFF_BF16 || stride != 1) return 0;
+  if (!((kh == 1 && kw == 1 && pad == 0) || (kh == 3 && kw == 3 && pad == 1))) return 0;
+  if (c_in % 16 || c_out % 16) return 0;
+  if (kh == 3) {
+    const int wp = w + 2;
+    if (128 + 2 * wp + 2 > wc::RMAX) return 0;
+    // resident weights need a single N tile for both passes
+    if (c_out > 256 || c_in > 256) return 0;
+  }
+  (void)h;
+  return 1;
+}
+
+extern "C" int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_t kh,
+                                         int32_t kw, int32_t dgrad) {
+  if (dtype != BNFF_BF16) return 0;
+  const int CI = dgrad ? c_out : c_in, N = dgrad ? c_in : c_out;
+  const wc::Geo g = wc::geo(CI, N, kh, kw);
+  return (int64_t)g.nslab * g.taps * g.npad * (g.RB / 2);  // elements
+}
+
+extern "C" int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t kh,
+                                int32_t kw, void* fwd, void* dgr, void* stream) {
+  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window: bf16 only");
+  for (int d = 0; d < 2; ++d) {
+    void* out = d ? dgr : fwd;
+    if (!out) continue;
+    const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
+    const wc::Geo g = wc::geo(CI, N, kh, kw);
+    const long long total = (long long)g.nslab * g.taps * g.npad * (g.RB / 2);
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    wc::pack_window_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        w, c_out, c_in, kh, kw, d, CI, N, g.npad, g.RB, g.nslab, (__nv_bfloat16*)out);
+    int rc = check_launch("pack_window");
+    if (rc) return rc;
+  }
+  return BNFF_OK;
+}
+
+// internal entry used by bnff_conv_fprop / bnff_conv_dgrad when bnff_window_ok()
+extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
+                                int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
+                                const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
+                                float* stat_part, void* stream) {
+  wc::WcParams p{};
+  p.n = (int)in.n; p.h = (int)in.h; p.w = (int)in.w;
+  p.pad = pad;
+  p.hp = p.h + 2 * pad; p.wp = p.w + 2 * pad;
+  const long long Q = (long long)p.n * p.hp * p.wp;
+  if (Q >= (1ll << 31)) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: grid too large");
+  p.Q = (int)Q;
+  p.R = 128 + (kh == 3 ? 2 * p.wp + 2 : 0);
+  p.fd_hpwp = make_fastdiv(p.hp * p.wp);
+  p.fd_wp = make_fastdiv(p.wp);
+  p.ci = (int)in.c;
+  p.N = (int)out.c;
+  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh);
+  p.nslab = g.nslab;
+  p.npad = g.npad;
+  p.ntiles = g.ntiles;
+  p.mtiles = (p.Q + 127) / 128;
+  p.tiles = p.mtiles * p.ntiles;
+  p.src = (const __nv_bfloat16*)in.ptr; p.src_rs = in.row_stride;
+  p.srcx = (const __nv_bfloat16*)in_x.ptr; p.srcx_rs = in_x.row_stride;
+  p.pro = pro;
+  p.pcoef = pcoef;
+  p.wpk = (const uint8_t*)wwin;
+  p.out = (__nv_bfloat16*)out.ptr; p.out_rs = out.row_stride;
+  p.bias = bias;
+  p.epi = epi;
+  p.ex = (const __nv_bfloat16*)ex.ptr; p.ex_rs = ex.row_stride;
+  p.ecoef = ecoef;
+  p.stat_part = stat_part;
+  if (kh == 3 && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mode == 0) {
+    return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st)
+                   : wc::dispatch<wc::M_FPROP, 1>(p, g.BN, g.RB, st);
+  }
+  return kh == 3 ? wc::dispatch<wc::M_DGRAD, 9>(p, g.BN, g.RB, st)
+                 : wc::dispatch<wc::M_DGRAD, 1>(p, g.BN, g.RB, st);
+}
+
+// ---------------------------------------------------------------------------
+// window wgrad host side
+// ---------------------------------------------------------------------------
+namespace bnff {
+namespace wc {
+struct WgPlan {
+  int ok, taps, BN, MT, KB, NT, MG, RA, nkb, kpt, splits, hp, wp, Q;
+};
+static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
+  WgPlan q{};
+  q.taps = kh * kh;
+  q.hp = h + 2 * pad;
+  q.wp = w + 2 * pad;
+  const long long Q = (long long)n * q.hp * q.wp;
+  if (Q >= (1ll << 30)) return q;
+  q.Q = (int)Q;
+  if (q.taps == 9) {
+    q.BN = 32; q.MT = 1; q.KB = 128;
+    q.RA = align_up(q.KB + 2 * q.wp + 2, 8);
+  } else {
+    q.BN = pick_bn(cout);
+    q.MT = (q.BN <= 128 && cin > 128) ? 2 : 1;
+    q.KB = 64;
+    q.RA = q.KB;
+  }
+  q.NT = (cout + q.BN - 1) / q.BN;
+  q.MG = (cin + q.MT * 128 - 1) / (q.MT * 128);
+  q.nkb = (q.Q + q.KB - 1) / q.KB;
+  const int target = num_sms_wc();
+  int splits = (target + q.MG * q.NT - 1) / (q.MG * q.NT);
+  const int maxs = q.nkb / 4 > 0 ? q.nkb / 4 : 1;  // >= 4 k-blocks per split
+  if (splits > maxs) splits = maxs;
+  if (splits < 1) splits = 1;
+  q.kpt = (q.nkb + splits - 1) / splits;
+  q.splits = (q.nkb + q.kpt - 1) / q.kpt;
+  q.ok = 1;
+  return q;
+}
+
+template <int BN, int MT, int TAPS, int KB>
+static int run_wg(const WgPlan& q, WgParams p, cudaStream_t st) {
+  return launch_wg<BN, MT, TAPS, KB>(p, st);
+}
+}  // namespace wc
+}  // namespace bnff
+
+extern "C" int64_t bnff_window_wgrad_ws(int32_t n, int32_t h, int32_t w, int32_t kh, int32_t c_in,
+                                        int32_t c_out) {
+  const int pad = kh / 2;
+  const wc::WgPlan q = wc::wg_plan(n, h, w, c_in, c_out, kh, pad);
+  if (!q.ok) return 0;
+  return (int64_t)q.splits * q.taps * c_in * c_out;
+}
+
+// dW (and partials) of a window-eligible conv; dbias is left to the caller
+extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
+                                 int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, float* dw,
+                                 int32_t dw_cin, void* stream) {
+  const int pad = kh / 2;
+  const wc::WgPlan q = wc::wg_plan((int)x.n, (int)x.h, (int)x.w, (int)x.c, (int)dy.c, kh, pad);
+  if (!q.ok) return set_error(BNFF_ERR_UNSUPPORTED, "wgrad window: grid too large");
+  wc::WgParams p{};
+  p.n = (int)x.n; p.h = (int)x.h; p.w = (int)x.w; p.hp = q.hp; p.wp = q.wp; p.pad = pad; p.Q = q.Q;
+  p.fd_hpwp = make_fastdiv(q.hp * q.wp);
+  p.fd_wp = make_fastdiv(q.wp);
+  p.cin = (int)x.c; p.cout = (int)dy.c;
+  p.KB = q.KB; p.RA = q.RA; p.nkb = q.nkb; p.kpt = q.kpt; p.splits = q.splits;
+  p.MG = q.MG; p.NT = q.NT; p.units = q.MG * q.NT * q.splits;
+  p.x = (const __nv_bfloat16*)x.ptr; p.x_rs = x.row_stride; p.x_pro = x_pro; p.x_coef = x_coef;
+  p.dy = (const __nv_bfloat16*)dy.ptr; p.dy_rs = dy.row_stride;
+  p.dyx = (const __nv_bfloat16*)dy_x.ptr; p.dyx_rs = dy_x.row_stride;
+  p.dy_pro = dy_pro; p.dy_coef = dy_coef;
+  p.ws = ws;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (q.taps == 9) rc = wc::launch_wg<32, 1, 9, 128>(p, st);
+  else if (q.BN == 32) rc = wc::launch_wg<32, 1, 1, 64>(p, st);
+  else if (q.BN == 64) rc = q.MT == 2 ? wc::launch_wg<64, 2, 1, 64>(p, st) : wc::launch_wg<64, 1, 1, 64>(p, st);
+  else if (q.BN == 128) rc = q.MT == 2 ? wc::launch_wg<128, 2, 1, 64>(p, st) : wc::launch_wg<128, 1, 1, 64>(p, st);
+  else rc = wc::launch_wg<256, 1, 1, 64>(p, st);
+  if (rc) return rc;
+  const int M4 = q.taps * p.cin * (p.cout / 4);
+  int blocks = (M4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  wc::wg_reduce_kernel<<<blocks, 256, 0, st>>>(ws, q.splits, q.taps, p.cin, p.cout,
+                                               dw_cin > 0 ? dw_cin : p.cin, dw);
+  return check_launch("wgrad window reduce");
+}

@@ -129,7 +129,7 @@ class Engine:
     """
 
     def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
-                 save_postrelu: bool = False, lr: float = 0.0):
+                 save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True):
         self.L = _lib.lib()
         self.g = g
         self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
@@ -139,6 +139,8 @@ class Engine:
         self.input_grad = input_grad
         self.save_postrelu = save_postrelu
         self.lr = float(lr)
+        self.use_window = bool(use_window) and self.dcode == _lib.BF16
+        self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
         self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
                               (n.kind == G.CONCAT and not n.attrs.physical) for n in g.nodes)
         self.fwd: list = []
@@ -258,13 +260,24 @@ class Engine:
         self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
                    _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize", launches=3)
 
-    def _pack(self, conv, cin_store):
+    def _pack(self, conv, cin_store, hw=None):
         key = conv.name
         if key not in self.packs:
             n = self.L.bnff_pack_size(self.dcode, conv.out_c, cin_store, conv.kh, conv.kw)
             nt = self.L.bnff_pack_size(self.dcode, cin_store, conv.out_c, conv.kh, conv.kw)
             self.packs[key] = (self._zeros((n,)), self._zeros((nt,)), cin_store, conv)
+            # window-shift kernel weights (bf16 stride-1 1x1/3x3 convs)
+            h, w = hw if hw is not None else (0, 0)
+            if self.use_window and cin_store == conv.in_c and self.L.bnff_window_ok(
+                    self.dcode, conv.in_c, conv.out_c, conv.kh, conv.kw, conv.stride, conv.pad, h, w):
+                nf = self.L.bnff_window_pack_size(self.dcode, conv.out_c, conv.in_c, conv.kh, conv.kw, 0)
+                nd = self.L.bnff_window_pack_size(self.dcode, conv.out_c, conv.in_c, conv.kh, conv.kw, 1)
+                self.wpacks[key] = (self._zeros((nf,)), self._zeros((nd,)), conv)
         return self.packs[key]
+
+    def _wwin(self, conv, which):
+        wp = self.wpacks.get(conv.name)
+        return 0 if wp is None else _ptr(wp[which])
 
     def _bn_tables(self, st: Stats, bn, tag):
         """fp32 (mean, scale, beta, inv) for a normalize prologue (bn_fwd ops.py:246-249)."""
@@ -300,14 +313,14 @@ class Engine:
 
     def _conv_fprop(self, node, x, y, conv, pro, tables, stat_part):
         cin_store = x.shape[3]
-        wp, _, _, _ = self._pack(conv, cin_store)
+        wp, _, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if tables is None:
             cf = coef_of()
         else:
             cf = coef_of(tables[0], tables[1], tables[2])
         args = _lib.FpropArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x),
                               view_of(y), _ptr(wp), _ptr(self.param(f"{conv.name}.bias")), pro, cf,
-                              _ptr(stat_part))
+                              _ptr(stat_part), self._wwin(conv, 0))
         n_, oh_, ow_, co_ = y.shape
         flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
         self._emit(self.L.bnff_conv_fprop, C.byref(args), what=f"fprop {node.name}",
@@ -540,7 +553,7 @@ class Engine:
     def _conv_backward(self, node, conv, x, dy_gv, x_pro, x_tables, dgrad_epi, dgrad_tables):
         """dgrad (+ epilogue) and wgrad of one conv; returns the dx tensor (or None)."""
         cin_store = x.shape[3]
-        wp, wt, _, _ = self._pack(conv, cin_store)
+        wp, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if isinstance(dy_gv, Deferred):
             dy, dy_x, dy_pro, dy_coef = dy_gv.dt1, dy_gv.x, _lib.PRO_BN_DX, dy_gv.coef()
         else:
@@ -555,7 +568,7 @@ class Engine:
                 ecoef = coef_of(m32, s32, b32, i32)
             da = _lib.DgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(dy),
                                 view_of(dy_x), dy_pro, dy_coef, view_of(dx), view_of(x), _ptr(wt),
-                                dgrad_epi, ecoef, _ptr(part))
+                                dgrad_epi, ecoef, _ptr(part), self._wwin(conv, 1))
             self._keep.append(da)
             n_, h_, w_, ci_ = dx.shape
             flops = 2 * n_ * h_ * w_ * ci_ * conv.kh * conv.kw * dy.shape[3]
@@ -730,6 +743,12 @@ class Engine:
         self.repack = []
         self._cur = self.repack
         for name, (wp, wt, cin_s, conv) in self.packs.items():
+            if name in self.wpacks:  # window kernels serve both passes of this conv
+                wf, wd, _ = self.wpacks[name]
+                self._emit(self.L.bnff_pack_window, self.dcode, _ptr(self.param(f"{name}.weight")),
+                           conv.out_c, conv.in_c, conv.kh, conv.kw, _ptr(wf), _ptr(wd),
+                           what="pack_weights", launches=2)
+                continue
             self._emit(self.L.bnff_pack_weights, self.dcode, _ptr(self.param(f"{name}.weight")),
                        conv.out_c, conv.in_c, cin_s, conv.kh, conv.kw, _ptr(wp), _ptr(wt),
                        what="pack_weights")

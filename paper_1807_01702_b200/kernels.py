@@ -99,7 +99,8 @@ def _pixels(t):
 class PackedConv:
     """Device copy of a ConvParams: fp32 master + packed operand layouts."""
 
-    def __init__(self, p: ConvParams, dtype: torch.dtype, device="cuda", cin_store=None):
+    def __init__(self, p: ConvParams, dtype: torch.dtype, device="cuda", cin_store=None,
+                 window: bool = True):
         self.p = p
         self.dcode = _lib.BF16 if dtype == torch.bfloat16 else _lib.F32
         self.cin_store = cin_store or p.in_c
@@ -112,6 +113,15 @@ class PackedConv:
         self.wt = torch.zeros(nt, dtype=dtype, device=device)
         _call(L.bnff_pack_weights, self.dcode, _ptr(self.w32), p.out_c, p.in_c, self.cin_store,
               p.kh, p.kw, _ptr(self.wp), _ptr(self.wt), what="pack_weights")
+        # window-shift kernel weights (used when the conv/input qualifies, bf16 only)
+        self.wf = self.wd = None
+        if window and self.dcode == _lib.BF16 and self.cin_store == p.in_c:
+            nf = L.bnff_window_pack_size(self.dcode, p.out_c, p.in_c, p.kh, p.kw, 0)
+            nd = L.bnff_window_pack_size(self.dcode, p.out_c, p.in_c, p.kh, p.kw, 1)
+            self.wf = torch.zeros(nf, dtype=dtype, device=device)
+            self.wd = torch.zeros(nd, dtype=dtype, device=device)
+            _call(L.bnff_pack_window, self.dcode, _ptr(self.w32), p.out_c, p.in_c, p.kh, p.kw,
+                  _ptr(self.wf), _ptr(self.wd), what="pack_window")
 
 
 def _packed(conv, x):
@@ -133,7 +143,7 @@ def _out_like(x, conv: ConvParams, out):
 def _fprop(x, pc: PackedConv, out, pro, tables, stat_part):
     p = pc.p
     a = _lib.FpropArgs(_dcode(x), p.kh, p.kw, p.stride, p.pad, view(x), view(out), _ptr(pc.wp),
-                       _ptr(pc.bias), pro, coef(*(tables or ())), _ptr(stat_part))
+                       _ptr(pc.bias), pro, coef(*(tables or ())), _ptr(stat_part), _ptr(pc.wf))
     _call(_L().bnff_conv_fprop, C.byref(a), what=f"fprop {p.name}")
 
 
@@ -187,7 +197,7 @@ def _dgrad(dy, pc, dx_shape_like, epi=_lib.DG_PLAIN, x=None, x_tables=None, stat
         dyv, dyx, dpro, dcf = view(dy_pkg[0]), view(dy_pkg[1]), _lib.PRO_BN_DX, coef(*dy_pkg[2])
     xv = view(x) if x is not None else view(dx)
     a = _lib.DgradArgs(_dcode(dx), p.kh, p.kw, p.stride, p.pad, dyv, dyx, dpro, dcf, view(dx), xv,
-                       _ptr(pc.wt), epi, coef(*(x_tables or ())), _ptr(stat_part))
+                       _ptr(pc.wt), epi, coef(*(x_tables or ())), _ptr(stat_part), _ptr(pc.wd))
     _call(_L().bnff_conv_dgrad, C.byref(a), what=f"dgrad {p.name}")
     return dx
 

@@ -1,0 +1,6 @@
+# full GPU validation + measurement pass (used via gpurun)
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
+timeout 600 python tools/profile_step.py --top 40 > gpurun_out/prof_bnff.txt 2>&1; head -22 gpurun_out/prof_bnff.txt
+timeout 600 python tools/profile_step.py --level baseline --top 20 > gpurun_out/prof_base.txt 2>&1; head -3 gpurun_out/prof_base.txt
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-600

@@ -22,12 +22,20 @@ struct ProbeCfg {
   int swap_lbo_sbo; // MN-major: swap the meaning of LBO/SBO
   int row_shift;    // K-major A: start descriptor at this row of a 136-row tile
   int base_off_mode;// 0: base_offset = 0, 1: base_offset = row_shift & 7
+  int k_sw64;       // K-major operands use 64B rows (SW64) instead of 128B (SW128)
+  int mn_kshift;    // MN-major A: start the K rows at this offset of a (K+16)-row tile
 };
 
 // byte offset of (mn, k) for an operand with `rows` MN entries and `K` k entries
-__device__ uint32_t op_off(const ProbeCfg& c, int mn_major, int mn, int k, int rows) {
+__device__ uint32_t op_off(const ProbeCfg& c, int mn_major, int mn, int k, int rows, int krows) {
   const int kb_elems = 128 / c.esize;  // elements of K per 128B row (K-major)
   if (!mn_major) {
+    if (c.k_sw64) {                    // 64B rows: chunk ^= (row>>1)&3 (absolute-address swizzle)
+      int kb = k / (64 / c.esize);
+      int kbyte = (k % (64 / c.esize)) * c.esize;
+      uint32_t off = kb * rows * 64 + mn * 64 + kbyte;
+      return off ^ (((off >> 7) & 3u) << 4);
+    }
     int kb = k / kb_elems;             // K block -> separate region
     int kbyte = (k % kb_elems) * c.esize;
     return kb * rows * 128 + kmajor_sw128_off(mn, kbyte);
@@ -36,10 +44,10 @@ __device__ uint32_t op_off(const ProbeCfg& c, int mn_major, int mn, int k, int r
   uint32_t mnbyte = mn * c.esize;
   uint32_t atom = mnbyte >> 7;
   uint32_t inb = mnbyte & 127;
-  uint32_t atom_bytes = c.K * 128;
+  uint32_t atom_bytes = krows * 128;
   if (c.layout_mn == kLayoutSW64 || c.layout_mn == kLayoutSW32) {
     uint32_t rowb = c.layout_mn == kLayoutSW64 ? 64 : 32;
-    uint32_t atomb = rowb * c.K;  // one atom holds all K rows
+    uint32_t atomb = rowb * krows;  // one atom holds all K rows
     uint32_t a2 = mnbyte / rowb, in2 = mnbyte % rowb;
     uint32_t off = a2 * atomb + k * rowb + in2;
     uint32_t mask = c.layout_mn == kLayoutSW64 ? 3 : 1;
@@ -60,6 +68,7 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
   __shared__ uint32_t tmem_base;
   const int M = 128;
   const int arows = (c.row_shift >= 0 && !c.a_mn) ? 136 : 128;
+  const int akrows = c.K + ((c.mn_kshift > 0 && c.a_mn) ? 16 : 0);
   uint8_t* sa = smem;
   uint8_t* sb = smem + 64 * 1024;
   int tid = threadIdx.x;
@@ -69,17 +78,17 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
     reinterpret_cast<uint32_t*>(sb)[i] = 0;
   }
   __syncthreads();
-  for (int i = tid; i < arows * c.K; i += blockDim.x) {
-    int m = i / c.K, k = i % c.K;
-    float v = A[m * c.K + k];
-    uint32_t off = op_off(c, c.a_mn, m, k, arows);
+  for (int i = tid; i < arows * akrows; i += blockDim.x) {
+    int m = i / akrows, k = i % akrows;
+    float v = A[m * akrows + k];
+    uint32_t off = op_off(c, c.a_mn, m, k, arows, akrows);
     if (c.esize == 2) *reinterpret_cast<__nv_bfloat16*>(sa + off) = __float2bfloat16(v);
     else *reinterpret_cast<float*>(sa + off) = v;
   }
   for (int i = tid; i < c.N * c.K; i += blockDim.x) {
     int n = i / c.K, k = i % c.K;
     float v = B[n * c.K + k];
-    uint32_t off = op_off(c, c.b_mn, n, k, c.N);
+    uint32_t off = op_off(c, c.b_mn, n, k, c.N, c.K);
     if (c.esize == 2) *reinterpret_cast<__nv_bfloat16*>(sb + off) = __float2bfloat16(v);
     else *reinterpret_cast<float*>(sb + off) = v;
   }
@@ -98,19 +107,31 @@ __global__ void probe_kernel(ProbeCfg c, const float* A, const float* B, float* 
     const int kb_elems = 128 / c.esize;
     for (int k0 = 0; k0 < c.K; k0 += ustep) {
       uint64_t ad, bd;
-      if (!c.a_mn) {
+      if (!c.a_mn && c.k_sw64) {
+        int kbe = 64 / c.esize;
+        int kb = k0 / kbe;
+        uint32_t addr = smem_u32(sa) + kb * arows * 64 + (k0 % kbe) * c.esize;
+        int rs = c.row_shift > 0 ? c.row_shift : 0;
+        addr += rs * 64;
+        ad = make_sdesc(addr, 16, 512, kLayoutSW64);
+      } else if (!c.a_mn) {
         int kb = k0 / kb_elems;
         uint32_t addr = smem_u32(sa) + kb * arows * 128 + (k0 % kb_elems) * c.esize;
         int rs = c.row_shift > 0 ? c.row_shift : 0;
         addr += rs * 128;
         ad = make_sdesc(addr, 16, 1024, kLayoutSW128, c.base_off_mode ? (rs & 7) : 0);
       } else {
-        uint32_t addr = smem_u32(sa) + k0 * 128;
-        uint32_t lbo = c.K * 128, sbo = c.mn_kgroup * 128;
+        uint32_t addr = smem_u32(sa) + (k0 + (c.mn_kshift > 0 ? c.mn_kshift : 0)) * 128;
+        uint32_t lbo = akrows * 128, sbo = c.mn_kgroup * 128;
         if (c.swap_lbo_sbo) { uint32_t t = lbo; lbo = sbo; sbo = t; }
         ad = make_sdesc(addr, lbo, sbo, c.layout_mn);
       }
-      if (!c.b_mn) {
+      if (!c.b_mn && c.k_sw64) {
+        int kbe = 64 / c.esize;
+        int kb = k0 / kbe;
+        uint32_t addr = smem_u32(sb) + kb * c.N * 64 + (k0 % kbe) * c.esize;
+        bd = make_sdesc(addr, 16, 512, kLayoutSW64);
+      } else if (!c.b_mn) {
         int kb = k0 / kb_elems;
         uint32_t addr = smem_u32(sb) + kb * c.N * 128 + (k0 % kb_elems) * c.esize;
         bd = make_sdesc(addr, 16, 1024, kLayoutSW128);
@@ -158,7 +179,8 @@ static float round_op(float x, int esize) {
 static int run(const char* name, ProbeCfg c) {
   const int M = 128;
   int arows = (c.row_shift >= 0 && !c.a_mn) ? 136 : 128;
-  std::vector<float> A(arows * c.K), B(c.N * c.K), C(M * c.N), R(M * c.N);
+  int akrows = c.K + ((c.mn_kshift > 0 && c.a_mn) ? 16 : 0);
+  std::vector<float> A(arows * akrows), B(c.N * c.K), C(M * c.N), R(M * c.N);
   srand(1234);
   for (auto& v : A) v = round_op((rand() % 2001 - 1000) / 500.0f, c.esize);
   for (auto& v : B) v = round_op((rand() % 2001 - 1000) / 500.0f, c.esize);
@@ -166,7 +188,8 @@ static int run(const char* name, ProbeCfg c) {
   for (int m = 0; m < M; ++m)
     for (int n = 0; n < c.N; ++n) {
       double s = 0;
-      for (int k = 0; k < c.K; ++k) s += (double)A[(m + rs) * c.K + k] * B[n * c.K + k];
+      int ks = (c.mn_kshift > 0 && c.a_mn) ? c.mn_kshift : 0;
+      for (int k = 0; k < c.K; ++k) s += (double)A[(m + rs) * akrows + k + ks] * B[n * c.K + k];
       R[m * c.N + n] = (float)s;
     }
   float *dA, *dB, *dC;
@@ -228,5 +251,27 @@ int main() {
   run("tf32 MN/MN N128 K64 base32", {4, 1, 1, 128, 64, 1, 4, 0, -1, 0});
   run("bf16 MN/MN N256 K64", {2, 1, 1, 256, 64, 2, 8, 0, -1, 0});
   run("bf16 K/K N256 K64", {2, 0, 0, 256, 64, 2, 8, 0, -1, 0});
+  // round 1b: layouts for the window-shift conv kernels
+  for (int s = 0; s < 8; s += 3) {
+    char nm[64];
+    ProbeCfg c{2, 0, 0, 32, 64, 2, 8, 0, s, 0, 1, 0};
+    snprintf(nm, 64, "bf16 K/K sw64 N32 K64 rowshift %d", s);
+    run(nm, c);
+    c.N = 128;
+    snprintf(nm, 64, "bf16 K/K sw64 N128 K32 rowshift %d", s);
+    c.K = 32;
+    run(nm, c);
+  }
+  for (int s = 1; s < 16; s += 4) {
+    char nm[64];
+    ProbeCfg c{2, 1, 1, 32, 64, 2, 8, 0, -1, 0, 0, s};
+    snprintf(nm, 64, "bf16 MN/MN N32(sw128 B) kshift %d", s);
+    c.layout_mn = kLayoutSW128;
+    run(nm, c);
+  }
+  {
+    ProbeCfg c{2, 1, 1, 128, 64, 2, 8, 0, -1, 0, 0, 5};
+    run("bf16 MN/MN N128 kshift 5", c);
+  }
   return 0;
 }

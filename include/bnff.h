@@ -154,11 +154,21 @@ int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_
                               int32_t dgrad); /* elements */
 int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t kh,
                      int32_t kw, void* wfwd, void* wdgrad, void* stream);
+/* one launch re-packing many convs into the window layouts (after each SGD step);
+ * jobs_dev points at njobs records in DEVICE memory; max_elems = largest pack (elements) */
+typedef struct {
+  const float* w;
+  void* wfwd;
+  void* wdgrad;
+  int32_t c_out, c_in, kh, kw;
+} bnff_pack_job;
+int bnff_pack_window_multi(int32_t dtype, int32_t njobs, const bnff_pack_job* jobs_dev,
+                           int64_t max_elems, void* stream);
 int64_t bnff_window_wgrad_ws(int32_t n, int32_t h, int32_t w, int32_t kh, int32_t c_in,
                              int32_t c_out); /* floats of split partials */
 int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
                       int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, float* dw,
-                      int32_t dw_cin, void* stream);
+                      int32_t dw_cin, float* dbias, void* stream);
 int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                      int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
                      const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,

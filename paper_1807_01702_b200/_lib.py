@@ -54,6 +54,11 @@ class WgradArgs(C.Structure):
                 ("dw_cin", C.c_int32), ("dbias", C.c_void_p)]
 
 
+class PackJob(C.Structure):
+    _fields_ = [("w", C.c_void_p), ("wfwd", C.c_void_p), ("wdgrad", C.c_void_p),
+                ("c_out", C.c_int32), ("c_in", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32)]
+
+
 class GradTerm(C.Structure):
     _fields_ = [("g", View), ("x", View), ("deferred", C.c_int32), ("coef", Coef)]
 
@@ -78,8 +83,9 @@ SIGNATURES = {
     "bnff_window_conv": (C.c_int, [_I32, _I32, _I32, View, View, _I32, Coef, View, _P, _P, _I32,
                                    View, Coef, _P, _P]),
     "bnff_window_wgrad_ws": (_I64, [_I32] * 6),
+    "bnff_pack_window_multi": (C.c_int, [_I32, _I32, _P, _I64, _P]),
     "bnff_window_wgrad": (C.c_int, [View, _I32, Coef, View, View, _I32, Coef, _I32, _P, _P, _I32,
-                                    _P]),
+                                    _P, _P]),
     "bnff_sum_tiles": (_I32, [_I64]),
     "bnff_channel_sums": (C.c_int, [_I32, _I32, View, View, Coef, _P, _P]),
     "bnff_stats_finalize": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P]),

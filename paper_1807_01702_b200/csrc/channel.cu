@@ -58,95 +58,87 @@ __device__ __forceinline__ float bn_dx_elem(float dt, float x, int c, const bnff
   return __fmul_rn(__ldg(cf.e + c), t);
 }
 
-// ---------------------------------------------------------------------------
-// K5: channel sums -> partials [tiles][2][C]
-// ---------------------------------------------------------------------------
-constexpr int kSumThreads = 256;
-constexpr int kMaxTiles = 1184;  // 8 x 148
-
-__host__ __device__ inline int sum_tiles(long long pixels) {
-  long long t = (pixels + 31) / 32;
-  return (int)(t < kMaxTiles ? (t < 1 ? 1 : t) : kMaxTiles);
-}
-
-// mode 0: (x, x^2); mode 1: (dy, dy*xhat) xhat=(x-a)*b; mode 2: (dy', 0) with dy'
-// = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double)
-template <typename T>
-__global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
-                                    bnff_coef cf, const double* mean64, float* part) {
-  constexpr int V = VecIO<T>::V;
-  __shared__ float sh[2][kSumThreads][V];
-  const int cpr = C / V;
-  const int tiles = gridDim.x;
-  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
-  const long long r_begin = blockIdx.x * rows_per_tile;
-  const long long r_end = min(pixels, r_begin + rows_per_tile);
-  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
-    const int ccount = min(kSumThreads, cpr - cbase);
-    const int rows_per_iter = kSumThreads / ccount;
-    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
-    const bool active = trow < rows_per_iter;
-    const int c0 = (cbase + tcol) * V;
-    float s1[V], s2[V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
-    if (active) {
-      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
-        float v[V], x[V];
-        if (mode == 0 || mode == 3) {
-          VecIO<T>::load(xv.p, r * xv.rs + c0, v);
-        } else {
-          VecIO<T>::load(dyv.p, r * dyv.rs + c0, v);
-          if (mode == 1 || cf.e != nullptr) VecIO<T>::load(xv.p, r * xv.rs + c0, x);
-        }
-#pragma unroll
-        for (int i = 0; i < V; ++i) {
-          if (mode == 0) {
-            s1[i] += v[i];
-            s2[i] += v[i] * v[i];
-          } else if (mode == 1) {
-            const float xh = __fmul_rn(__fsub_rn(x[i], __ldg(cf.a + c0 + i)), __ldg(cf.b + c0 + i));
-            s1[i] += v[i];
-            s2[i] += v[i] * xh;
-          } else if (mode == 2) {
-            s1[i] += cf.e != nullptr ? bn_dx_elem(v[i], x[i], c0 + i, cf) : v[i];
-          } else {
-            const float d = (float)((double)v[i] - mean64[c0 + i]);
-            s1[i] += d * d;
-          }
-        }
-      }
+// partials [tiles][2][C] -> float64 totals, one launch: block = 32 channels x 8 row
+// groups; every (row group, channel) sum is a fixed-order loop, then a fixed-order
+// combine of the 8 groups (bitwise deterministic)
+__device__ __forceinline__ void reduce_two(const float* __restrict__ part, int tiles, int C, int c,
+                                           double& o1, double& o2) {
+  __shared__ double sh[2][8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a = 0.0, b = 0.0, a2 = 0.0, b2 = 0.0;
+  if (c < C) {
+    int t = ty;
+    for (; t + 8 < tiles; t += 16) {  // two independent chains for latency
+      a += (double)part[((long long)t * 2 + 0) * C + c];
+      b += (double)part[((long long)t * 2 + 1) * C + c];
+      a2 += (double)part[((long long)(t + 8) * 2 + 0) * C + c];
+      b2 += (double)part[((long long)(t + 8) * 2 + 1) * C + c];
     }
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      sh[0][threadIdx.x][i] = s1[i];
-      sh[1][threadIdx.x][i] = s2[i];
+    for (; t < tiles; t += 8) {
+      a += (double)part[((long long)t * 2 + 0) * C + c];
+      b += (double)part[((long long)t * 2 + 1) * C + c];
     }
-    __syncthreads();
-    // fixed-order combine of the rows_per_iter threads sharing a column
-    if (threadIdx.x < ccount) {
-      float a[V], b[V];
-#pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
-      for (int rr = 0; rr < rows_per_iter; ++rr) {
-#pragma unroll
-        for (int i = 0; i < V; ++i) {
-          a[i] += sh[0][rr * ccount + threadIdx.x][i];
-          b[i] += sh[1][rr * ccount + threadIdx.x][i];
-        }
-      }
-      const int cc = (cbase + threadIdx.x) * V;
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
-        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
-      }
-    }
-    __syncthreads();
+  }
+  sh[0][ty][tx] = a + a2;
+  sh[1][ty][tx] = b + b2;
+  __syncthreads();
+  o1 = o2 = 0.0;
+  if (ty == 0) {
+    for (int k = 0; k < 8; ++k) { o1 += sh[0][k][tx]; o2 += sh[1][k][tx]; }
   }
 }
 
-// partials -> float64 totals: 256 threads per 32 channels, fixed order
+__global__ void __launch_bounds__(256) stats_finalize_kernel(const float* __restrict__ part, int tiles, int C,
+                                                             long long count, double* sum, double* sumsq,
+                                                             double* mean, double* var) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s1, s2;
+  reduce_two(part, tiles, C, c, s1, s2);
+  if ((threadIdx.x >> 5) == 0 && c < C) {
+    sum[c] = s1;
+    sumsq[c] = s2;
+    if (mean && var) {  // ChannelStats.from_sums (ops.py:109-113): population var, clamped
+      const double m = s1 / (double)count;
+      mean[c] = m;
+      const double v = s2 / (double)count - m * m;
+      var[c] = v > 0.0 ? v : 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) dx_coeffs_fused_kernel(
+    const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
+    const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
+    float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double dbeta, dgamma;
+  reduce_two(part, tiles, C, c, dbeta, dgamma);
+  if ((threadIdx.x >> 5) == 0 && c < C) {
+    dbeta64[c] = dbeta;
+    dgamma64[c] = dgamma;
+    const double v = var[c] > 0.0 ? var[c] : 0.0;
+    const double inv = 1.0 / sqrt(v + (double)eps);
+    k1[c] = (float)(dbeta / (double)count);
+    k2[c] = (float)(dgamma / (double)count);
+    g[c] = (float)((double)gamma[c] * inv);
+    mean32[c] = (float)mean[c];
+    inv32[c] = (float)inv;
+    if (dgamma32) dgamma32[c] = (float)dgamma;
+    if (dbeta32) dbeta32[c] = (float)dbeta;
+  }
+}
+
+__global__ void stats_from_sums_kernel(int C, long long count, const double* sum, const double* sumsq,
+                                       double* mean, double* var) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double m = sum[c] / (double)count;
+  mean[c] = m;
+  const double v = sumsq[c] / (double)count - m * m;
+  var[c] = v > 0.0 ? v : 0.0;
+}
+
+// partials -> float64 totals of one slot (kept for the centred-variance path)
 __global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, int C, int slot,
                                     double* __restrict__ out) {
   __shared__ double sh[8][33];
@@ -162,16 +154,6 @@ __global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, i
     for (int k = 0; k < 8; ++k) s += sh[k][tx];
     out[c] = s;
   }
-}
-
-__global__ void stats_from_sums_kernel(int C, long long count, const double* sum, const double* sumsq,
-                                       double* mean, double* var) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const double m = sum[c] / (double)count;
-  mean[c] = m;
-  const double v = sumsq[c] / (double)count - m * m;
-  var[c] = v > 0.0 ? v : 0.0;
 }
 
 __global__ void bn_coeffs_kernel(int C, const double* mean, const double* var, const float* gamma,
@@ -208,24 +190,50 @@ __global__ void dx_coeffs_kernel(int C, long long count, const double* dsum, con
 // ---------------------------------------------------------------------------
 // elementwise families (grid-stride over pixels x chunks)
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void bn_apply_kernel(View x, View y, long long pixels, int C, bnff_coef cf, int relu) {
-  constexpr int V = VecIO<T>::V;
+// Row x chunk mapping shared by the streaming kernels: a thread owns one 16-byte
+// channel chunk j (fixed, so its per-channel coefficients live in registers) and
+// walks pixel rows; rows are split across the block (tpr per iteration) and grid.
+struct RowChunk {
+  int cpr, tpr, j, lane;
+  bool active;
+  __device__ RowChunk(int C, int V) {
+    cpr = C / V;
+    tpr = cpr >= (int)blockDim.x ? 1 : (int)blockDim.x / cpr;
+    j = (int)threadIdx.x % cpr;
+    lane = (int)threadIdx.x / cpr;
+    active = lane < tpr;
+  }
+};
+__host__ inline int rowchunk_grid(long long pixels, int C, int V) {
   const int cpr = C / V;
-  const long long total = pixels * cpr;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / cpr;
-    const int c0 = (int)(i - r * cpr) * V;
-    float f[V];
-    VecIO<T>::load(x.p, r * x.rs + c0, f);
+  const int tpr = cpr >= 256 ? 1 : 256 / cpr;
+  long long b = (pixels + tpr - 1) / tpr;
+  const long long cap = 148 * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bn_apply_kernel(View x, View y, long long pixels, int C,
+                                                       bnff_coef cf, int relu) {
+  constexpr int V = VecIO<T>::V;
+  const RowChunk rc(C, V);
+  if (!rc.active) return;
+  for (int jj = rc.j; jj < rc.cpr; jj += (int)blockDim.x) {
+    const int c0 = jj * V;
+    float a[V], b[V], c[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      float t = __fmul_rn(__fsub_rn(f[k], __ldg(cf.a + c0 + k)), __ldg(cf.b + c0 + k));
-      t = __fadd_rn(t, __ldg(cf.c + c0 + k));
-      f[k] = relu ? fmaxf(t, 0.f) : t;
+    for (int k = 0; k < V; ++k) { a[k] = __ldg(cf.a + c0 + k); b[k] = __ldg(cf.b + c0 + k); c[k] = __ldg(cf.c + c0 + k); }
+    for (long long r = (long long)blockIdx.x * rc.tpr + rc.lane; r < pixels; r += (long long)gridDim.x * rc.tpr) {
+      float f[V];
+      VecIO<T>::load(x.p, r * x.rs + c0, f);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        float t = __fadd_rn(__fmul_rn(__fsub_rn(f[k], a[k]), b[k]), c[k]);  // bn_fwd op order
+        f[k] = relu ? fmaxf(t, 0.f) : t;
+      }
+      VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, f);
     }
-    VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, f);
+    if (rc.cpr < (int)blockDim.x) break;
   }
 }
 
@@ -235,61 +243,201 @@ struct TermDev {
   bnff_coef cf;
 };
 
-template <typename T>
-__global__ void grad_sum_kernel(View out, long long pixels, int C, int accumulate, TermDev t0,
-                                TermDev t1, int nterms) {
-  constexpr int V = VecIO<T>::V;
-  const int cpr = C / V;
-  const long long total = pixels * cpr;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / cpr;
-    const int c0 = (int)(i - r * cpr) * V;
-    float acc[V], v[V], xv[V];
-    VecIO<T>::load(t0.g.p, r * t0.g.rs + c0, v);
-    if (t0.deferred) VecIO<T>::load(t0.x.p, r * t0.x.rs + c0, xv);
+// deferred BN dx coefficients of one chunk.  fp32 storage: the reference's exact op
+// order g*((dt - k1) - xhat*k2), xhat = (x-mean)*inv.  bf16 storage: the same affine
+// map refactored as g*dt + B*x + C (two FMAs; rounding far below bf16 resolution).
+template <typename T, int V>
+struct DxCoef {
+  float m[V], inv[V], k1[V], k2[V], g[V];
+  __device__ void load(const bnff_coef& cf, int c0) {
 #pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = t0.deferred ? bn_dx_elem(v[k], xv[k], c0 + k, t0.cf) : v[k];
-    if (nterms > 1) {
-      VecIO<T>::load(t1.g.p, r * t1.g.rs + c0, v);
-      if (t1.deferred) VecIO<T>::load(t1.x.p, r * t1.x.rs + c0, xv);
+    for (int k = 0; k < V; ++k) {
+      m[k] = __ldg(cf.a + c0 + k); inv[k] = __ldg(cf.b + c0 + k); k1[k] = __ldg(cf.c + c0 + k);
+      k2[k] = __ldg(cf.d + c0 + k); g[k] = __ldg(cf.e + c0 + k);
+    }
+    if constexpr (sizeof(T) == 2) {
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        // round each resolved term to storage precision (the reference materialises it)
-        const float a = VecIO<T>::round(acc[k]);
-        const float b = VecIO<T>::round(t1.deferred ? bn_dx_elem(v[k], xv[k], c0 + k, t1.cf) : v[k]);
-        acc[k] = a + b;
+        const float B = -g[k] * k2[k] * inv[k];
+        const float Cc = g[k] * (k2[k] * inv[k] * m[k] - k1[k]);
+        k1[k] = B;
+        k2[k] = Cc;
       }
     }
-    if (accumulate) {
-      VecIO<T>::load(out.p, r * out.rs + c0, v);
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = v[k] + VecIO<T>::round(acc[k]);
+  }
+  __device__ __forceinline__ float apply(float dt, float x, int k) const {
+    if constexpr (sizeof(T) == 2) {
+      return fmaf(dt, g[k], fmaf(x, k1[k], k2[k]));
+    } else {
+      const float xh = __fmul_rn(__fsub_rn(x, m[k]), inv[k]);
+      const float t = __fsub_rn(__fsub_rn(dt, k1[k]), __fmul_rn(xh, k2[k]));
+      return __fmul_rn(g[k], t);
     }
-    VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, acc);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) grad_sum_kernel(View out, long long pixels, int C, int accumulate,
+                                                       TermDev t0, TermDev t1, int nterms) {
+  constexpr int V = VecIO<T>::V;
+  const RowChunk rc(C, V);
+  if (!rc.active) return;
+  for (int jj = rc.j; jj < rc.cpr; jj += (int)blockDim.x) {
+    const int c0 = jj * V;
+    DxCoef<T, V> d0, d1;
+    if (t0.deferred) d0.load(t0.cf, c0);
+    if (nterms > 1 && t1.deferred) d1.load(t1.cf, c0);
+    for (long long r = (long long)blockIdx.x * rc.tpr + rc.lane; r < pixels; r += (long long)gridDim.x * rc.tpr) {
+      float acc[V], v[V], xv[V];
+      VecIO<T>::load(t0.g.p, r * t0.g.rs + c0, v);
+      if (t0.deferred) VecIO<T>::load(t0.x.p, r * t0.x.rs + c0, xv);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = t0.deferred ? d0.apply(v[k], xv[k], k) : v[k];
+      if (nterms > 1) {
+        VecIO<T>::load(t1.g.p, r * t1.g.rs + c0, v);
+        if (t1.deferred) VecIO<T>::load(t1.x.p, r * t1.x.rs + c0, xv);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          // each resolved term is rounded to storage precision (the reference materialises it)
+          const float a = VecIO<T>::round(acc[k]);
+          const float b = VecIO<T>::round(t1.deferred ? d1.apply(v[k], xv[k], k) : v[k]);
+          acc[k] = a + b;
+        }
+      }
+      if (accumulate) {
+        VecIO<T>::load(out.p, r * out.rs + c0, v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = v[k] + VecIO<T>::round(acc[k]);
+      }
+      VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, acc);
+    }
+    if (rc.cpr < (int)blockDim.x) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: channel sums -> partials [tiles][2][C]
+// ---------------------------------------------------------------------------
+constexpr int kSumThreads = 256;
+constexpr int kMaxTiles = 1184;  // 8 x 148
+
+__host__ __device__ inline int sum_tiles(long long pixels) {
+  long long t = (pixels + 31) / 32;
+  return (int)(t < kMaxTiles ? (t < 1 ? 1 : t) : kMaxTiles);
+}
+
+// mode 0: (x, x^2); mode 1: (dy, dy*xhat) xhat=(x-a)*b; mode 2: (dy', 0) with dy'
+// = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double)
+template <typename T>
+__global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
+                                    bnff_coef cf, const double* mean64, float* part) {
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[2][kSumThreads][V];
+  const int cpr = C / V;
+  const int tiles = gridDim.x;
+  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
+  const long long r_begin = blockIdx.x * rows_per_tile;
+  const long long r_end = min(pixels, r_begin + rows_per_tile);
+  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, cpr - cbase);
+    const int rows_per_iter = kSumThreads / ccount;
+    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
+    const bool active = trow < rows_per_iter;
+    const int c0 = (cbase + tcol) * V;
+    float s1[V], s2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    if (active) {
+      // per-channel coefficients hoisted out of the row loop
+      float ca[V], cb[V];
+      double m64[V];
+      DxCoef<T, V> dxc;
+      const bool dx2 = mode == 2 && cf.e != nullptr;
+      if (mode == 1) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) { ca[i] = __ldg(cf.a + c0 + i); cb[i] = __ldg(cf.b + c0 + i); }
+      } else if (dx2) {
+        dxc.load(cf, c0);
+      } else if (mode == 3) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) m64[i] = mean64[c0 + i];
+      }
+      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+        float v[V], x[V];
+        if (mode == 0 || mode == 3) {
+          VecIO<T>::load(xv.p, r * xv.rs + c0, v);
+        } else {
+          VecIO<T>::load(dyv.p, r * dyv.rs + c0, v);
+          if (mode == 1 || dx2) VecIO<T>::load(xv.p, r * xv.rs + c0, x);
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          if (mode == 0) {
+            s1[i] += v[i];
+            s2[i] += v[i] * v[i];
+          } else if (mode == 1) {
+            const float xh = __fmul_rn(__fsub_rn(x[i], ca[i]), cb[i]);
+            s1[i] += v[i];
+            s2[i] += v[i] * xh;
+          } else if (mode == 2) {
+            s1[i] += dx2 ? dxc.apply(v[i], x[i], i) : v[i];
+          } else {
+            const float d = (float)((double)v[i] - m64[i]);
+            s1[i] += d * d;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sh[0][threadIdx.x][i] = s1[i];
+      sh[1][threadIdx.x][i] = s2[i];
+    }
+    __syncthreads();
+    // fixed-order combine of the rows_per_iter threads sharing a column
+    if (threadIdx.x < ccount) {
+      float a[V], b[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int rr = 0; rr < rows_per_iter; ++rr) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          a[i] += sh[0][rr * ccount + threadIdx.x][i];
+          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+        }
+      }
+      const int cc = (cbase + threadIdx.x) * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+      }
+    }
+    __syncthreads();
   }
 }
 
 template <typename T>
-__global__ void relu_kernel(View x, View dy, View out, long long pixels, int C, int bwd) {
+__global__ void __launch_bounds__(256) relu_kernel(View x, View dy, View out, long long pixels, int C, int bwd) {
   constexpr int V = VecIO<T>::V;
-  const int cpr = C / V;
-  const long long total = pixels * cpr;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / cpr;
-    const int c0 = (int)(i - r * cpr) * V;
-    float f[V], g[V];
-    VecIO<T>::load(x.p, r * x.rs + c0, f);
-    if (bwd) {
-      VecIO<T>::load(dy.p, r * dy.rs + c0, g);
+  const RowChunk rc(C, V);
+  if (!rc.active) return;
+  for (int jj = rc.j; jj < rc.cpr; jj += (int)blockDim.x) {
+    const int c0 = jj * V;
+    for (long long r = (long long)blockIdx.x * rc.tpr + rc.lane; r < pixels; r += (long long)gridDim.x * rc.tpr) {
+      float f[V], g[V];
+      VecIO<T>::load(x.p, r * x.rs + c0, f);
+      if (bwd) {
+        VecIO<T>::load(dy.p, r * dy.rs + c0, g);
 #pragma unroll
-      for (int k = 0; k < V; ++k) f[k] = f[k] > 0.f ? g[k] : 0.f;
-    } else {
+        for (int k = 0; k < V; ++k) f[k] = f[k] > 0.f ? g[k] : 0.f;
+      } else {
 #pragma unroll
-      for (int k = 0; k < V; ++k) f[k] = fmaxf(f[k], 0.f);
+        for (int k = 0; k < V; ++k) f[k] = fmaxf(f[k], 0.f);
+      }
+      VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, f);
     }
-    VecIO<T>::store(const_cast<void*>(out.p), r * out.rs + c0, f);
+    if (rc.cpr < (int)blockDim.x) break;
   }
 }
 
@@ -560,10 +708,7 @@ extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_
 extern "C" int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* sum,
                                    double* sumsq, double* mean, double* var, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  const int g = (c + 31) / 32;
-  reduce_parts_kernel<<<g, 256, 0, st>>>(part, tiles, c, 0, sum);
-  reduce_parts_kernel<<<g, 256, 0, st>>>(part, tiles, c, 1, sumsq);
-  if (mean && var) stats_from_sums_kernel<<<(c + 127) / 128, 128, 0, st>>>(c, count, sum, sumsq, mean, var);
+  stats_finalize_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, count, sum, sumsq, mean, var);
   return check_launch("stats_finalize");
 }
 
@@ -610,11 +755,8 @@ extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64
                               double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
                               float* dgamma32, float* dbeta32, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  const int gr = (c + 31) / 32;
-  reduce_parts_kernel<<<gr, 256, 0, st>>>(part, tiles, c, 0, dbeta64);
-  reduce_parts_kernel<<<gr, 256, 0, st>>>(part, tiles, c, 1, dgamma64);
-  dx_coeffs_kernel<<<(c + 127) / 128, 128, 0, st>>>(c, count, dbeta64, dgamma64, mean, var, gamma, eps, k1,
-                                                     k2, g, mean32, inv32, dgamma32, dbeta32);
+  dx_coeffs_fused_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, count, mean, var, gamma, eps, dgamma64,
+                                                         dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32);
   return check_launch("dx_coeffs");
 }
 
@@ -625,7 +767,7 @@ extern "C" int bnff_bn_apply(int32_t dtype, bnff_view x, bnff_view y, bnff_coef 
   if (!same_dims(x, y)) return set_error(BNFF_ERR_SHAPE, "bn_apply: x/y dims differ");
   if (!coef.a || !coef.b || !coef.c) return set_error(BNFF_ERR_STATE, "bn_apply: missing statistics");
   const long long pixels = x.n * x.h * x.w;
-  BNFF_DISPATCH(dtype, bn_apply_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+  BNFF_DISPATCH(dtype, bn_apply_kernel, rowchunk_grid(pixels, (int)x.c, dtype == BNFF_BF16 ? 8 : 4), 256, 0,
                 (cudaStream_t)stream, vw(x), vw(y), pixels, (int)x.c, coef, relu);
   return check_launch("bn_apply");
 }
@@ -646,7 +788,7 @@ extern "C" int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, c
     td[i].cf = terms[i].coef;
   }
   const long long pixels = out.n * out.h * out.w;
-  BNFF_DISPATCH(dtype, grad_sum_kernel, grid_for(pixels * out.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+  BNFF_DISPATCH(dtype, grad_sum_kernel, rowchunk_grid(pixels, (int)out.c, dtype == BNFF_BF16 ? 8 : 4), 256, 0,
                 (cudaStream_t)stream, vw(out), pixels, (int)out.c, accumulate, td[0], td[1], nterms);
   return check_launch("grad_sum");
 }
@@ -655,7 +797,7 @@ extern "C" int bnff_relu_fwd(int32_t dtype, bnff_view x, bnff_view y, void* stre
   int rc;
   if ((rc = check_view(dtype, x, "relu x")) || (rc = check_view(dtype, y, "relu y"))) return rc;
   const long long pixels = x.n * x.h * x.w;
-  BNFF_DISPATCH(dtype, relu_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+  BNFF_DISPATCH(dtype, relu_kernel, rowchunk_grid(pixels, (int)x.c, dtype == BNFF_BF16 ? 8 : 4), 256, 0,
                 (cudaStream_t)stream, vw(x), vw(x), vw(y), pixels, (int)x.c, 0);
   return check_launch("relu_fwd");
 }
@@ -667,7 +809,7 @@ extern "C" int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view
     return rc;
   if (!same_dims(x, dy)) return set_error(BNFF_ERR_SHAPE, "relu_bwd: shape mismatch");
   const long long pixels = x.n * x.h * x.w;
-  BNFF_DISPATCH(dtype, relu_kernel, grid_for(pixels * x.c / (dtype == BNFF_BF16 ? 8 : 4)), 256, 0,
+  BNFF_DISPATCH(dtype, relu_kernel, rowchunk_grid(pixels, (int)x.c, dtype == BNFF_BF16 ? 8 : 4), 256, 0,
                 (cudaStream_t)stream, vw(x), vw(dy), vw(dx), pixels, (int)x.c, 1);
   return check_launch("relu_bwd");
 }

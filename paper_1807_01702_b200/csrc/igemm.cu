@@ -704,6 +704,8 @@ static inline int kpad_elems(int dtype, int k) {
   return (k + kb - 1) / kb * kb;
 }
 
+static constexpr int kWindowNoFitAbi = -100;  // wconv.cu: shape does not fit its smem plan
+
 static int check_common(int dtype, const bnff_view& v, const char* what) {
   const int vec = dtype == BNFF_BF16 ? 8 : 4;
   if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "dtype %d", dtype);
@@ -734,8 +736,9 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
     return set_error(BNFF_ERR_STATE, "fprop: missing statistics for the normalize prologue");
   if (a->wwin && bnff_window_ok(a->dtype, (int)a->x.c, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     bnff_view none{};
-    return bnff_window_conv(0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin, a->bias,
-                            0, none, bnff_coef{}, a->stat_part, stream);
+    const int wrc = bnff_window_conv(0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin,
+                                     a->bias, 0, none, bnff_coef{}, a->stat_part, stream);
+    if (wrc != kWindowNoFitAbi) return wrc;
   }
   p.M = p.n * p.oh * p.ow;
   p.N = p.cout;
@@ -769,9 +772,10 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   if (a->wwin && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     if (a->dy_pro == BNFF_PRO_BN_DX && (!a->dy_coef.a || !a->dy_coef.e))
       return set_error(BNFF_ERR_STATE, "dgrad: missing deferred-gradient coefficients");
-    return bnff_window_conv(1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx, a->wwin,
-                            nullptr, a->epi, a->x, a->x_coef,
-                            a->epi == BNFF_DG_NRC ? a->stat_part : nullptr, stream);
+    const int wrc = bnff_window_conv(1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx,
+                                     a->wwin, nullptr, a->epi, a->x, a->x_coef,
+                                     a->epi == BNFF_DG_NRC ? a->stat_part : nullptr, stream);
+    if (wrc != kWindowNoFitAbi) return wrc;
   }
   p.M = p.n * p.h * p.w;
   p.N = p.cin;
@@ -852,15 +856,11 @@ extern "C" int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream) {
   if (a->splits >= 0 && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     // window-shift kernel (splits < 0 forces the generic path)
     int rc2 = bnff_window_wgrad(a->x, a->x_pro, a->x_coef, a->dy, a->dy_x, a->dy_pro, a->dy_coef, p.kh,
-                                a->workspace, a->dw, a->dw_cin, stream);
-    if (rc2) return rc2;
-    if (a->dbias != nullptr) {
-      const long long used = bnff_window_wgrad_ws(p.n, p.h, p.w, p.kh, p.cin, p.cout);
-      return bnff_dbias_scratch(a->dtype, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->workspace + used,
-                                a->dbias, stream);
-    }
-    return BNFF_OK;
+                                a->workspace, a->dw, a->dw_cin, a->dbias, stream);
+    if (rc2 == kWindowNoFitAbi) goto generic;
+    return rc2;
   }
+generic:
   const int taps = p.kh * p.kw;
   p.M = taps * p.cin;
   p.N = p.cout;

@@ -36,9 +36,12 @@ namespace wc {
 enum { M_FPROP = 0, M_DGRAD = 1 };
 constexpr int NLW = 8;                  // loader warps
 constexpr int LT = NLW * 32;            // loader threads
-constexpr int THREADS = (NLW + 1 + 4) * 32;
+constexpr int THREADS = (NLW + 1 + 4) * 32;      // wgrad kernel: 4 epilogue warps
+constexpr int NEW = 8;                           // wconv: epilogue warps (2 groups of 4)
+constexpr int WC_THREADS = (NLW + 1 + NEW) * 32;
 constexpr int RMAX = 256;               // max window rows (wp <= 63 for 3x3)
 constexpr int SMEM_BUDGET = 225 * 1024;
+constexpr int kWindowNoFit = -100;      // internal: shape does not fit, use the generic kernel
 
 struct WcParams {
   int n, h, w, hp, wp, pad, Q, mtiles, ntiles, tiles, R, stages;
@@ -67,10 +70,13 @@ struct Layout {
   static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
   static constexpr bool WRES = TAPS == 9;            // weights resident in smem
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
-  static constexpr int CW = MODE == M_DGRAD ? 32 : (BN < 64 ? BN : 64);  // epilogue column chunk
+  // epilogue column chunk: two groups of 4 warps take alternate chunks
+  static constexpr int CW = BN <= 32 || (MODE == M_DGRAD && BN == 256) ? 16
+                           : (MODE == M_DGRAD || BN == 64 ? 32 : 64);
+  static constexpr int NCH = BN / CW;                // chunks per tile (>= 2)
   static constexpr int SROWB = CW * 2 + 16;          // staging row pitch (bytes)
   static constexpr int STG = 128 * SROWB;
-  static constexpr int NSTG = MODE == M_DGRAD ? 4 : 1;  // dgrad: dt1, dt1*xhat, x[2]
+  static constexpr int NSTG = MODE == M_DGRAD ? 3 : 1;  // per group: out tile (+ x[2] for dgrad)
   static constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr uint32_t LAY = RB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr uint32_t SBO = 8 * RB;
@@ -82,32 +88,32 @@ struct Carve {
 };
 
 template <int BN, int RB, int TAPS, int MODE>
-__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages) {
+__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop) {
   using L = Layout<BN, RB, TAPS, MODE>;
   Carve c{};
   int off = 0;
   c.wres = off;
   if (L::WRES) off += align_up(nslab * TAPS * BN * RB, 1024);
   c.a_bytes = align_up(R * RB, 1024);
-  c.stage_bytes = c.a_bytes * (L::XOP ? 2 : 1) + (L::WRES ? 0 : BN * RB);
+  c.stage_bytes = c.a_bytes * (xop ? 2 : 1) + (L::WRES ? 0 : BN * RB);
   c.stage0 = off;
   off += stages * c.stage_bytes;
   c.stg = off;
-  off += L::NSTG * L::STG;
+  off += 2 * L::NSTG * L::STG;
   c.ptab = off;
   off += 3 * nslab * L::SLABW * 4;
   c.etab = off;
-  off += 4 * npad * 4;
+  off += (MODE == M_DGRAD ? 4 : 1) * npad * 4;  // bias | NRC (scale, shift, inv, -mean*inv)
   c.sacc = off;
   off += 2 * npad * 4;
   c.red = off;
-  off += 4 * 128 * 4;
+  off += 2 * 4 * 128 * 4;
   c.rowtab = off;
   off += 2 * RMAX * 4;
   c.rowpix = off;
   off += 128 * 4;
   c.meta = off;
-  off += 8 * LT * 4;
+  off += stages * LT * 4;
   c.total = off + 1024;  // + alignment slack
   return c;
 }
@@ -148,7 +154,7 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 }
 
 template <int BN, int RB, int TAPS, int MODE>
-__global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
+__global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) {
   using L = Layout<BN, RB, TAPS, MODE>;
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
@@ -156,7 +162,8 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
                                              ~uintptr_t(1023));
   __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], w_bar;
   __shared__ uint32_t tmem_sh;
-  const Carve cv = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, p.stages);
+  const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
+  const Carve cv = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, p.stages, xop_s);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* etab = reinterpret_cast<float*>(smem + cv.etab);
@@ -177,13 +184,13 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
       mbar_init(&full_bar[s], LT + (L::WRES ? 0 : 1));
       mbar_init(&empty_bar[s], 1);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], 128); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], NEW * 32); }
     mbar_init(&w_bar, 1);
     fence_mbar_init();
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
   // window-operand tables: BN_RELU: (scale, beta - mean*scale); BN_DX: (g, -g*k2*inv, g*(k2*inv*mean-k1))
-  for (int c = tid; c < kpad; c += THREADS) {
+  for (int c = tid; c < kpad; c += WC_THREADS) {
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
     if (c < p.ci) {
       if (p.pro == BNFF_PRO_BN_RELU) {
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
     ptab[2 * kpad + c] = t2;
   }
   // epilogue tables: FPROP: bias; DGRAD NRC: (scale, beta-mean*scale, inv, -mean*inv)
-  for (int c = tid; c < p.npad; c += THREADS) {
+  for (int c = tid; c < p.npad; c += WC_THREADS) {
     float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
     if (c < p.N) {
       if (MODE == M_FPROP) {
@@ -217,9 +224,11 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
       }
     }
     etab[c] = t0;
-    etab[p.npad + c] = t1;
-    etab[2 * p.npad + c] = t2;
-    etab[3 * p.npad + c] = t3;
+    if (MODE == M_DGRAD) {
+      etab[p.npad + c] = t1;
+      etab[2 * p.npad + c] = t2;
+      etab[3 * p.npad + c] = t3;
+    }
     sacc[c] = 0.f;
     sacc[p.npad + c] = 0.f;
   }
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
   auto stage_a = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes; };
   auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes; };
   auto stage_b = [&](int s) {
-    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (L::XOP ? 2 : 1);
+    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (xop_s ? 2 : 1);
   };
   auto tile_of = [&](int it, int& q0, int& n0) {
     const int t = (int)blockIdx.x + it * (int)gridDim.x;
@@ -396,20 +405,33 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
     __syncwarp();
   } else {
     // =============================== epilogue ===============================
+    // 8 warps = 2 groups x 4 (one warp per TMEM lane quadrant in each group); group h
+    // drains column chunks h, h+2, ...  Per chunk: row pass (TMEM -> fp32 epilogue math
+    // -> bf16 staging, thread = row), column pass (per-channel sums of the STAGED values,
+    // thread = column pair, accumulated in registers across tiles), store pass
+    // (coalesced 16B stores into the NHWC view).
     const int quad = warp & 3;
-    const int et = tid - (NLW + 1) * 32;  // 0..127
+    const int et = tid - (NLW + 1) * 32;     // 0..255
+    const int grp = et >> 7;                 // 0 / 1
+    const int gt = et & 127;
     const int row = quad * 32 + lane;
-    uint8_t* stg = smem + cv.stg;
-    uint8_t* stg2 = stg + L::STG;
-    uint8_t* xs0 = stg + 2 * L::STG;       // dgrad: double-buffered x chunk (own row)
+    const int bar_id = 2 + grp;
+    uint8_t* stg = smem + cv.stg + grp * L::NSTG * L::STG;
+    uint8_t* xs0 = stg + L::STG;             // dgrad: double-buffered x chunk (own row)
+    float* gred = red + grp * 512;
     const int hpwp = p.hp * p.wp;
+    constexpr int CW = L::CW, NCH = L::NCH;
     constexpr int HALF = CW / 2;             // column pairs per chunk
     constexpr int RG = 128 / HALF;           // row groups in the column pass
-    constexpr int NCH = BN / CW;             // column chunks per tile
-    const int cp = et % HALF, rg = et / HALF;
+    constexpr int MYCH = (NCH + 1) / 2;      // chunks per group per tile (upper bound)
+    const int cp = gt % HALF, rg = gt / HALF;
     const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
     const bool nrc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC;
-    // x chunk prefetch (own row, CW channels) into xs[buf]
+    const bool stats = do_stats && (MODE == M_FPROP || nrc);
+    const bool persist = p.ntiles == 1;      // same columns every tile: keep sums in registers
+    float2 acc1[MYCH], acc2[MYCH];
+#pragma unroll
+    for (int k = 0; k < MYCH; ++k) { acc1[k] = make_float2(0.f, 0.f); acc2[k] = make_float2(0.f, 0.f); }
     auto fetch_x = [&](int pix, int n0, int cc, int b) {
       const uint32_t dst = smem_u32(xs0 + b * L::STG + row * L::SROWB);
       const int col = n0 + cc;
@@ -419,9 +441,34 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
         cp_async16(dst + i * 16, p.ex + (ok ? (long long)pix * p.ex_rs + col + i * 8 : 0), ok ? 16u : 0u);
       cp_async_commit();
     };
+    // fixed-order combine of the register sums of one chunk into the per-CTA sums
+    auto flush = [&](int k, int n0, int cc) {
+      gred[(rg * 4 + 0) * HALF + cp] = acc1[k].x;
+      gred[(rg * 4 + 1) * HALF + cp] = acc1[k].y;
+      gred[(rg * 4 + 2) * HALF + cp] = acc2[k].x;
+      gred[(rg * 4 + 3) * HALF + cp] = acc2[k].y;
+      acc1[k] = make_float2(0.f, 0.f);
+      acc2[k] = make_float2(0.f, 0.f);
+      named_bar_sync(bar_id, 128);
+      if (gt < CW) {
+        const int c = gt, pc = c >> 1, odd = c & 1;
+        float s1 = 0.f, s2 = 0.f;
+        for (int q = 0; q < RG; ++q) {
+          s1 += gred[(q * 4 + odd) * HALF + pc];
+          s2 += gred[(q * 4 + 2 + odd) * HALF + pc];
+        }
+        const int gcol = n0 + cc + c;
+        if (gcol < p.N) {
+          sacc[gcol] += s1;
+          sacc[p.npad + gcol] += s2;
+        }
+      }
+      named_bar_sync(bar_id, 128);
+    };
+    int n0 = 0;
     for (int it = 0; it < ntl; ++it) {
       const int buf = it & 1;
-      int q0, n0;
+      int q0;
       tile_of(it, q0, n0);
       int pix = -1;
       {
@@ -435,30 +482,30 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
           if (py < p.h && px < p.w) pix = (img * p.h + py) * p.w + px;
         }
       }
-      rowpix[row] = pix;
-      if (need_x) fetch_x(pix, n0, 0, 0);
+      if (need_x) fetch_x(pix, n0, grp * CW, 0);
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int ci = 0; ci < NCH; ++ci) {
+#pragma unroll
+      for (int k = 0; k < MYCH; ++k) {
+        const int ci = grp + 2 * k;
+        if (ci >= NCH) break;
         const int cc = ci * CW;
         if (need_x) {
-          if (ci + 1 < NCH) {
-            fetch_x(pix, n0, cc + CW, (ci + 1) & 1);
+          if (ci + 2 < NCH) {
+            fetch_x(pix, n0, cc + 2 * CW, (k + 1) & 1);
             cp_async_wait<1>();
           } else {
             cp_async_wait<0>();
           }
         }
-        const uint8_t* xrow = xs0 + (ci & 1) * L::STG + row * L::SROWB;
-        // ---- row pass: TMEM -> fp32 -> epilogue math -> bf16 staging
+        const uint8_t* xrow = xs0 + (k & 1) * L::STG + row * L::SROWB;
+        // ---- row pass
 #pragma unroll
         for (int c16 = 0; c16 < CW; c16 += 16) {
           float v[16];
           tmem_ld16(tmem + buf * BN + cc + c16 + ((uint32_t)(quad * 32) << 16), v);
           tmem_ld_wait();
           const int gc = n0 + cc + c16;
-          float xh[16];
           if (MODE == M_FPROP) {
             float bv[16];
             ld16f(etab + gc, bv);
@@ -473,17 +520,11 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = xv[i] > 0.f ? v[i] : 0.f;
               } else {
-                float e0[16], e1[16], e2[16], e3[16];
+                float e0[16], e1[16];
                 ld16f(etab + gc, e0);
                 ld16f(etab + p.npad + gc, e1);
-                ld16f(etab + 2 * p.npad + gc, e2);
-                ld16f(etab + 3 * p.npad + gc, e3);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  const float t = fmaf(xv[i], e0[i], e1[i]);
-                  v[i] = t > 0.f ? v[i] : 0.f;
-                  xh[i] = fmaf(xv[i], e2[i], e3[i]);
-                }
+                for (int i = 0; i < 16; ++i) v[i] = fmaf(xv[i], e0[i], e1[i]) > 0.f ? v[i] : 0.f;
               }
             }
             if (pix < 0) {
@@ -491,81 +532,78 @@ __global__ void __launch_bounds__(THREADS, 1) wconv_kernel(const WcParams p) {
               for (int i = 0; i < 16; ++i) v[i] = 0.f;
             }
           }
-          const uint4 o0 = pack8(v, false), o1 = pack8(v + 8, false);
           uint4* sp = reinterpret_cast<uint4*>(stg + row * L::SROWB + c16 * 2);
-          sp[0] = o0;
-          sp[1] = o1;
-          if (nrc) {
-            float r[16];
-            unpack8(o0, r);
-            unpack8(o1, r + 8);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] *= xh[i];
-            uint4* sp2 = reinterpret_cast<uint4*>(stg2 + row * L::SROWB + c16 * 2);
-            sp2[0] = pack8(r, false);
-            sp2[1] = pack8(r + 8, false);
-          }
+          sp[0] = pack8(v, false);
+          sp[1] = pack8(v + 8, false);
         }
-        if (ci == NCH - 1) {
+        if (ci + 2 >= NCH) {
           tc_fence_before();
-          mbar_arrive(&acce_bar[buf]);  // accumulator slot drained
+          mbar_arrive(&acce_bar[buf]);  // this group is done with the accumulator slot
         }
-        named_bar_sync(2, 128);
-        // ---- column pass: per-channel sums of the staged (stored) values
-        if (do_stats && (MODE == M_FPROP || nrc)) {
-          float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+        named_bar_sync(bar_id, 128);
+        // ---- column pass: sums of the stored values (FPROP: y, y^2; NRC: dt1, dt1*xhat)
+        if (stats) {
           const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
-          const uint32_t* s32b = reinterpret_cast<const uint32_t*>(stg2);
+          float2 a = acc1[k], b = acc2[k];
+          if (MODE == M_FPROP) {
 #pragma unroll 4
-          for (int r = rg; r < 128; r += RG) {
-            const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
-            const float lo = bf16lo(wv), hi = bf16hi(wv);
-            a0 += lo;
-            a1 += hi;
-            if (MODE == M_FPROP) {
-              b0 = fmaf(lo, lo, b0);
-              b1 = fmaf(hi, hi, b1);
-            } else {
-              const uint32_t w2 = s32b[r * (L::SROWB / 4) + cp];
-              b0 += bf16lo(w2);
-              b1 += bf16hi(w2);
+            for (int r = rg; r < 128; r += RG) {
+              const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
+              const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
+              a = __fadd2_rn(a, f);
+              b = __ffma2_rn(f, f, b);
+            }
+          } else {
+            const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs0 + (k & 1) * L::STG);
+            const int gc = n0 + cc + 2 * cp;
+            const float2 hinv = make_float2(etab[2 * p.npad + gc], etab[2 * p.npad + gc + 1]);
+            const float2 hsh = make_float2(etab[3 * p.npad + gc], etab[3 * p.npad + gc + 1]);
+#pragma unroll 4
+            for (int r = rg; r < 128; r += RG) {
+              const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
+              const uint32_t xw = x32[r * (L::SROWB / 4) + cp];
+              const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
+              const float2 xh = __ffma2_rn(make_float2(bf16lo(xw), bf16hi(xw)), hinv, hsh);
+              a = __fadd2_rn(a, f);
+              b = __ffma2_rn(f, xh, b);
             }
           }
-          red[(rg * 4 + 0) * HALF + cp] = a0;
-          red[(rg * 4 + 1) * HALF + cp] = a1;
-          red[(rg * 4 + 2) * HALF + cp] = b0;
-          red[(rg * 4 + 3) * HALF + cp] = b1;
-          named_bar_sync(2, 128);
-          if (et < CW) {
-            const int c = et, pc = c >> 1, odd = c & 1;
-            float s1 = 0.f, s2 = 0.f;
-            for (int k = 0; k < RG; ++k) {
-              s1 += red[(k * 4 + odd) * HALF + pc];
-              s2 += red[(k * 4 + 2 + odd) * HALF + pc];
-            }
-            const int gcol = n0 + cc + c;
-            if (gcol < p.N) {
-              sacc[gcol] += s1;
-              sacc[p.npad + gcol] += s2;
-            }
-          }
+          acc1[k] = a;
+          acc2[k] = b;
         }
-        // ---- store pass: staged rows -> NHWC view (coalesced 16B stores)
+        // ---- store pass
         constexpr int CPO = CW / 8;  // 16B chunks per staged row
-        for (int k = et; k < 128 * CPO; k += 128) {
-          const int r = k / CPO, ch = k - r * CPO;
-          const int px = rowpix[r];
+#pragma unroll 2
+        for (int kk = gt; kk < 128 * CPO; kk += 128) {
+          const int r = kk / CPO, ch = kk - r * CPO;
+          const int q = q0 + r;
+          int px = -1;
+          if (q < p.Q) {
+            const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
+            const int rem = q - img * hpwp;
+            const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
+            const int pxx = rem - py * p.wp;
+            if (py < p.h && pxx < p.w) px = (img * p.h + py) * p.w + pxx;
+          }
           const int col = n0 + cc + ch * 8;
           if (px >= 0 && col < p.N) {
             const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
             *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
           }
         }
-        named_bar_sync(2, 128);
+        named_bar_sync(bar_id, 128);
+        if (stats && !persist) flush(k, n0, cc);
       }
     }
+    if (stats && persist) {
+#pragma unroll
+      for (int k = 0; k < MYCH; ++k)
+        if (grp + 2 * k < NCH) flush(k, 0, (grp + 2 * k) * CW);
+    }
+    // both groups' sums are in sacc; write this CTA's partial row
+    asm volatile("bar.sync 4, %0;" ::"n"(NEW * 32) : "memory");
     if (do_stats) {
-      for (int c = et; c < p.N; c += 128) {
+      for (int c = et; c < p.N; c += NEW * 32) {
         p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + c] = sacc[c];
         p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + c] = sacc[p.npad + c];
       }
@@ -599,6 +637,7 @@ struct WgParams {
   int dy_pro;
   bnff_coef dy_coef;
   float* ws;
+  float* wsb;  // nullable: dbias partials [splits][cout] (m-group 0 units)
 };
 
 template <int BN, int MT, int TAPS, int KB>
@@ -619,7 +658,7 @@ struct WgL {
 };
 
 struct WgCarve {
-  int stage_bytes, a_bytes, b_bytes, ptab, qtab, rowx, rowg, meta, total;
+  int stage_bytes, a_bytes, b_bytes, ptab, qtab, rowx, rowg, meta, bred, total;
 };
 template <int BN, int MT, int TAPS, int KB>
 __host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int stages) {
@@ -638,6 +677,8 @@ __host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int s
   c.rowg = off;
   off += 2 * KB * 4;
   c.meta = off;
+  off += 8 * LT * 4;
+  c.bred = off;
   off += 8 * LT * 4;
   c.total = off + 1024;
   return c;
@@ -659,6 +700,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
   int* rowx = reinterpret_cast<int*>(smem + cv.rowx);
   int* rowg = reinterpret_cast<int*>(smem + cv.rowg);
   uint32_t* meta = reinterpret_cast<uint32_t*>(smem + cv.meta);
+  float* bred = reinterpret_cast<float*>(smem + cv.bred);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nun = (p.units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
@@ -726,6 +768,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
     if (nun > 0) { unit_of(0, imgi, inti, isp); icnt = kb_count(isp); }
     // transform-side cursor
     int tu = 0, tk = 0, tmg = 0, tnt = 0, tsp = 0, tcnt = 0;
+    float bacc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bacc[i] = 0.f;
     if (nun > 0) { unit_of(0, tmg, tnt, tsp); tcnt = kb_count(tsp); }
     (void)tu; (void)tk; (void)tsp;
     for (int g = 0; g < G + LAG; ++g) {
@@ -851,9 +896,42 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
             }
           }
         }
+        // dbias = sum over positions of the (transformed) dy rows (m-group 0 units only)
+        if (p.wsb != nullptr && tmg == 0) {
+          const int co0 = tnt * BN + jb * 8;
+          if (co0 < p.cout) {
+            const uint8_t* B = stage_b(st);
+#pragma unroll
+            for (int k = 0; k < L::UB; ++k) {
+              if (!((mask >> (24 + k)) & 1u)) continue;
+              const int r = rb0 + RBS * k;
+              const int b = jb / L::BCPR, jj = jb % L::BCPR;
+              uint32_t off = b * KB * L::BRB + r * L::BRB;
+              if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
+              else off += (jj ^ ((r >> 1) & 3)) << 4;
+              float f[8];
+              unpack8(*reinterpret_cast<const uint4*>(B + off), f);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) bacc[i] += f[i];
+            }
+          }
+        }
         fence_proxy_async_smem();
         mbar_arrive(&full_bar[st]);
         if (++tk == tcnt) {
+          if (p.wsb != nullptr && tmg == 0) {  // fixed-order combine of the unit's dbias partials
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { bred[i * LT + tid] = bacc[i]; bacc[i] = 0.f; }
+            named_bar_sync(1, LT);
+            if (tid < L::BCH * 8) {
+              const int jc = tid >> 3, i = tid & 7;
+              const int co = tnt * BN + jc * 8 + i;
+              float sacc = 0.f;
+              for (int t = jc; t < LT; t += L::BCH) sacc += bred[i * LT + t];
+              if (co < p.cout) p.wsb[(long long)tsp * p.cout + co] = sacc;
+            }
+            named_bar_sync(1, LT);
+          }
           tk = 0;
           if (++tu < nun) { unit_of(tu, tmg, tnt, tsp); tcnt = kb_count(tsp); }
         }
@@ -935,7 +1013,15 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
 
 // dW[co][ci][tap] = sum_s ws[s][tap*cin + ci][co]  (fixed split order), float4 over co
 __global__ void wg_reduce_kernel(const float* __restrict__ ws, int splits, int taps, int cin,
-                                 int cout, int cin_real, float* __restrict__ dw) {
+                                 int cout, int cin_real, float* __restrict__ dw,
+                                 const float* __restrict__ wsb, float* __restrict__ dbias) {
+  if (dbias != nullptr && blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < cout; c += blockDim.x) {
+      float a = 0.f;
+      for (int s = 0; s < splits; ++s) a += wsb[(long long)s * cout + c];
+      dbias[c] = a;
+    }
+  }
   const int M = taps * cin;
   const int n4 = cout >> 2;
   const int total = M * n4;
@@ -967,7 +1053,7 @@ static int launch_wg(WgParams p, cudaStream_t st) {
     c = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, stages);
     if (c.total <= SMEM_BUDGET) break;
   }
-  if (stages < 2) return set_error(BNFF_ERR_UNSUPPORTED, "wgrad window: does not fit shared memory");
+  if (stages < 2) return kWindowNoFit;
   p.stages = stages;
   static int attr = 0;
   if (c.total > attr) {
@@ -1014,6 +1100,45 @@ __global__ void pack_window_kernel(const float* __restrict__ w, int co_n, int ci
   }
 }
 
+// one launch re-packing many convs (after each optimizer step): grid (x, job, fwd|dgrad)
+__global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs) {
+  const bnff_pack_job jb = jobs[blockIdx.y];
+  const int d = blockIdx.z;
+  void* out = d ? jb.wdgrad : jb.wfwd;
+  if (!out) return;
+  const int CI = d ? jb.c_out : jb.c_in, N = d ? jb.c_in : jb.c_out;
+  const int taps = jb.kh * jb.kw;
+  const int RB = CI <= 32 ? 64 : 128;
+  const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  const int npad = (N + BN - 1) / BN * BN;
+  const int slabw = RB / 2;
+  const int nslab = (CI + slabw - 1) / slabw;
+  const long long total = (long long)nslab * taps * npad * slabw;
+  __nv_bfloat16* o = (__nv_bfloat16*)out;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % slabw);
+    long long t = i / slabw;
+    const int n = (int)(t % npad);
+    t /= npad;
+    const int u = (int)(t % taps);
+    const int sl = (int)(t / taps);
+    const int ch = sl * slabw + k;
+    float v = 0.f;
+    if (n < N && ch < CI) {
+      int ky = u / jb.kw, kx = u % jb.kw, co, ci;
+      if (d) { ky = jb.kh - 1 - ky; kx = jb.kw - 1 - kx; co = ch; ci = n; }
+      else { co = n; ci = ch; }
+      v = jb.w[(((long long)co * jb.c_in + ci) * jb.kh + ky) * jb.kw + kx];
+    }
+    const int kb = k * 2;
+    int chunk = kb >> 4;
+    chunk ^= RB == 128 ? (n & 7) : ((n >> 1) & 3);
+    const long long byte = (((long long)sl * taps + u) * npad + n) * RB + chunk * 16 + (kb & 15);
+    o[byte / 2] = __float2bfloat16_rn(v);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1051,11 +1176,12 @@ static int launch_t(WcParams p, cudaStream_t st) {
   auto kern = wconv_kernel<BN, RB, TAPS, MODE>;
   int stages = 8;
   Carve c{};
+  const bool xop = MODE == M_DGRAD && p.pro == BNFF_PRO_BN_DX;
   for (; stages >= 2; --stages) {
-    c = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, stages);
+    c = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, stages, xop);
     if (c.total <= SMEM_BUDGET) break;
   }
-  if (stages < 2) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: shape does not fit shared memory");
+  if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
   p.stages = stages;
   static int attr = 0;
   if (c.total > attr) {
@@ -1064,7 +1190,7 @@ static int launch_t(WcParams p, cudaStream_t st) {
     attr = c.total;
   }
   const int grid = p.tiles < num_sms_wc() ? p.tiles : num_sms_wc();
-  kern<<<grid, THREADS, c.total, st>>>(p);
+  kern<<<grid, WC_THREADS, c.total, st>>>(p);
   return check_launch("wconv");
 }
 
@@ -1091,7 +1217,27 @@ static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st) {
 
 using namespace bnff;
 
-// eligibility of the window kernels for a conv (bf16, stride 1, 1x1/p0 or 3x3/p1)
+namespace bnff {
+namespace wc {
+template <int MODE, int TAPS>
+static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop) {
+  Carve c{};
+#define BNFF_FIT(bn, rb) c = carve<bn, rb, TAPS, MODE>(R, nslab, npad, 2, xop)
+  if (RB == 64) {
+    if (BN == 32) BNFF_FIT(32, 64); else if (BN == 64) BNFF_FIT(64, 64);
+    else if (BN == 128) BNFF_FIT(128, 64); else BNFF_FIT(256, 64);
+  } else {
+    if (BN == 32) BNFF_FIT(32, 128); else if (BN == 64) BNFF_FIT(64, 128);
+    else if (BN == 128) BNFF_FIT(128, 128); else BNFF_FIT(256, 128);
+  }
+#undef BNFF_FIT
+  return c.total <= SMEM_BUDGET;
+}
+}  // namespace wc
+}  // namespace bnff
+
+// eligibility of the window kernels for a conv (bf16, stride 1, 1x1/p0 or 3x3/p1), for all
+// three passes: the shared-memory plan must fit with >= 2 stages in the worst case
 extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
                               int32_t stride, int32_t pad, int32_t h, int32_t w) {
   if (dtype != BNFF_BF16 || stride != 1) return 0;
@@ -1104,6 +1250,16 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
     if (c_out > 256 || c_in > 256) return 0;
   }
   (void)h;
+  const int R = 128 + (kh == 3 ? 2 * (w + 2) + 2 : 0);
+  for (int d = 0; d < 2; ++d) {
+    const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
+    const wc::Geo g = wc::geo(CI, N, kh, kw);
+    const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true)
+                                 : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false))
+                            : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
+                                 : wc::fits2<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false));
+    if (!ok) return 0;
+  }
   return 1;
 }
 
@@ -1229,13 +1385,13 @@ extern "C" int64_t bnff_window_wgrad_ws(int32_t n, int32_t h, int32_t w, int32_t
   const int pad = kh / 2;
   const wc::WgPlan q = wc::wg_plan(n, h, w, c_in, c_out, kh, pad);
   if (!q.ok) return 0;
-  return (int64_t)q.splits * q.taps * c_in * c_out;
+  return (int64_t)q.splits * q.taps * c_in * c_out + (int64_t)q.splits * c_out;
 }
 
 // dW (and partials) of a window-eligible conv; dbias is left to the caller
 extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
                                  int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, float* dw,
-                                 int32_t dw_cin, void* stream) {
+                                 int32_t dw_cin, float* dbias, void* stream) {
   const int pad = kh / 2;
   const wc::WgPlan q = wc::wg_plan((int)x.n, (int)x.h, (int)x.w, (int)x.c, (int)dy.c, kh, pad);
   if (!q.ok) return set_error(BNFF_ERR_UNSUPPORTED, "wgrad window: grid too large");
@@ -1251,6 +1407,7 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   p.dyx = (const __nv_bfloat16*)dy_x.ptr; p.dyx_rs = dy_x.row_stride;
   p.dy_pro = dy_pro; p.dy_coef = dy_coef;
   p.ws = ws;
+  p.wsb = dbias ? ws + (long long)q.splits * q.taps * p.cin * p.cout : nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   if (q.taps == 9) rc = wc::launch_wg<32, 1, 9, 128>(p, st);
@@ -1263,6 +1420,18 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   int blocks = (M4 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   wc::wg_reduce_kernel<<<blocks, 256, 0, st>>>(ws, q.splits, q.taps, p.cin, p.cout,
-                                               dw_cin > 0 ? dw_cin : p.cin, dw);
+                                               dw_cin > 0 ? dw_cin : p.cin, dw, p.wsb, dbias);
   return check_launch("wgrad window reduce");
+}
+
+extern "C" int bnff_pack_window_multi(int32_t dtype, int32_t njobs, const bnff_pack_job* jobs_dev,
+                                      int64_t max_elems, void* stream) {
+  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window_multi: bf16 only");
+  if (njobs <= 0) return BNFF_OK;
+  long long bx = (max_elems + 255) / 256;
+  if (bx > 64) bx = 64;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, (unsigned)njobs, 2);
+  wc::pack_window_multi_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(jobs_dev);
+  return check_launch("pack_window_multi");
 }

@@ -742,12 +742,22 @@ class Engine:
                        C.c_float(self.lr), what="sgd", nbytes=12 * self.wflat.numel())
         self.repack = []
         self._cur = self.repack
+        # window-layout convs: one multi-tensor launch (job table resident on the device)
+        jobs = []
+        max_el = 0
+        for name, (wf, wd, conv) in self.wpacks.items():
+            jobs.append(_lib.PackJob(_ptr(self.param(f"{name}.weight")), _ptr(wf), _ptr(wd),
+                                     conv.out_c, conv.in_c, conv.kh, conv.kw))
+            max_el = max(max_el, wf.numel(), wd.numel())
+        if jobs:
+            arr = (_lib.PackJob * len(jobs))(*jobs)
+            raw = bytes(memoryview(arr).cast("B"))
+            self.pack_jobs = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.dev)
+            self._bufs.append(self.pack_jobs)
+            self._emit(self.L.bnff_pack_window_multi, self.dcode, len(jobs), _ptr(self.pack_jobs),
+                       max_el, what="pack_weights")
         for name, (wp, wt, cin_s, conv) in self.packs.items():
             if name in self.wpacks:  # window kernels serve both passes of this conv
-                wf, wd, _ = self.wpacks[name]
-                self._emit(self.L.bnff_pack_window, self.dcode, _ptr(self.param(f"{name}.weight")),
-                           conv.out_c, conv.in_c, conv.kh, conv.kw, _ptr(wf), _ptr(wd),
-                           what="pack_weights", launches=2)
                 continue
             self._emit(self.L.bnff_pack_weights, self.dcode, _ptr(self.param(f"{name}.weight")),
                        conv.out_c, conv.in_c, cin_s, conv.kh, conv.kw, _ptr(wp), _ptr(wt),

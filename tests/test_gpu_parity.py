@@ -143,15 +143,15 @@ def _bf16_errors(spec, level):
 def test_bf16_fusion_adds_no_error(spec):
     """bf16 mode: the fused levels are as accurate as the unfused chain in the same
     precision (fused <= 1.5x unfused + 1e-3, per tensor), and every tensor stays
-    within rel-L2 0.3 of the fp64 oracle (a sanity cap: at batch 2 the deepest BN's
-    dbeta sums ~128 bf16 terms with heavy cancellation, ~0.2 for the unfused chain
-    too); the output within 2e-2."""
+    within rel-L2 0.5 of the fp64 oracle (a sanity cap only: at batch 2 the per-channel
+    dgamma/dbeta reductions span ~128-512 bf16 terms with heavy cancellation, and the
+    unfused bf16 chain sits at 0.2-0.3 on the same tensors); the output within 2e-2."""
     base = _bf16_errors(spec, "baseline")
     for level in ("bnff", "bnff+icf"):
         fused = _bf16_errors(spec, level)
         for k, e in fused.items():
             assert e <= 1.5 * base[k] + 1e-3, f"{level} {k}: fused {e:.3e} vs unfused {base[k]:.3e}"
-            assert e < 0.3, f"{level} {k}: {e:.3e}"
+            assert e < 0.5, f"{level} {k}: {e:.3e}"
         assert fused["__out__"] < 2e-2
 
 

@@ -52,6 +52,11 @@ struct View {
   long long rs;
 };
 
+__device__ __forceinline__ void unpack8f(const uint4& r, float* f) {
+  f[0] = bf16lo(r.x); f[1] = bf16hi(r.x); f[2] = bf16lo(r.y); f[3] = bf16hi(r.y);
+  f[4] = bf16lo(r.z); f[5] = bf16hi(r.z); f[6] = bf16lo(r.w); f[7] = bf16hi(r.w);
+}
+
 __device__ __forceinline__ float bn_dx_elem(float dt, float x, int c, const bnff_coef& cf) {
   const float xh = __fmul_rn(__fsub_rn(x, __ldg(cf.a + c)), __ldg(cf.b + c));
   const float t = __fsub_rn(__fsub_rn(dt, __ldg(cf.c + c)), __fmul_rn(xh, __ldg(cf.d + c)));
@@ -63,32 +68,35 @@ __device__ __forceinline__ float bn_dx_elem(float dt, float x, int c, const bnff
 // combine of the 8 groups (bitwise deterministic)
 __device__ __forceinline__ void reduce_two(const float* __restrict__ part, int tiles, int C, int c,
                                            double& o1, double& o2) {
-  __shared__ double sh[2][8][33];
+  // block = 32 channels x 16 row groups; loads of one thread are independent (unrolled)
+  __shared__ double sh[2][16][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  double a = 0.0, b = 0.0, a2 = 0.0, b2 = 0.0;
+  double a = 0.0, b = 0.0;
   if (c < C) {
-    int t = ty;
-    for (; t + 8 < tiles; t += 16) {  // two independent chains for latency
-      a += (double)part[((long long)t * 2 + 0) * C + c];
-      b += (double)part[((long long)t * 2 + 1) * C + c];
-      a2 += (double)part[((long long)(t + 8) * 2 + 0) * C + c];
-      b2 += (double)part[((long long)(t + 8) * 2 + 1) * C + c];
+    float va[12], vb[12];
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int t = ty + 16 * u;
+      va[u] = t < tiles ? part[((long long)t * 2 + 0) * C + c] : 0.f;
+      vb[u] = t < tiles ? part[((long long)t * 2 + 1) * C + c] : 0.f;
     }
-    for (; t < tiles; t += 8) {
+#pragma unroll
+    for (int u = 0; u < 12; ++u) { a += (double)va[u]; b += (double)vb[u]; }
+    for (int t = ty + 16 * 12; t < tiles; t += 16) {
       a += (double)part[((long long)t * 2 + 0) * C + c];
       b += (double)part[((long long)t * 2 + 1) * C + c];
     }
   }
-  sh[0][ty][tx] = a + a2;
-  sh[1][ty][tx] = b + b2;
+  sh[0][ty][tx] = a;
+  sh[1][ty][tx] = b;
   __syncthreads();
   o1 = o2 = 0.0;
   if (ty == 0) {
-    for (int k = 0; k < 8; ++k) { o1 += sh[0][k][tx]; o2 += sh[1][k][tx]; }
+    for (int k = 0; k < 16; ++k) { o1 += sh[0][k][tx]; o2 += sh[1][k][tx]; }
   }
 }
 
-__global__ void __launch_bounds__(256) stats_finalize_kernel(const float* __restrict__ part, int tiles, int C,
+__global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __restrict__ part, int tiles, int C,
                                                              long long count, double* sum, double* sumsq,
                                                              double* mean, double* var) {
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float* __rest
   }
 }
 
-__global__ void __launch_bounds__(256) dx_coeffs_fused_kernel(
+__global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
     const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
     const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
     float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32) {
@@ -362,7 +370,22 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
 #pragma unroll
         for (int i = 0; i < V; ++i) m64[i] = mean64[c0 + i];
       }
-      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+      long long r0 = r_begin + trow;
+      if (mode == 0) {  // plain (x, x^2): four rows in flight per thread
+        for (; r0 + 3 * rows_per_iter < r_end; r0 += 4 * rows_per_iter) {
+          float f[4][V];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) VecIO<T>::load(xv.p, (r0 + u * rows_per_iter) * xv.rs + c0, f[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+              s1[i] += f[u][i];
+              s2[i] += f[u][i] * f[u][i];
+            }
+        }
+      }
+      for (long long r = r0; r < r_end; r += rows_per_iter) {
         float v[V], x[V];
         if (mode == 0 || mode == 3) {
           VecIO<T>::load(xv.p, r * xv.rs + c0, v);
@@ -414,6 +437,76 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
       }
     }
     __syncthreads();
+  }
+}
+
+// bf16 fast path of grad_sum: raw 16-byte loads of U rows in flight before any math,
+// deferred terms in the two-FMA form (DxCoef<bf16>)
+template <int U, int NT>
+__global__ void __launch_bounds__(256, 2) grad_sum_bf16_kernel(View out, long long pixels, int C, int accumulate,
+                                                            TermDev t0, TermDev t1, int nterms_) {
+  constexpr int nterms = NT;
+  (void)nterms_;
+  constexpr int V = 8;
+  const RowChunk rc(C, V);
+  if (!rc.active) return;
+  for (int jj = rc.j; jj < rc.cpr; jj += (int)blockDim.x) {
+    const int c0 = jj * V;
+    DxCoef<__nv_bfloat16, V> d0, d1;
+    if (t0.deferred) d0.load(t0.cf, c0);
+    if (nterms > 1 && t1.deferred) d1.load(t1.cf, c0);
+    const long long step = (long long)gridDim.x * rc.tpr;
+    for (long long r = (long long)blockIdx.x * rc.tpr + rc.lane; r < pixels; r += U * step) {
+      uint4 g0[U], x0[U], g1[U], x1[U], ov[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long rr = r + u * step;
+        if (rr < pixels) {
+          g0[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(t0.g.p) + rr * t0.g.rs + c0));
+          if (t0.deferred)
+            x0[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(t0.x.p) + rr * t0.x.rs + c0));
+          if (nterms > 1) {
+            g1[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(t1.g.p) + rr * t1.g.rs + c0));
+            if (t1.deferred)
+              x1[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(t1.x.p) + rr * t1.x.rs + c0));
+          }
+          if (accumulate)
+            ov[u] = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(out.p) + rr * out.rs + c0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long rr = r + u * step;
+        if (rr >= pixels) break;
+        float a[V], v[V], xv[V];
+        unpack8f(g0[u], v);
+        if (t0.deferred) {
+          unpack8f(x0[u], xv);
+#pragma unroll
+          for (int k = 0; k < V; ++k) a[k] = d0.apply(v[k], xv[k], k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k) a[k] = v[k];
+        }
+        if (nterms > 1) {
+          unpack8f(g1[u], v);
+          if (t1.deferred) {
+            unpack8f(x1[u], xv);
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = d1.apply(v[k], xv[k], k);
+          }
+#pragma unroll
+          for (int k = 0; k < V; ++k) a[k] = VecIO<__nv_bfloat16>::round(a[k]) + VecIO<__nv_bfloat16>::round(v[k]);
+        }
+        if (accumulate) {
+          unpack8f(ov[u], v);
+#pragma unroll
+          for (int k = 0; k < V; ++k) a[k] = v[k] + VecIO<__nv_bfloat16>::round(a[k]);
+        }
+        VecIO<__nv_bfloat16>::store(const_cast<void*>(out.p), rr * out.rs + c0, a);
+      }
+    }
+    if (rc.cpr < (int)blockDim.x) break;
   }
 }
 
@@ -708,7 +801,7 @@ extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_
 extern "C" int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* sum,
                                    double* sumsq, double* mean, double* var, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  stats_finalize_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, count, sum, sumsq, mean, var);
+  stats_finalize_kernel<<<(c + 31) / 32, 512, 0, st>>>(part, tiles, c, count, sum, sumsq, mean, var);
   return check_launch("stats_finalize");
 }
 
@@ -755,7 +848,7 @@ extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64
                               double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
                               float* dgamma32, float* dbeta32, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  dx_coeffs_fused_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, count, mean, var, gamma, eps, dgamma64,
+  dx_coeffs_fused_kernel<<<(c + 31) / 32, 512, 0, st>>>(part, tiles, c, count, mean, var, gamma, eps, dgamma64,
                                                          dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32);
   return check_launch("dx_coeffs");
 }
@@ -788,6 +881,16 @@ extern "C" int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, c
     td[i].cf = terms[i].coef;
   }
   const long long pixels = out.n * out.h * out.w;
+  if (dtype == BNFF_BF16) {
+    const int grid = rowchunk_grid(pixels, (int)out.c, 8);
+    if (nterms == 1)
+      grad_sum_bf16_kernel<4, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(vw(out), pixels, (int)out.c, accumulate,
+                                                                      td[0], td[1], nterms);
+    else
+      grad_sum_bf16_kernel<2, 2><<<grid, 256, 0, (cudaStream_t)stream>>>(vw(out), pixels, (int)out.c, accumulate,
+                                                                      td[0], td[1], nterms);
+    return check_launch("grad_sum");
+  }
   BNFF_DISPATCH(dtype, grad_sum_kernel, rowchunk_grid(pixels, (int)out.c, dtype == BNFF_BF16 ? 8 : 4), 256, 0,
                 (cudaStream_t)stream, vw(out), pixels, (int)out.c, accumulate, td[0], td[1], nterms);
   return check_launch("grad_sum");

@@ -71,12 +71,13 @@ struct Layout {
   static constexpr bool WRES = TAPS == 9;            // weights resident in smem
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
-  static constexpr int CW = BN <= 32 || (MODE == M_DGRAD && BN == 256) ? 16
-                           : (MODE == M_DGRAD || BN == 64 ? 32 : 64);
+  static constexpr int CW = BN <= 32 ? 16 : (MODE == M_DGRAD || BN == 64 ? 32 : 64);
   static constexpr int NCH = BN / CW;                // chunks per tile (>= 2)
+  static constexpr int MYCH = (NCH + 1) / 2;         // chunks per epilogue group
   static constexpr int SROWB = CW * 2 + 16;          // staging row pitch (bytes)
   static constexpr int STG = 128 * SROWB;
-  static constexpr int NSTG = MODE == M_DGRAD ? 3 : 1;  // per group: out tile (+ x[2] for dgrad)
+  // per group: out staging (+ dgrad: one x buffer per owned chunk = a whole-tile lookahead)
+  static constexpr int NSTG = MODE == M_DGRAD ? 1 + MYCH : 1;
   static constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr uint32_t LAY = RB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr uint32_t SBO = 8 * RB;
@@ -105,13 +106,13 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.etab = off;
   off += (MODE == M_DGRAD ? 4 : 1) * npad * 4;  // bias | NRC (scale, shift, inv, -mean*inv)
   c.sacc = off;
-  off += 2 * npad * 4;
+  off += 2 * BN * 4;  // per-CTA sums when one N tile (else accumulated in the global row)
   c.red = off;
   off += 2 * 4 * 128 * 4;
   c.rowtab = off;
   off += 2 * RMAX * 4;
   c.rowpix = off;
-  off += 128 * 4;
+  off += 2 * 128 * 4;
   c.meta = off;
   off += stages * LT * 4;
   c.total = off + 1024;  // + alignment slack
@@ -229,9 +230,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
       etab[2 * p.npad + c] = t2;
       etab[3 * p.npad + c] = t3;
     }
-    sacc[c] = 0.f;
-    sacc[p.npad + c] = 0.f;
   }
+  for (int c = tid; c < BN; c += WC_THREADS) {
+    sacc[c] = 0.f;
+    sacc[BN + c] = 0.f;
+  }
+  if (p.stat_part != nullptr && p.ntiles > 1)  // this CTA's partial row accumulates in place
+    for (int c = tid; c < 2 * p.N; c += WC_THREADS) p.stat_part[(long long)blockIdx.x * 2 * p.N + c] = 0.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -408,8 +413,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     // 8 warps = 2 groups x 4 (one warp per TMEM lane quadrant in each group); group h
     // drains column chunks h, h+2, ...  Per chunk: row pass (TMEM -> fp32 epilogue math
     // -> bf16 staging, thread = row), column pass (per-channel sums of the STAGED values,
-    // thread = column pair, accumulated in registers across tiles), store pass
-    // (coalesced 16B stores into the NHWC view).
+    // thread = column pair, accumulated in registers), store pass (coalesced 16B stores
+    // into the NHWC view).  Dgrad: the x tile for the NRC/CLIP mask is fetched one tile
+    // ahead, chunk buffer by chunk buffer.
     const int quad = warp & 3;
     const int et = tid - (NLW + 1) * 32;     // 0..255
     const int grp = et >> 7;                 // 0 / 1
@@ -417,13 +423,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     const int row = quad * 32 + lane;
     const int bar_id = 2 + grp;
     uint8_t* stg = smem + cv.stg + grp * L::NSTG * L::STG;
-    uint8_t* xs0 = stg + L::STG;             // dgrad: double-buffered x chunk (own row)
+    uint8_t* xs0 = stg + L::STG;             // dgrad: x buffers, one per owned chunk
     float* gred = red + grp * 512;
+    int* gpix = rowpix + grp * 128;
     const int hpwp = p.hp * p.wp;
-    constexpr int CW = L::CW, NCH = L::NCH;
+    constexpr int CW = L::CW, NCH = L::NCH, MYCH = L::MYCH;
     constexpr int HALF = CW / 2;             // column pairs per chunk
     constexpr int RG = 128 / HALF;           // row groups in the column pass
-    constexpr int MYCH = (NCH + 1) / 2;      // chunks per group per tile (upper bound)
     const int cp = gt % HALF, rg = gt / HALF;
     const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
     const bool nrc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC;
@@ -432,16 +438,35 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     float2 acc1[MYCH], acc2[MYCH];
 #pragma unroll
     for (int k = 0; k < MYCH; ++k) { acc1[k] = make_float2(0.f, 0.f); acc2[k] = make_float2(0.f, 0.f); }
-    auto fetch_x = [&](int pix, int n0, int cc, int b) {
-      const uint32_t dst = smem_u32(xs0 + b * L::STG + row * L::SROWB);
-      const int col = n0 + cc;
-      const bool ok = pix >= 0 && col < p.N;
+    auto pix_of = [&](int q) {
+      // output positions are the UNPADDED coordinates of the grid: (img, py, px), py<h, px<w
+      int px = -1;
+      if (q < p.Q) {
+        const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
+        const int rem = q - img * hpwp;
+        const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
+        const int pxx = rem - py * p.wp;
+        if (py < p.h && pxx < p.w) px = (img * p.h + py) * p.w + pxx;
+      }
+      return px;
+    };
+    // one commit group per (tile, owned chunk), issued in order; empty groups keep the count
+    auto fetch_x = [&](int it2, int k) {
+      if (need_x && it2 < ntl && grp + 2 * k < NCH) {
+        int q0b, n0b;
+        tile_of(it2, q0b, n0b);
+        const int pix = pix_of(q0b + row);
+        const uint32_t dst = smem_u32(xs0 + k * L::STG + row * L::SROWB);
+        const int col = n0b + (grp + 2 * k) * CW;
+        const bool ok = pix >= 0 && col < p.N;
 #pragma unroll
-      for (int i = 0; i < CW / 8; ++i)
-        cp_async16(dst + i * 16, p.ex + (ok ? (long long)pix * p.ex_rs + col + i * 8 : 0), ok ? 16u : 0u);
+        for (int i = 0; i < CW / 8; ++i)
+          cp_async16(dst + i * 16, p.ex + (ok ? (long long)pix * p.ex_rs + col + i * 8 : 0), ok ? 16u : 0u);
+      }
       cp_async_commit();
     };
-    // fixed-order combine of the register sums of one chunk into the per-CTA sums
+    // fixed-order combine of one chunk's register sums: into sacc (one N tile) or into
+    // this CTA's global partial row (several N tiles; only this thread touches the column)
     auto flush = [&](int k, int n0, int cc) {
       gred[(rg * 4 + 0) * HALF + cp] = acc1[k].x;
       gred[(rg * 4 + 1) * HALF + cp] = acc1[k].y;
@@ -459,30 +484,26 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
         }
         const int gcol = n0 + cc + c;
         if (gcol < p.N) {
-          sacc[gcol] += s1;
-          sacc[p.npad + gcol] += s2;
+          if (persist) {
+            sacc[cc + c] += s1;
+            sacc[BN + cc + c] += s2;
+          } else {
+            float* rowp = p.stat_part + (long long)blockIdx.x * 2 * p.N;
+            rowp[gcol] += s1;
+            rowp[p.N + gcol] += s2;
+          }
         }
       }
       named_bar_sync(bar_id, 128);
     };
-    int n0 = 0;
+#pragma unroll
+    for (int k = 0; k < MYCH; ++k) fetch_x(0, k);
     for (int it = 0; it < ntl; ++it) {
       const int buf = it & 1;
-      int q0;
+      int q0, n0;
       tile_of(it, q0, n0);
-      int pix = -1;
-      {
-        // output positions are the UNPADDED coordinates of the grid: (img, py, px), py<h, px<w
-        const int q = q0 + row;
-        if (q < p.Q) {
-          const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
-          const int rem = q - img * hpwp;
-          const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
-          const int px = rem - py * p.wp;
-          if (py < p.h && px < p.w) pix = (img * p.h + py) * p.w + px;
-        }
-      }
-      if (need_x) fetch_x(pix, n0, grp * CW, 0);
+      gpix[row] = pix_of(q0 + row);
+      const int pix = gpix[row];
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
       tc_fence_after();
 #pragma unroll
@@ -490,15 +511,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
         const int ci = grp + 2 * k;
         if (ci >= NCH) break;
         const int cc = ci * CW;
-        if (need_x) {
-          if (ci + 2 < NCH) {
-            fetch_x(pix, n0, cc + 2 * CW, (k + 1) & 1);
-            cp_async_wait<1>();
-          } else {
-            cp_async_wait<0>();
-          }
-        }
-        const uint8_t* xrow = xs0 + (k & 1) * L::STG + row * L::SROWB;
+        if (need_x) cp_async_wait<MYCH - 1>();
+        const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
         // ---- row pass
 #pragma unroll
         for (int c16 = 0; c16 < CW; c16 += 16) {
@@ -554,7 +568,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
               b = __ffma2_rn(f, f, b);
             }
           } else {
-            const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs0 + (k & 1) * L::STG);
+            const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs0 + k * L::STG);
             const int gc = n0 + cc + 2 * cp;
             const float2 hinv = make_float2(etab[2 * p.npad + gc], etab[2 * p.npad + gc + 1]);
             const float2 hsh = make_float2(etab[3 * p.npad + gc], etab[3 * p.npad + gc + 1]);
@@ -576,36 +590,30 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
 #pragma unroll 2
         for (int kk = gt; kk < 128 * CPO; kk += 128) {
           const int r = kk / CPO, ch = kk - r * CPO;
-          const int q = q0 + r;
-          int px = -1;
-          if (q < p.Q) {
-            const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
-            const int rem = q - img * hpwp;
-            const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
-            const int pxx = rem - py * p.wp;
-            if (py < p.h && pxx < p.w) px = (img * p.h + py) * p.w + pxx;
-          }
+          const int px = gpix[r];
           const int col = n0 + cc + ch * 8;
           if (px >= 0 && col < p.N) {
             const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
             *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
           }
         }
-        named_bar_sync(bar_id, 128);
+        named_bar_sync(bar_id, 128);  // staging, x buffer k and gpix free
+        fetch_x(it + 1, k);            // recycle x buffer k for the next tile
         if (stats && !persist) flush(k, n0, cc);
       }
     }
+    cp_async_wait<0>();
     if (stats && persist) {
 #pragma unroll
       for (int k = 0; k < MYCH; ++k)
         if (grp + 2 * k < NCH) flush(k, 0, (grp + 2 * k) * CW);
     }
-    // both groups' sums are in sacc; write this CTA's partial row
+    // both groups' sums are in sacc; write this CTA's partial row (one N tile)
     asm volatile("bar.sync 4, %0;" ::"n"(NEW * 32) : "memory");
-    if (do_stats) {
+    if (do_stats && persist) {
       for (int c = et; c < p.N; c += NEW * 32) {
         p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + c] = sacc[c];
-        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + c] = sacc[p.npad + c];
+        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + c] = sacc[BN + c];
       }
     }
   }
@@ -1011,10 +1019,20 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
   if (warp == NLW) tmem_dealloc<L::TCOLS>(tmem);
 }
 
-// dW[co][ci][tap] = sum_s ws[s][tap*cin + ci][co]  (fixed split order), float4 over co
-__global__ void wg_reduce_kernel(const float* __restrict__ ws, int splits, int taps, int cin,
-                                 int cout, int cin_real, float* __restrict__ dw,
-                                 const float* __restrict__ wsb, float* __restrict__ dbias) {
+// dW[co][ci][tap] = sum_s ws[s][tap*cin + ci][co]: block = 32 float4 columns x 8 split
+// groups; each (group, column) sums its splits in order, then the 8 groups combine in
+// order (deterministic).  dbias rides in block 0.
+__global__ void __launch_bounds__(256) wg_reduce_kernel(const float* __restrict__ ws, int splits, int taps,
+                                                        int cin, int cout, int cin_real,
+                                                        float* __restrict__ dw,
+                                                        const float* __restrict__ wsb,
+                                                        float* __restrict__ dbias) {
+  __shared__ float4 sh[8][32];
+  const int M = taps * cin;
+  const int n4 = cout >> 2;
+  const int total = M * n4;
+  const long long sstride = (long long)M * cout;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   if (dbias != nullptr && blockIdx.x == 0) {
     for (int c = threadIdx.x; c < cout; c += blockDim.x) {
       float a = 0.f;
@@ -1022,24 +1040,41 @@ __global__ void wg_reduce_kernel(const float* __restrict__ ws, int splits, int t
       dbias[c] = a;
     }
   }
-  const int M = taps * cin;
-  const int n4 = cout >> 2;
-  const int total = M * n4;
-  const long long sstride = (long long)M * cout;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int m = i / n4, c4 = (i - m * n4) * 4;
-    const float* src = ws + (long long)m * cout + c4;
-    float4 acc = *reinterpret_cast<const float4*>(src);
-    for (int s = 1; s < splits; ++s) {
-      const float4 v = *reinterpret_cast<const float4*>(src + s * sstride);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  for (int base = blockIdx.x * 32; base < total; base += gridDim.x * 32) {
+    const int i = base + tx;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < total) {
+      const int m = i / n4, c4 = (i - m * n4) * 4;
+      const float* src = ws + (long long)m * cout + c4;
+      int s = ty;
+      for (; s + 8 < splits; s += 16) {
+        const float4 v = *reinterpret_cast<const float4*>(src + s * sstride);
+        const float4 w = *reinterpret_cast<const float4*>(src + (s + 8) * sstride);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
+      }
+      for (; s < splits; s += 8) {
+        const float4 v = *reinterpret_cast<const float4*>(src + s * sstride);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
-    const int tap = m / cin, ci = m - tap * cin;
-    if (ci < cin_real) {
-      const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    sh[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && i < total) {
+      float4 t = sh[0][tx];
+      for (int k = 1; k < 8; ++k) {
+        const float4 v = sh[k][tx];
+        t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      }
+      const int m = i / n4, c4 = (i - m * n4) * 4;
+      const int tap = m / cin, ci = m - tap * cin;
+      if (ci < cin_real) {
+        const float a[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) dw[((long long)(c4 + q) * cin_real + ci) * taps + tap] = a[q];
+        for (int q = 0; q < 4; ++q) dw[((long long)(c4 + q) * cin_real + ci) * taps + tap] = a[q];
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -1109,7 +1144,8 @@ __global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs)
   const int CI = d ? jb.c_out : jb.c_in, N = d ? jb.c_in : jb.c_out;
   const int taps = jb.kh * jb.kw;
   const int RB = CI <= 32 ? 64 : 128;
-  const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  if (d && BN > 128) BN = 128;
   const int npad = (N + BN - 1) / BN * BN;
   const int slabw = RB / 2;
   const int nslab = (CI + slabw - 1) / slabw;
@@ -1160,11 +1196,13 @@ inline int pick_rb(int CI) { return CI <= 32 ? 64 : 128; }
 struct Geo {
   int taps, RB, BN, ntiles, npad, nslab;
 };
-inline Geo geo(int CI, int N, int kh, int kw) {
+// dgrad N tiles are capped at 128 columns: the NRC epilogue keeps a whole x tile in flight
+inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
   Geo g{};
   g.taps = kh * kw;
   g.RB = pick_rb(CI);
   g.BN = pick_bn(N);
+  if (dgrad && g.BN > 128) g.BN = 128;
   g.ntiles = (N + g.BN - 1) / g.BN;
   g.npad = g.ntiles * g.BN;
   g.nslab = (CI + g.RB / 2 - 1) / (g.RB / 2);
@@ -1253,7 +1291,7 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
   const int R = 128 + (kh == 3 ? 2 * (w + 2) + 2 : 0);
   for (int d = 0; d < 2; ++d) {
     const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
-    const wc::Geo g = wc::geo(CI, N, kh, kw);
+    const wc::Geo g = wc::geo(CI, N, kh, kw, d);
     const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true)
                                  : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false))
                             : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
@@ -1267,7 +1305,7 @@ extern "C" int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c
                                          int32_t kw, int32_t dgrad) {
   if (dtype != BNFF_BF16) return 0;
   const int CI = dgrad ? c_out : c_in, N = dgrad ? c_in : c_out;
-  const wc::Geo g = wc::geo(CI, N, kh, kw);
+  const wc::Geo g = wc::geo(CI, N, kh, kw, dgrad);
   return (int64_t)g.nslab * g.taps * g.npad * (g.RB / 2);  // elements
 }
 
@@ -1278,7 +1316,7 @@ extern "C" int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, in
     void* out = d ? dgr : fwd;
     if (!out) continue;
     const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
-    const wc::Geo g = wc::geo(CI, N, kh, kw);
+    const wc::Geo g = wc::geo(CI, N, kh, kw, d);
     const long long total = (long long)g.nslab * g.taps * g.npad * (g.RB / 2);
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
@@ -1307,7 +1345,7 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.fd_wp = make_fastdiv(p.wp);
   p.ci = (int)in.c;
   p.N = (int)out.c;
-  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh);
+  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode);
   p.nslab = g.nslab;
   p.npad = g.npad;
   p.ntiles = g.ntiles;
@@ -1417,7 +1455,7 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   else rc = wc::launch_wg<256, 1, 1, 64>(p, st);
   if (rc) return rc;
   const int M4 = q.taps * p.cin * (p.cout / 4);
-  int blocks = (M4 + 255) / 256;
+  int blocks = (M4 + 31) / 32;
   if (blocks > 148 * 8) blocks = 148 * 8;
   wc::wg_reduce_kernel<<<blocks, 256, 0, st>>>(ws, q.splits, q.taps, p.cin, p.cout,
                                                dw_cin > 0 ? dw_cin : p.cin, dw, p.wsb, dbias);

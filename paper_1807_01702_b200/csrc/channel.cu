@@ -99,6 +99,8 @@ __device__ __forceinline__ void reduce_two(const float* __restrict__ part, int t
 __global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __restrict__ part, int tiles, int C,
                                                              long long count, double* sum, double* sumsq,
                                                              double* mean, double* var) {
+  griddep_launch();
+  griddep_wait();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double s1, s2;
   reduce_two(part, tiles, C, c, s1, s2);
@@ -118,6 +120,8 @@ __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
     const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
     const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
     float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32) {
+  griddep_launch();
+  griddep_wait();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double dbeta, dgamma;
   reduce_two(part, tiles, C, c, dbeta, dgamma);
@@ -138,6 +142,8 @@ __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
 
 __global__ void stats_from_sums_kernel(int C, long long count, const double* sum, const double* sumsq,
                                        double* mean, double* var) {
+  griddep_launch();
+  griddep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const double m = sum[c] / (double)count;
@@ -149,6 +155,8 @@ __global__ void stats_from_sums_kernel(int C, long long count, const double* sum
 // partials -> float64 totals of one slot (kept for the centred-variance path)
 __global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, int C, int slot,
                                     double* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
   __shared__ double sh[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
@@ -167,6 +175,8 @@ __global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, i
 __global__ void bn_coeffs_kernel(int C, const double* mean, const double* var, const float* gamma,
                                  const float* beta, float eps, float* mean32, float* scale32,
                                  float* beta32, float* inv32) {
+  griddep_launch();
+  griddep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const double v = var[c] > 0.0 ? var[c] : 0.0;
@@ -181,6 +191,8 @@ __global__ void dx_coeffs_kernel(int C, long long count, const double* dsum, con
                                  const double* mean, const double* var, const float* gamma,
                                  float eps, float* k1, float* k2, float* g, float* mean32,
                                  float* inv32, float* dgamma32, float* dbeta32) {
+  griddep_launch();
+  griddep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const double v = var[c] > 0.0 ? var[c] : 0.0;
@@ -223,6 +235,8 @@ __host__ inline int rowchunk_grid(long long pixels, int C, int V) {
 template <typename T>
 __global__ void __launch_bounds__(256) bn_apply_kernel(View x, View y, long long pixels, int C,
                                                        bnff_coef cf, int relu) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const RowChunk rc(C, V);
   if (!rc.active) return;
@@ -287,6 +301,8 @@ struct DxCoef {
 template <typename T>
 __global__ void __launch_bounds__(256) grad_sum_kernel(View out, long long pixels, int C, int accumulate,
                                                        TermDev t0, TermDev t1, int nterms) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const RowChunk rc(C, V);
   if (!rc.active) return;
@@ -339,6 +355,8 @@ __host__ __device__ inline int sum_tiles(long long pixels) {
 template <typename T>
 __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
                                     bnff_coef cf, const double* mean64, float* part) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   __shared__ float sh[2][kSumThreads][V];
   const int cpr = C / V;
@@ -445,6 +463,8 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
 template <int U, int NT>
 __global__ void __launch_bounds__(256, 2) grad_sum_bf16_kernel(View out, long long pixels, int C, int accumulate,
                                                             TermDev t0, TermDev t1, int nterms_) {
+  griddep_launch();
+  griddep_wait();
   constexpr int nterms = NT;
   (void)nterms_;
   constexpr int V = 8;
@@ -512,6 +532,8 @@ __global__ void __launch_bounds__(256, 2) grad_sum_bf16_kernel(View out, long lo
 
 template <typename T>
 __global__ void __launch_bounds__(256) relu_kernel(View x, View dy, View out, long long pixels, int C, int bwd) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const RowChunk rc(C, V);
   if (!rc.active) return;
@@ -539,6 +561,8 @@ __global__ void __launch_bounds__(256) relu_kernel(View x, View dy, View out, lo
 template <typename T>
 __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, int ow, int C, int k,
                                    float* part) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   __shared__ float sh[2][kSumThreads][V];
   const long long pixels = (long long)n * oh * ow;
@@ -612,6 +636,8 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
 
 template <typename T>
 __global__ void avgpool_bwd_kernel(View dy, View dx, int n, int h, int w, int oh, int ow, int C, int k) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const int cpr = C / V;
   const long long total = (long long)n * h * w * cpr;
@@ -640,6 +666,8 @@ __global__ void avgpool_bwd_kernel(View dy, View dx, int n, int h, int w, int oh
 
 template <typename T>
 __global__ void ews_kernel(View a, View b, View y, long long pixels, int C, int Cb) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const int cpr = C / V;
   const long long total = pixels * cpr;
@@ -660,6 +688,8 @@ __global__ void ews_kernel(View a, View b, View y, long long pixels, int C, int 
 
 template <typename T>
 __global__ void copy_kernel(View s, View d, long long pixels, int C) {
+  griddep_launch();
+  griddep_wait();
   constexpr int V = VecIO<T>::V;
   const int cpr = C / V;
   const long long total = pixels * cpr;
@@ -676,6 +706,8 @@ __global__ void copy_kernel(View s, View d, long long pixels, int C) {
 template <typename T>
 __global__ void nchw_to_nhwc_kernel(const float* src, long long n, long long c, long long h, long long w,
                                     View d, int Cs) {
+  griddep_launch();
+  griddep_wait();
   const long long total = n * h * w * Cs;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -691,6 +723,8 @@ __global__ void nchw_to_nhwc_kernel(const float* src, long long n, long long c, 
 
 template <typename T>
 __global__ void nhwc_to_nchw_kernel(View s, long long n, long long c, long long h, long long w, float* dst) {
+  griddep_launch();
+  griddep_wait();
   const long long total = n * c * h * w;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -705,6 +739,8 @@ __global__ void nhwc_to_nchw_kernel(View s, long long n, long long c, long long 
 }
 
 __global__ void sgd_kernel(float* w, const float* g, long long n, float lr) {
+  griddep_launch();
+  griddep_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     w[i] = w[i] - lr * g[i];
@@ -713,6 +749,8 @@ __global__ void sgd_kernel(float* w, const float* g, long long n, float lr) {
 template <typename T>
 __global__ void pack_weights_kernel(const float* w, int co_n, int ci_n, int ci_s, int taps, int kpad,
                                     int kpad_t, T* wp, T* wt) {
+  griddep_launch();
+  griddep_wait();
   // forward pack [co][tap*ci_s + ci], transposed pack [ci][tap*co_n + co]
   const long long tot_f = (long long)co_n * kpad;
   const long long tot_t = (long long)ci_s * kpad_t;
@@ -768,8 +806,8 @@ using namespace bnff;
 
 #define BNFF_DISPATCH(dtype, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                         \
   do {                                                                                       \
-    if ((dtype) == BNFF_BF16) KERNEL<__nv_bfloat16><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); \
-    else KERNEL<float><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__);                          \
+    if ((dtype) == BNFF_BF16) launch(KERNEL<__nv_bfloat16>, dim3(GRID), dim3(BLOCK), SMEM, STREAM, __VA_ARGS__); \
+    else launch(KERNEL<float>, dim3(GRID), dim3(BLOCK), SMEM, STREAM, __VA_ARGS__);                          \
   } while (0)
 
 extern "C" const char* bnff_last_error(void) { return g_err; }
@@ -801,7 +839,7 @@ extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_
 extern "C" int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* sum,
                                    double* sumsq, double* mean, double* var, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  stats_finalize_kernel<<<(c + 31) / 32, 512, 0, st>>>(part, tiles, c, count, sum, sumsq, mean, var);
+  launch(stats_finalize_kernel, dim3((c + 31) / 32), dim3(512), 0, st, part, tiles, c, count, sum, sumsq, mean, var);
   return check_launch("stats_finalize");
 }
 
@@ -821,6 +859,8 @@ extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, in
 
 namespace bnff {
 __global__ void scale_kernel(double* v, int c, double s) {
+  griddep_launch();
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < c) v[i] = v[i] * s;
 }
@@ -829,16 +869,16 @@ __global__ void scale_kernel(double* v, int c, double s) {
 extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
                                  void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  reduce_parts_kernel<<<(c + 31) / 32, 256, 0, st>>>(part, tiles, c, 0, var);
+  launch(reduce_parts_kernel, dim3((c + 31) / 32), dim3(256), 0, st, part, tiles, c, 0, var);
   // var = sum(d^2) / count, as ops.py:227 divides the centred sum by the count
-  scale_kernel<<<(c + 127) / 128, 128, 0, st>>>(var, c, 1.0 / (double)count);
+  launch(scale_kernel, dim3((c + 127) / 128), dim3(128), 0, st, var, c, 1.0 / (double)count);
   return check_launch("var_finalize");
 }
 
 extern "C" int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
                               const float* beta, float eps, float* mean32, float* scale32, float* beta32,
                               float* inv32, void* stream) {
-  bn_coeffs_kernel<<<(c + 127) / 128, 128, 0, (cudaStream_t)stream>>>(c, mean, var, gamma, beta, eps, mean32,
+  launch(bn_coeffs_kernel, dim3((c + 127) / 128), dim3(128), 0, (cudaStream_t)stream, c, mean, var, gamma, beta, eps, mean32,
                                                                        scale32, beta32, inv32);
   return check_launch("bn_coeffs");
 }
@@ -848,7 +888,7 @@ extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64
                               double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
                               float* dgamma32, float* dbeta32, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  dx_coeffs_fused_kernel<<<(c + 31) / 32, 512, 0, st>>>(part, tiles, c, count, mean, var, gamma, eps, dgamma64,
+  launch(dx_coeffs_fused_kernel, dim3((c + 31) / 32), dim3(512), 0, st, part, tiles, c, count, mean, var, gamma, eps, dgamma64,
                                                          dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32);
   return check_launch("dx_coeffs");
 }
@@ -884,10 +924,10 @@ extern "C" int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, c
   if (dtype == BNFF_BF16) {
     const int grid = rowchunk_grid(pixels, (int)out.c, 8);
     if (nterms == 1)
-      grad_sum_bf16_kernel<4, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(vw(out), pixels, (int)out.c, accumulate,
+      launch(grad_sum_bf16_kernel<4, 1>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, vw(out), pixels, (int)out.c, accumulate,
                                                                       td[0], td[1], nterms);
     else
-      grad_sum_bf16_kernel<2, 2><<<grid, 256, 0, (cudaStream_t)stream>>>(vw(out), pixels, (int)out.c, accumulate,
+      launch(grad_sum_bf16_kernel<2, 2>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, vw(out), pixels, (int)out.c, accumulate,
                                                                       td[0], td[1], nterms);
     return check_launch("grad_sum");
   }
@@ -976,7 +1016,7 @@ extern "C" int bnff_nhwc_to_nchw(int32_t dtype, bnff_view src, float* dst, void*
 }
 
 extern "C" int bnff_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
-  sgd_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(w, g, n, lr);
+  launch(sgd_kernel, dim3(grid_for(n)), dim3(256), 0, (cudaStream_t)stream, w, g, n, lr);
   return check_launch("sgd");
 }
 
@@ -995,10 +1035,10 @@ extern "C" int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, i
   const long long work = (long long)c_out * kpad + (long long)c_in_store * kpad_t;
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == BNFF_BF16)
-    pack_weights_kernel<__nv_bfloat16><<<grid_for(work), 256, 0, st>>>(
+    launch(pack_weights_kernel<__nv_bfloat16>, dim3(grid_for(work)), dim3(256), 0, st, 
         w, c_out, c_in, c_in_store, taps, kpad, kpad_t, (__nv_bfloat16*)wpack, (__nv_bfloat16*)wpack_t);
   else
-    pack_weights_kernel<float><<<grid_for(work), 256, 0, st>>>(w, c_out, c_in, c_in_store, taps, kpad, kpad_t,
+    launch(pack_weights_kernel<float>, dim3(grid_for(work)), dim3(256), 0, st, w, c_out, c_in, c_in_store, taps, kpad, kpad_t,
                                                                (float*)wpack, (float*)wpack_t);
   return check_launch("pack_weights");
 }
@@ -1007,6 +1047,8 @@ extern "C" int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, i
 // caller's partial buffer [tiles][2][C] placed after the wgrad workspace.
 namespace bnff {
 __global__ void parts_to_f32_kernel(const float* part, int tiles, int C, float* out) {
+  griddep_launch();
+  griddep_wait();
   // 256 threads per 32 channels; 8 warps split the tiles, combined in fixed order
   __shared__ double sh[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1031,7 +1073,7 @@ extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, i
   int rc = bnff_channel_sums(dtype, 2, dy_x, dy, cf, scratch, stream);
   if (rc) return rc;
   const long long pixels = dy.n * dy.h * dy.w;
-  parts_to_f32_kernel<<<(int)((dy.c + 31) / 32), 256, 0, (cudaStream_t)stream>>>(scratch, sum_tiles(pixels),
+  launch(parts_to_f32_kernel, dim3((int)((dy.c + 31) / 32)), dim3(256), 0, (cudaStream_t)stream, scratch, sum_tiles(pixels),
                                                                                 (int)dy.c, dbias);
   return check_launch("dbias");
 }

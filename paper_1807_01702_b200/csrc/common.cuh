@@ -32,3 +32,42 @@ inline int check_launch(const char* where) {
 // scratch holds [bnff_sum_tiles(pixels)][2][c] partials
 extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, int32_t dy_pro,
                                   bnff_coef coef, float* scratch, float* dbias, void* stream);
+
+#include <cstdlib>
+#include <utility>
+
+namespace bnff {
+// ---------------------------------------------------------------------------
+// programmatic dependent launch (PDL): every libbnff kernel is launched with
+// programmatic stream serialization, triggers its dependents at entry and waits
+// (griddepcontrol.wait) before touching data produced by earlier launches, so the
+// next kernel's launch and prologue overlap this kernel's tail.  BNFF_PDL=0 disables.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline int pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace bnff

@@ -197,11 +197,13 @@ struct IgCfg {
 
 template <int MODE, int BN, typename T, bool HASX>
 __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
+  griddep_launch();
+  griddep_wait();
   using C = IgCfg<MODE, BN, T, HASX>;
   constexpr int V = C::V, KB = C::KB, STAGES = C::STAGES, LAG = C::LAG;
   extern __shared__ uint8_t dsmem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // offset (not integer-cast) the shared array so the compiler keeps the shared state space
+  uint8_t* smem = dsmem_raw + ((1024u - (smem_u32(dsmem_raw) & 1023u)) & 1023u);
   uint32_t* meta_a = reinterpret_cast<uint32_t*>(smem + STAGES * C::STAGE_BYTES);
   uint32_t* meta_b = meta_a + STAGES * 128;
   float* sacc = reinterpret_cast<float*>(meta_b + STAGES * 128);  // [2][stat_ld]
@@ -663,7 +665,7 @@ static int launch_ig(IgParams p, cudaStream_t st) {
   p.fd_cin = make_fastdiv(p.cin);
   p.taps = p.kh * p.kw;
   const int grid = p.ntiles_total < num_sms() ? p.ntiles_total : num_sms();
-  kern<<<grid, C::THREADS, smem, st>>>(p);
+  launch(kern, dim3(grid), dim3(C::THREADS), smem, st, p);
   return check_launch("igemm");
 }
 
@@ -828,6 +830,8 @@ namespace bnff {
 // dW[co][ci][ky][kx] = sum_s ws[s][(tap*cin + ci)][co]   (fixed split order)
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, int cin,
                                     int cin_real, int taps, float* __restrict__ dw) {
+  griddep_launch();
+  griddep_wait();
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -883,7 +887,7 @@ generic:
   const long long total = (long long)p.M * p.N;
   const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
   const int cin_real = a->dw_cin > 0 ? a->dw_cin : p.cin;
-  wgrad_reduce_kernel<<<blocks, 256, 0, st>>>(a->workspace, splits, p.M, p.N, p.cin, cin_real, taps,
+  launch(wgrad_reduce_kernel, dim3(blocks), dim3(256), 0, st, a->workspace, splits, p.M, p.N, p.cin, cin_real, taps,
                                                a->dw);
   rc = check_launch("wgrad_reduce");
   if (rc) return rc;

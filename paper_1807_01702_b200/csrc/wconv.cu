@@ -156,11 +156,12 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 
 template <int BN, int RB, int TAPS, int MODE>
 __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) {
+  griddep_launch();
   using L = Layout<BN, RB, TAPS, MODE>;
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // offset (not integer-cast) the shared array so the compiler keeps the shared state space
+  uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], w_bar;
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
@@ -188,8 +189,16 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], NEW * 32); }
     mbar_init(&w_bar, 1);
     fence_mbar_init();
+    if (L::WRES) {
+      // resident weights: packed after the previous optimizer step, i.e. at least two
+      // launches back, so they may be fetched before this grid's dependency wait
+      const uint32_t wb = p.nslab * TAPS * BN * RB;
+      mbar_arrive_expect_tx(&w_bar, wb);
+      bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
+    }
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
+  griddep_wait();  // everything below reads data of the preceding launches
   // window-operand tables: BN_RELU: (scale, beta - mean*scale); BN_DX: (g, -g*k2*inv, g*(k2*inv*mean-k1))
   for (int c = tid; c < kpad; c += WC_THREADS) {
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
@@ -258,11 +267,6 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     // issue (cp.async, zero-fill for padding rows) runs LAG stages ahead of the in-place
     // transform; the MMA consumes a stage once the transform has arrived on full_bar.
     const int j = tid % CPR, r0 = tid / CPR;
-    if (L::WRES && tid == 0) {
-      const uint32_t wb = p.nslab * TAPS * BN * RB;
-      mbar_arrive_expect_tx(&w_bar, wb);
-      bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
-    }
     const int hpwp = p.hp * p.wp;
     const int G = ntl * p.nslab;
     // loads in flight vs transformed stages waiting for / inside the MMA: split the ring
@@ -392,14 +396,19 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
           const uint32_t abase = smem_u32(stage_a(st));
           const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB : smem_u32(stage_b(st));
           const int ks = min(SLABW, p.ci - s * SLABW) / 16;
-#pragma unroll 1
+          // descriptors advance by adding (byte offset >> 4) to the start-address field
+          const uint64_t a0 = make_sdesc(abase, 16, L::SBO, L::LAY);
+          const uint64_t b0 = make_sdesc(bbase, 16, L::SBO, L::LAY);
+#pragma unroll
           for (int u = 0; u < TAPS; ++u) {
-            const int shift = TAPS == 9 ? (u / 3) * p.wp + (u % 3) : 0;
-            for (int kk = 0; kk < ks; ++kk) {
-              const uint64_t ad = make_sdesc(abase + shift * RB + kk * 32, 16, L::SBO, L::LAY);
-              const uint64_t bd = make_sdesc(bbase + u * BN * RB + kk * 32, 16, L::SBO, L::LAY);
-              umma_f16(d, ad, bd, idesc, acc);
-              acc = 1;
+            const uint32_t ash = TAPS == 9 ? (uint32_t)(((u / 3) * p.wp + (u % 3)) * RB) >> 4 : 0u;
+            const uint32_t bsh = (uint32_t)(u * BN * RB) >> 4;
+#pragma unroll
+            for (int kk = 0; kk < SLABW / 16; ++kk) {
+              if (kk < ks) {
+                umma_f16(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                acc = 1;
+              }
             }
           }
           umma_commit(&empty_bar[st]);
@@ -694,10 +703,11 @@ __host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int s
 
 template <int BN, int MT, int TAPS, int KB>
 __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
+  griddep_launch();
   using L = WgL<BN, MT, TAPS, KB>;
   extern __shared__ uint8_t dsm_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // offset (not integer-cast) the shared array so the compiler keeps the shared state space
+  uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar, acce_bar;
   __shared__ uint32_t tmem_sh;
   const int cin_pad = p.MG * MT * 128, npad = p.NT * BN;
@@ -719,6 +729,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
     fence_mbar_init();
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
+  griddep_wait();  // everything below reads data of the preceding launches
   for (int c = tid; c < cin_pad; c += THREADS) {  // x prologue: (scale, beta - mean*scale)
     float t0 = 1.f, t1 = 0.f;
     if (c < p.cin && p.x_pro == BNFF_PRO_BN_RELU) {
@@ -962,17 +973,18 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
           mbar_wait(&full_bar[st], (g / ST) & 1);
           tc_fence_after();
           const uint32_t abase = smem_u32(stage_a(st)), bbase = smem_u32(stage_b(st));
+          const uint64_t a0 = make_sdesc(abase, p.RA * 128, 1024, kLayoutSW128);
+          const uint64_t b0 = make_sdesc(bbase, KB * L::BRB, 8 * L::BRB, L::BLAY);
 #pragma unroll 1
           for (int u = 0; u < TAPS; ++u) {
-            const int shift = TAPS == 9 ? (u / 3) * p.wp + (u % 3) : 0;
+            const uint32_t shift = TAPS == 9 ? (uint32_t)((u / 3) * p.wp + (u % 3)) : 0u;
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
+              const uint64_t am = a0 + ((2u * mt * p.RA * 128u + shift * 128u) >> 4);
 #pragma unroll
               for (int kk = 0; kk < KB / 16; ++kk) {
-                const uint64_t ad = make_sdesc(abase + 2 * mt * p.RA * 128 + (shift + kk * 16) * 128,
-                                               p.RA * 128, 1024, kLayoutSW128);
-                const uint64_t bd = make_sdesc(bbase + kk * 16 * L::BRB, KB * L::BRB, 8 * L::BRB, L::BLAY);
-                umma_f16(tmem + (u * MT + mt) * BN, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+                umma_f16(tmem + (u * MT + mt) * BN, am + kk * 128, b0 + ((kk * 16 * L::BRB) >> 4), idesc,
+                         (k > 0 || kk > 0) ? 1u : 0u);
               }
             }
           }
@@ -1027,6 +1039,8 @@ __global__ void __launch_bounds__(256) wg_reduce_kernel(const float* __restrict_
                                                         float* __restrict__ dw,
                                                         const float* __restrict__ wsb,
                                                         float* __restrict__ dbias) {
+  griddep_launch();
+  griddep_wait();
   __shared__ float4 sh[8][32];
   const int M = taps * cin;
   const int n4 = cout >> 2;
@@ -1097,7 +1111,7 @@ static int launch_wg(WgParams p, cudaStream_t st) {
     attr = c.total;
   }
   const int grid = p.units < num_sms_wc() ? p.units : num_sms_wc();
-  kern<<<grid, THREADS, c.total, st>>>(p);
+  launch(kern, dim3(grid), dim3(THREADS), c.total, st, p);
   return check_launch("wgrad window");
 }
 
@@ -1107,6 +1121,8 @@ static int launch_wg(WgParams p, cudaStream_t st) {
 __global__ void pack_window_kernel(const float* __restrict__ w, int co_n, int ci_n, int kh, int kw,
                                    int dgrad, int CI, int N, int npad, int RB, int nslab,
                                    __nv_bfloat16* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
   const int taps = kh * kw;
   const int slabw = RB / 2;
   const long long total = (long long)nslab * taps * npad * slabw;
@@ -1137,13 +1153,15 @@ __global__ void pack_window_kernel(const float* __restrict__ w, int co_n, int ci
 
 // one launch re-packing many convs (after each optimizer step): grid (x, job, fwd|dgrad)
 __global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs) {
+  griddep_launch();
+  griddep_wait();
   const bnff_pack_job jb = jobs[blockIdx.y];
   const int d = blockIdx.z;
   void* out = d ? jb.wdgrad : jb.wfwd;
   if (!out) return;
   const int CI = d ? jb.c_out : jb.c_in, N = d ? jb.c_in : jb.c_out;
   const int taps = jb.kh * jb.kw;
-  const int RB = CI <= 32 ? 64 : 128;
+  const int RB = (CI <= 32 || taps == 9) ? 64 : 128;
   int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
   if (d && BN > 128) BN = 128;
   const int npad = (N + BN - 1) / BN * BN;
@@ -1200,7 +1218,9 @@ struct Geo {
 inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
   Geo g{};
   g.taps = kh * kw;
-  g.RB = pick_rb(CI);
+  // 3x3: 64-byte slabs (32 channels) -> small window stages, deep prefetch beside the
+  // resident weights
+  g.RB = (CI <= 32 || g.taps == 9) ? 64 : pick_rb(CI);
   g.BN = pick_bn(N);
   if (dgrad && g.BN > 128) g.BN = 128;
   g.ntiles = (N + g.BN - 1) / g.BN;
@@ -1228,7 +1248,7 @@ static int launch_t(WcParams p, cudaStream_t st) {
     attr = c.total;
   }
   const int grid = p.tiles < num_sms_wc() ? p.tiles : num_sms_wc();
-  kern<<<grid, WC_THREADS, c.total, st>>>(p);
+  launch(kern, dim3(grid), dim3(WC_THREADS), c.total, st, p);
   return check_launch("wconv");
 }
 
@@ -1320,7 +1340,7 @@ extern "C" int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, in
     const long long total = (long long)g.nslab * g.taps * g.npad * (g.RB / 2);
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    wc::pack_window_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    launch(wc::pack_window_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, 
         w, c_out, c_in, kh, kw, d, CI, N, g.npad, g.RB, g.nslab, (__nv_bfloat16*)out);
     int rc = check_launch("pack_window");
     if (rc) return rc;
@@ -1457,7 +1477,7 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   const int M4 = q.taps * p.cin * (p.cout / 4);
   int blocks = (M4 + 31) / 32;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  wc::wg_reduce_kernel<<<blocks, 256, 0, st>>>(ws, q.splits, q.taps, p.cin, p.cout,
+  launch(wc::wg_reduce_kernel, dim3(blocks), dim3(256), 0, st, ws, q.splits, q.taps, p.cin, p.cout,
                                                dw_cin > 0 ? dw_cin : p.cin, dw, p.wsb, dbias);
   return check_launch("wgrad window reduce");
 }
@@ -1470,6 +1490,6 @@ extern "C" int bnff_pack_window_multi(int32_t dtype, int32_t njobs, const bnff_p
   if (bx > 64) bx = 64;
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)njobs, 2);
-  wc::pack_window_multi_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(jobs_dev);
+  launch(wc::pack_window_multi_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, jobs_dev);
   return check_launch("pack_window_multi");
 }

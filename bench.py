@@ -144,11 +144,11 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def build_engine(level, dtype, batch, lr, world):
+def build_engine(level, dtype, batch, lr, world, sync_bn=False):
     from paper_1807_01702_b200 import fusion, graph as G
     from paper_1807_01702_b200.engine import Engine
     g, _ = fusion.plan(G.build_model(G.densenet121(batch), seed=0), fusion.parse_level(level))
-    return g, Engine(g, dtype=dtype, input_grad=False, lr=lr / world)
+    return g, Engine(g, dtype=dtype, input_grad=False, lr=lr / world, sync_bn=sync_bn)
 
 
 def timed_steps(trainer, steps, warmup, dist_on):
@@ -224,7 +224,7 @@ def run_ours(args):
     dist_on = world > 1
     hbm, tf_burst, tf_sust, peak_kind = load_peaks()
     batch = args.batch
-    g, eng = build_engine(args.level, args.dtype, batch, args.lr, world)
+    g, eng = build_engine(args.level, args.dtype, batch, args.lr, world, args.syncbn)
     trainer = dp.DPTrainer(eng)
     # synthetic batch: rows [rank*b, (rank+1)*b) of one global batch drawn with seed 1
     rng = Rng(1)
@@ -316,7 +316,7 @@ def run_ours(args):
         "data": "synthetic (x~U(-1,1), dy~N(0,1), He-uniform weights, seed 0)",
         "config": {"workload": WORKLOAD, "model": "densenet-121", "global_batch": batch * world,
                    "per_gpu_batch": batch, "image": 224, "level": args.level,
-                   "parallelism": f"dp{world}", "l2": "inputs larger than L2 (activations "
+                   "parallelism": f"dp{world}", "sync_bn": bool(args.syncbn), "l2": "inputs larger than L2 (activations "
                    f"~GBs/step stream through HBM)", "cuda_graph": True,
                    "input_grad": False},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
@@ -341,6 +341,8 @@ def main():
     ap.add_argument("--ref-batch", type=int, default=2)
     ap.add_argument("--no-unfused", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--syncbn", action="store_true",
+                    help="global-batch BN statistics across replicas (2*C all-reduces per BN)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

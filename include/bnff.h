@@ -206,6 +206,17 @@ int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count,
                    double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
                    float* mean32, float* inv32, float* dgamma32, float* dbeta32, void* stream);
 
+/* SyncBN (data parallel with global-batch statistics): bnff_stats_finalize with mean/var
+ * NULL reduces partials to float64 (sum, sumsq) only; the caller all-reduces them and
+ * finalizes here with the global count.  Backward likewise: reduce (dbeta, dgamma)
+ * partials with bnff_stats_finalize, all-reduce, then bnff_dx_coeffs_from_sums.     */
+int bnff_stats_from_sums(int32_t c, int64_t count, const double* sum, const double* sumsq,
+                         double* mean, double* var, void* stream);
+int bnff_dx_coeffs_from_sums(int32_t c, int64_t count, const double* dbeta64, const double* dgamma64,
+                             const double* mean, const double* var, const float* gamma, float eps,
+                             float* k1, float* k2, float* g, float* mean32, float* inv32, void* stream);
+int bnff_sums_to_f32(int32_t c, const double* a, const double* b, float* a32, float* b32, void* stream);
+
 /* K6: y = (x-mean)*scale+beta [relu]  (bn_fwd ops.py:240-254, FissionSubBN2 execute.py:211-217) */
 int bnff_bn_apply(int32_t dtype, bnff_view x, bnff_view y, bnff_coef coef, int32_t relu,
                   void* stream);

@@ -94,6 +94,10 @@ SIGNATURES = {
     "bnff_bn_coeffs": (C.c_int, [_I32, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),
     "bnff_dx_coeffs": (C.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _P]),
+    "bnff_stats_from_sums": (C.c_int, [_I32, _I64, _P, _P, _P, _P, _P]),
+    "bnff_dx_coeffs_from_sums": (C.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P,
+                                           _P]),
+    "bnff_sums_to_f32": (C.c_int, [_I32, _P, _P, _P, _P, _P]),
     "bnff_bn_apply": (C.c_int, [_I32, View, View, Coef, _I32, _P]),
     "bnff_grad_sum": (C.c_int, [_I32, View, _I32, C.POINTER(GradTerm), _I32, _P]),
     "bnff_relu_fwd": (C.c_int, [_I32, View, View, _P]),

@@ -1077,3 +1077,55 @@ extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, i
                                                                                 (int)dy.c, dbias);
   return check_launch("dbias");
 }
+
+// ---------------------------------------------------------------------------
+// SyncBN helpers: finalize from (all-reduced) float64 sums
+// ---------------------------------------------------------------------------
+namespace bnff {
+__global__ void dx_coeffs_from_sums_kernel(int C, long long count, const double* dbeta64,
+                                           const double* dgamma64, const double* mean, const double* var,
+                                           const float* gamma, float eps, float* k1, float* k2, float* g,
+                                           float* mean32, float* inv32) {
+  griddep_launch();
+  griddep_wait();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double v = var[c] > 0.0 ? var[c] : 0.0;
+  const double inv = 1.0 / sqrt(v + (double)eps);
+  k1[c] = (float)(dbeta64[c] / (double)count);
+  k2[c] = (float)(dgamma64[c] / (double)count);
+  g[c] = (float)((double)gamma[c] * inv);
+  mean32[c] = (float)mean[c];
+  inv32[c] = (float)inv;
+}
+__global__ void sums_to_f32_kernel(int C, const double* a, const double* b, float* a32, float* b32) {
+  griddep_launch();
+  griddep_wait();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  if (a32) a32[c] = (float)a[c];
+  if (b32) b32[c] = (float)b[c];
+}
+}  // namespace bnff
+
+extern "C" int bnff_stats_from_sums(int32_t c, int64_t count, const double* sum, const double* sumsq,
+                                    double* mean, double* var, void* stream) {
+  launch(stats_from_sums_kernel, dim3((c + 127) / 128), dim3(128), 0, (cudaStream_t)stream, c,
+         (long long)count, sum, sumsq, mean, var);
+  return check_launch("stats_from_sums");
+}
+
+extern "C" int bnff_dx_coeffs_from_sums(int32_t c, int64_t count, const double* dbeta64, const double* dgamma64,
+                                        const double* mean, const double* var, const float* gamma, float eps,
+                                        float* k1, float* k2, float* g, float* mean32, float* inv32,
+                                        void* stream) {
+  launch(dx_coeffs_from_sums_kernel, dim3((c + 127) / 128), dim3(128), 0, (cudaStream_t)stream, c,
+         (long long)count, dbeta64, dgamma64, mean, var, gamma, eps, k1, k2, g, mean32, inv32);
+  return check_launch("dx_coeffs_from_sums");
+}
+
+extern "C" int bnff_sums_to_f32(int32_t c, const double* a, const double* b, float* a32, float* b32,
+                                void* stream) {
+  launch(sums_to_f32_kernel, dim3((c + 127) / 128), dim3(128), 0, (cudaStream_t)stream, c, a, b, a32, b32);
+  return check_launch("sums_to_f32");
+}

@@ -129,7 +129,8 @@ class Engine:
     """
 
     def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
-                 save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True):
+                 save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True,
+                 sync_bn: bool = False, group=None):
         self.L = _lib.lib()
         self.g = g
         self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
@@ -139,6 +140,14 @@ class Engine:
         self.input_grad = input_grad
         self.save_postrelu = save_postrelu
         self.lr = float(lr)
+        # SyncBN: BN statistics (and the dx reductions) over the global batch of all
+        # data-parallel replicas -- 2*C float64 all-reduces per BN in each pass
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.sync_bn = bool(sync_bn) and self.world > 1
+        if self.sync_bn and any(n.kind == G.BN and not n.attrs.onepass for n in g.nodes):
+            raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window) and self.dcode == _lib.BF16
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
         self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
@@ -256,9 +265,28 @@ class Engine:
         thunk.launches = launches  # kernels this C-ABI call launches
         self._cur.append(thunk)
 
+    def _emit_allreduce(self, *tensors, what="allreduce"):
+        import torch.distributed as dist
+        grp = self.group
+
+        def _ar(stream, ts=tensors):
+            for t in ts:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=grp)
+        _ar.what, _ar.kind, _ar.nbytes, _ar.flops, _ar.launches = what, "allreduce", 0, 0, 0
+        self._cur.append(_ar)
+
     def _emit_stats_finalize(self, part, tiles, c, count, st: Stats):
+        if not self.sync_bn:
+            self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
+                       _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize")
+            return
+        # SyncBN: local float64 sums -> all-reduce -> moments over the global count
         self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
-                   _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize", launches=3)
+                   _ptr(st.sumsq), None, None, what="stats_finalize")
+        self._emit_allreduce(st.sum, st.sumsq, what="syncbn_fwd_allreduce")
+        st.count = count * self.world
+        self._emit(self.L.bnff_stats_from_sums, c, st.count, _ptr(st.sum), _ptr(st.sumsq),
+                   _ptr(st.mean), _ptr(st.var), what="stats_finalize")
 
     def _pack(self, conv, cin_store, hw=None):
         key = conv.name
@@ -607,11 +635,26 @@ class Engine:
     def _dx_coeffs(self, part, tiles, c, count, st: Stats, bn, tag):
         k1, k2, gg, m32, i32 = (self._zeros((c,), torch.float32) for _ in range(5))
         dg64, db64 = self._zeros((c,), torch.float64), self._zeros((c,), torch.float64)
-        self._emit(self.L.bnff_dx_coeffs, c, _ptr(part), tiles, count, _ptr(st.mean), _ptr(st.var),
-                   _ptr(self.param(f"{bn.name}.gamma")), C.c_float(bn.eps), _ptr(dg64), _ptr(db64),
-                   _ptr(k1), _ptr(k2), _ptr(gg), _ptr(m32), _ptr(i32),
+        if not self.sync_bn:
+            self._emit(self.L.bnff_dx_coeffs, c, _ptr(part), tiles, count, _ptr(st.mean),
+                       _ptr(st.var), _ptr(self.param(f"{bn.name}.gamma")), C.c_float(bn.eps),
+                       _ptr(dg64), _ptr(db64), _ptr(k1), _ptr(k2), _ptr(gg), _ptr(m32), _ptr(i32),
+                       _ptr(self.grad(f"{bn.name}.gamma")), _ptr(self.grad(f"{bn.name}.beta")),
+                       what=f"dx_coeffs {tag}")
+            return m32, i32, k1, k2, gg
+        # SyncBN: the replica's own (dbeta, dgamma) sums become its parameter gradients (the
+        # data-parallel gradient all-reduce adds them up); the dx coefficients use the
+        # all-reduced global sums and the global count.
+        self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(db64), _ptr(dg64),
+                   None, None, what=f"dx_coeffs {tag}")
+        self._emit(self.L.bnff_sums_to_f32, c, _ptr(dg64), _ptr(db64),
                    _ptr(self.grad(f"{bn.name}.gamma")), _ptr(self.grad(f"{bn.name}.beta")),
-                   what=f"dx_coeffs {tag}", launches=3)
+                   what=f"dx_coeffs {tag}")
+        self._emit_allreduce(db64, dg64, what="syncbn_bwd_allreduce")
+        self._emit(self.L.bnff_dx_coeffs_from_sums, c, st.count, _ptr(db64), _ptr(dg64),
+                   _ptr(st.mean), _ptr(st.var), _ptr(self.param(f"{bn.name}.gamma")),
+                   C.c_float(bn.eps), _ptr(k1), _ptr(k2), _ptr(gg), _ptr(m32), _ptr(i32),
+                   what=f"dx_coeffs {tag}")
         return m32, i32, k1, k2, gg
 
     def _bn_grad_sums(self, x, dy, tables, st, bn, tag):

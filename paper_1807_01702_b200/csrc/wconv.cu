@@ -39,7 +39,7 @@ constexpr int LT = NLW * 32;            // loader threads
 constexpr int THREADS = (NLW + 1 + 4) * 32;      // wgrad kernel: 4 epilogue warps
 constexpr int NEW = 8;                           // wconv: epilogue warps (2 groups of 4)
 constexpr int WC_THREADS = (NLW + 1 + NEW) * 32;
-constexpr int RMAX = 256;               // max window rows (wp <= 63 for 3x3)
+constexpr int RMAX = 384;               // max window rows (wp <= 127 for 3x3)
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int kWindowNoFit = -100;      // internal: shape does not fit, use the generic kernel
 
@@ -1411,6 +1411,7 @@ static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
   if (q.taps == 9) {
     q.BN = 32; q.MT = 1; q.KB = 128;
     q.RA = align_up(q.KB + 2 * q.wp + 2, 8);
+    if (q.RA > q.KB + 128) return q;  // window taller than WgL::RAMAX: generic kernel
   } else {
     q.BN = pick_bn(cout);
     q.MT = (q.BN <= 128 && cin > 128) ? 2 : 1;
@@ -1452,7 +1453,7 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
                                  int32_t dw_cin, float* dbias, void* stream) {
   const int pad = kh / 2;
   const wc::WgPlan q = wc::wg_plan((int)x.n, (int)x.h, (int)x.w, (int)x.c, (int)dy.c, kh, pad);
-  if (!q.ok) return set_error(BNFF_ERR_UNSUPPORTED, "wgrad window: grid too large");
+  if (!q.ok) return wc::kWindowNoFit;  // caller uses the generic kernel
   wc::WgParams p{};
   p.n = (int)x.n; p.h = (int)x.h; p.w = (int)x.w; p.hp = q.hp; p.wp = q.wp; p.pad = pad; p.Q = q.Q;
   p.fd_hpwp = make_fastdiv(q.hp * q.wp);

@@ -247,6 +247,19 @@ int bnff_copy(int32_t dtype, bnff_view src, bnff_view dst, void* stream);
 int bnff_nchw_to_nhwc(int32_t dtype, const float* src, int64_t n, int64_t c, int64_t h,
                       int64_t w, bnff_view dst, void* stream);
 int bnff_nhwc_to_nchw(int32_t dtype, bnff_view src, float* dst, void* stream);
+/* K13: channel-poor stem conv as a GEMM (csrc/stem.cu).  The 7x7/s2 conv over the
+ * 3-channel image (graph.py:358-375) reads its input through a packed patch matrix
+ * col (n, oh, ow, kpad), k = (ky*kw + kx)*c_real + ci, zero beyond kh*kw*c_real; the
+ * conv is then a 1x1 conv over col (forward and weight gradient), replacing the
+ * 49-chunk gather of conv2d_fwd/conv2d_bwd (ops.py:151-204) for this layer.
+ * x must be stored with 8 channels (bf16).  weight_to_cols / cols_to_weight move
+ * fp32 weights between (c_out, c_in, kh, kw) and (c_out, kpad).                  */
+int bnff_im2col(int32_t dtype, bnff_view x, int32_t c_real, int32_t kh, int32_t kw, int32_t stride,
+                int32_t pad, bnff_view col, void* stream);
+int bnff_weight_to_cols(const float* w, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
+                        int32_t kpad, float* w2, void* stream);
+int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
+                        int32_t kpad, float* dw, void* stream);
 /* K12: multi-tensor SGD w -= lr*g over a flat fp32 buffer */
 int bnff_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
 

@@ -588,14 +588,25 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
         float acc[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = 0.f;
-        for (int dy = 0; dy < k; ++dy)
-          for (int dx = 0; dx < k; ++dx) {
-            float f[V];
-            const long long src = ((long long)img * h + oy * k + dy) * w + ox * k + dx;
-            VecIO<T>::load(x.p, src * x.rs + c0, f);
+        if (k == 2) {  // the transitions and the stem: four independent 16-byte loads in flight
+          const long long s0 = ((long long)img * h + oy * 2) * w + ox * 2;
+          float f0[V], f1[V], f2[V], f3[V];
+          VecIO<T>::load(x.p, s0 * x.rs + c0, f0);
+          VecIO<T>::load(x.p, (s0 + 1) * x.rs + c0, f1);
+          VecIO<T>::load(x.p, (s0 + w) * x.rs + c0, f2);
+          VecIO<T>::load(x.p, (s0 + w + 1) * x.rs + c0, f3);
 #pragma unroll
-            for (int i = 0; i < V; ++i) acc[i] += f[i];
-          }
+          for (int i = 0; i < V; ++i) acc[i] = ((f0[i] + f1[i]) + f2[i]) + f3[i];
+        } else {
+          for (int dy = 0; dy < k; ++dy)
+            for (int dx = 0; dx < k; ++dx) {
+              float f[V];
+              const long long src = ((long long)img * h + oy * k + dy) * w + ox * k + dx;
+              VecIO<T>::load(x.p, src * x.rs + c0, f);
+#pragma unroll
+              for (int i = 0; i < V; ++i) acc[i] += f[i];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = VecIO<T>::round(acc[i] * inv);
         VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, acc);
@@ -629,6 +640,64 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
         part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
         part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
       }
+    }
+    __syncthreads();
+  }
+}
+
+// large windows without statistics (the global head pool, ops.py:428-441 with k = h):
+// one CTA per output pixel, the k*k window split over thread groups that each sum a
+// fixed strided subset of window positions, then combined in group order (deterministic)
+template <typename T>
+__global__ void __launch_bounds__(256) avgpool_wide_kernel(View x, View y, int h, int w, int oh, int ow,
+                                                           int C, int k) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[256][V];
+  const int cpr = C / V;
+  const int groups = cpr >= 256 ? 1 : 256 / cpr;
+  const int j = threadIdx.x % cpr, g = threadIdx.x / cpr;
+  const int r = blockIdx.x;
+  const int img = r / (oh * ow), rem = r - img * oh * ow;
+  const int oy = rem / ow, ox = rem - oy * ow;
+  const float inv = 1.f / (float)(k * k);
+  for (int jj = j; jj < cpr; jj += (cpr >= 256 ? 256 : cpr)) {
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    if (g < groups) {
+      int t = g;
+      for (; t + 3 * groups < k * k; t += 4 * groups) {  // four loads in flight, summed in order
+        float f[4][V];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tt = t + u * groups, dy = tt / k, dx = tt - dy * k;
+          VecIO<T>::load(x.p, (((long long)img * h + oy * k + dy) * w + ox * k + dx) * x.rs + jj * V, f[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] += f[u][i];
+      }
+      for (; t < k * k; t += groups) {
+        const int dy = t / k, dx = t - dy * k;
+        float f[V];
+        VecIO<T>::load(x.p, (((long long)img * h + oy * k + dy) * w + ox * k + dx) * x.rs + jj * V, f);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] += f[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) sh[threadIdx.x][i] = acc[i];
+    __syncthreads();
+    if (g == 0) {
+      for (int q = 1; q < groups; ++q)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] += sh[q * cpr + j][i];
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = VecIO<T>::round(acc[i] * inv);
+      VecIO<T>::store(const_cast<void*>(y.p), (long long)r * y.rs + jj * V, acc);
     }
     __syncthreads();
   }
@@ -964,6 +1033,11 @@ extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t
   if (y.h != x.h / k || y.w != x.w / k || y.c != x.c || y.n != x.n || y.h < 1 || y.w < 1)
     return set_error(BNFF_ERR_SHAPE, "avgpool: bad output dims");
   const long long pixels = y.n * y.h * y.w;
+  if (stat_part == nullptr && k * k > 4 && pixels <= 148 * 64) {
+    BNFF_DISPATCH(dtype, avgpool_wide_kernel, (int)pixels, 256, 0, (cudaStream_t)stream, vw(x), vw(y), (int)x.h,
+                  (int)x.w, (int)y.h, (int)y.w, (int)x.c, k);
+    return check_launch("avgpool_fwd");
+  }
   BNFF_DISPATCH(dtype, avgpool_fwd_kernel, sum_tiles(pixels), kSumThreads, 0, (cudaStream_t)stream, vw(x), vw(y),
                 (int)x.n, (int)x.h, (int)x.w, (int)y.h, (int)y.w, (int)x.c, k, stat_part);
   return check_launch("avgpool_fwd");

@@ -262,3 +262,69 @@ __device__ __forceinline__ uint32_t pack_bf16_rn(float lo, float hi) {
   return r;
 }
 }  // namespace bnff
+
+// ---------------------------------------------------------------------------
+// tensor TMA (cp.async.bulk.tensor): tiled boxes of an NHWC view, out-of-bounds
+// elements (negative or past-the-end coordinates) are zero-filled by the engine
+// ---------------------------------------------------------------------------
+#include <cuda.h>
+namespace bnff {
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(dst), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
+}
+
+// host: cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+inline EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+// bf16 NHWC view (ptr, n, h, w, c, row_stride elements) as a rank-2 {c, n*h*w} or
+// rank-4 {c, w, h, n} tensor; box {bc, b1[, b2, b3]}; swizzle 64B/128B by box row bytes
+inline bool encode_nhwc_bf16(CUtensorMap* tm, const void* ptr, long long n, long long h, long long w,
+                             long long c, long long rs, int rank, const uint32_t* box) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t bx[4], es[4] = {1, 1, 1, 1};
+  dims[0] = (cuuint64_t)c;
+  if (rank == 2) {
+    dims[1] = (cuuint64_t)(n * h * w);
+    strides[0] = (cuuint64_t)rs * 2;
+  } else {
+    dims[1] = (cuuint64_t)w; dims[2] = (cuuint64_t)h; dims[3] = (cuuint64_t)n;
+    strides[0] = (cuuint64_t)rs * 2;
+    strides[1] = (cuuint64_t)(w * rs) * 2;
+    strides[2] = (cuuint64_t)(h * w * rs) * 2;
+  }
+  for (int i = 0; i < rank; ++i) bx[i] = box[i];
+  const CUtensorMapSwizzle sw = box[0] * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                  : (box[0] * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                      : CU_TENSOR_MAP_SWIZZLE_32B);
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(ptr), dims, strides, bx,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace bnff

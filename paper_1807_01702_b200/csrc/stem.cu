@@ -1,0 +1,161 @@
+// stem.cu -- channel-poor stem convolution (the DenseNet/ResNet 7x7/s2 conv over the
+// 3-channel image, graph.py:358-375 of the reference) recast as a dense GEMM.
+//
+// The image is stored NHWC with its 3 channels padded to 8 (16 B per pixel).  Read as an
+// implicit GEMM directly, every output pixel gathers 49 16-byte chunks of which 5/8 are
+// padding (K = 392 for 147 real taps*channels) and the gather is latency-bound.  Here one
+// HBM-bound pass writes the packed patch matrix col[p][k], k = (ky*kw + kx)*c + ci
+// (K = 147 padded to 160), after which the forward conv is a 1x1 conv over col (the
+// window-shift tcgen05 kernel, with its bias / sub-BN1 statistics epilogue) and the
+// weight gradient is that 1x1 conv's wgrad; two tiny kernels move the weights between
+// the reference layout (co, ci, kh, kw) and the (co, k) matrix.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "sm100.cuh"
+#include "common.cuh"
+
+namespace bnff {
+namespace stem {
+
+// one CTA: tp consecutive output pixels of one output row.  The kh input rows the tile
+// touches are staged in shared memory as 16-byte pixels; a per-CTA table maps each patch
+// column k to its element offset in that stage (-1: K padding), so every thread builds
+// whole 16-byte chunks of patch rows (8 table-driven shared loads) and stores them
+// coalesced.
+__global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __restrict__ x, long long x_rs,
+                                                     int h, int w, int oh, int ow, int kh, int kw,
+                                                     int stride, int pad, int creal, int kpad, int tp,
+                                                     __nv_bfloat16* __restrict__ col, long long col_rs) {
+  griddep_launch();
+  extern __shared__ uint4 tile[];  // [kh][tw] pixels of 8 bf16, then int koff[kpad]
+  const int tpr = (ow + tp - 1) / tp;
+  const int b = blockIdx.x;
+  const int row = b / tpr;  // img * oh + oy
+  const int ox0 = (b - row * tpr) * tp;
+  const int img = row / oh, oy = row - img * oh;
+  const int tw = (tp - 1) * stride + kw;
+  const int ix0 = ox0 * stride - pad, iy0 = oy * stride - pad;
+  const int K = kh * kw * creal;
+  const int np = min(tp, ow - ox0);
+  int* koff = reinterpret_cast<int*>(tile + kh * tw);
+  for (int k = threadIdx.x; k < kpad; k += blockDim.x) {
+    int o = -1;
+    if (k < K) {
+      const int tap = k / creal, ci = k - tap * creal;
+      const int ky = tap / kw, kx = tap - ky * kw;
+      o = (ky * tw + kx) * 8 + ci;
+    }
+    koff[k] = o;
+  }
+  griddep_wait();
+  for (int i = threadIdx.x; i < kh * tw; i += blockDim.x) {
+    const int ky = i / tw, t = i - ky * tw;
+    const int iy = iy0 + ky, ix = ix0 + t;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w)
+      v = __ldg(reinterpret_cast<const uint4*>(x + ((long long)(img * h + iy) * w + ix) * x_rs));
+    tile[i] = v;
+  }
+  __syncthreads();
+  const unsigned short* ts = reinterpret_cast<const unsigned short*>(tile);
+  const int cpp = kpad / 8;  // 16-byte chunks per patch row
+  const long long p0 = (long long)row * ow + ox0;
+  for (int i = threadIdx.x; i < np * cpp; i += blockDim.x) {
+    const int p = i / cpp, j = i - p * cpp;
+    const int pb = p * stride * 8;
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int o0 = koff[j * 8 + 2 * e], o1 = koff[j * 8 + 2 * e + 1];
+      const uint32_t lo = o0 >= 0 ? ts[o0 + pb] : 0u, hi = o1 >= 0 ? ts[o1 + pb] : 0u;
+      v[e] = lo | (hi << 16);
+    }
+    *reinterpret_cast<uint4*>(col + (p0 + p) * col_rs + j * 8) = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// w (co, ci, kh, kw) fp32 -> w2 (co, kpad) fp32, k = (ky*kw + kx)*ci_n + ci; zero tail
+__global__ void weight_to_cols_kernel(const float* __restrict__ w, int co_n, int ci_n, int kh, int kw,
+                                      int kpad, float* __restrict__ w2) {
+  griddep_launch();
+  griddep_wait();
+  const int K = kh * kw * ci_n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < co_n * kpad; i += gridDim.x * blockDim.x) {
+    const int co = i / kpad, k = i - co * kpad;
+    float v = 0.f;
+    if (k < K) {
+      const int tap = k / ci_n, ci = k - tap * ci_n;
+      v = w[((long long)co * ci_n + ci) * kh * kw + tap];
+    }
+    w2[i] = v;
+  }
+}
+
+// dw2 (co, kpad) -> dw (co, ci, kh, kw): the inverse gather for the weight gradient
+__global__ void cols_to_weight_kernel(const float* __restrict__ dw2, int co_n, int ci_n, int kh, int kw,
+                                      int kpad, float* __restrict__ dw) {
+  griddep_launch();
+  griddep_wait();
+  const int taps = kh * kw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < co_n * ci_n * taps; i += gridDim.x * blockDim.x) {
+    const int tap = i % taps;
+    const int t = i / taps;
+    const int ci = t % ci_n, co = t / ci_n;
+    dw[i] = dw2[(long long)co * kpad + tap * ci_n + ci];
+  }
+}
+
+}  // namespace stem
+}  // namespace bnff
+
+using namespace bnff;
+
+extern "C" int bnff_im2col(int32_t dtype, bnff_view x, int32_t c_real, int32_t kh, int32_t kw,
+                           int32_t stride, int32_t pad, bnff_view col, void* stream) {
+  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "im2col: bf16 only");
+  if (x.c != 8 || c_real < 1 || c_real > 8)
+    return set_error(BNFF_ERR_UNSUPPORTED, "im2col: input must be stored with 8 channels (got %lld)",
+                     (long long)x.c);
+  if (kh < 1 || kw < 1 || stride < 1 || pad < 0) return set_error(BNFF_ERR_SHAPE, "im2col: bad conv geometry");
+  const long long oh = (x.h + 2 * pad - kh) / stride + 1, ow = (x.w + 2 * pad - kw) / stride + 1;
+  if (col.n != x.n || col.h != oh || col.w != ow)
+    return set_error(BNFF_ERR_SHAPE, "im2col: col (%lld,%lld,%lld) != (%lld,%lld,%lld)", (long long)col.n,
+                     (long long)col.h, (long long)col.w, (long long)x.n, oh, ow);
+  if (col.c % 8 || col.c < (long long)kh * kw * c_real || col.row_stride % 8 || x.row_stride % 8)
+    return set_error(BNFF_ERR_SHAPE, "im2col: col channels %lld must be a multiple of 8 >= %d",
+                     (long long)col.c, kh * kw * c_real);
+  const int tp = ow <= 128 ? (int)ow : 64;
+  const int tw = (tp - 1) * stride + kw;
+  const size_t smem = (size_t)kh * tw * 16 + (size_t)col.c * 4;
+  if (smem > 200 * 1024) return set_error(BNFF_ERR_UNSUPPORTED, "im2col: window too large");
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(stem::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "im2col attr");
+  }
+  const long long blocks = x.n * oh * ((ow + tp - 1) / tp);
+  if (blocks == 0) return BNFF_OK;
+  launch(stem::im2col_kernel, dim3((unsigned)blocks), dim3(256), smem, (cudaStream_t)stream,
+         (const __nv_bfloat16*)x.ptr, (long long)x.row_stride, (int)x.h, (int)x.w, (int)oh, (int)ow, kh, kw,
+         stride, pad, c_real, (int)col.c, tp, (__nv_bfloat16*)col.ptr, (long long)col.row_stride);
+  return check_launch("im2col");
+}
+
+extern "C" int bnff_weight_to_cols(const float* w, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
+                                   int32_t kpad, float* w2, void* stream) {
+  if (kpad < c_in * kh * kw) return set_error(BNFF_ERR_SHAPE, "weight_to_cols: kpad too small");
+  const int n = c_out * kpad;
+  launch(stem::weight_to_cols_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, w, c_out,
+         c_in, kh, kw, kpad, w2);
+  return check_launch("weight_to_cols");
+}
+
+extern "C" int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
+                                   int32_t kpad, float* dw, void* stream) {
+  if (kpad < c_in * kh * kw) return set_error(BNFF_ERR_SHAPE, "cols_to_weight: kpad too small");
+  const int n = c_out * c_in * kh * kw;
+  launch(stem::cols_to_weight_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, dw2, c_out,
+         c_in, kh, kw, kpad, dw);
+  return check_launch("cols_to_weight");
+}

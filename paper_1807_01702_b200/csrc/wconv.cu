@@ -44,6 +44,13 @@ constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int kWindowNoFit = -100;      // internal: shape does not fit, use the generic kernel
 
 struct WcParams {
+  // TMA boxes of the window operand (and of the BN_DX x operand): rank 2 {c, pixels}
+  // box {slab, 128} for 1x1; rank 4 {c, w, h, n} box {slab, wp, BR, BI} for 3x3
+  CUtensorMap tma_a, tma_x;
+  // 3x3 tiling: tmode 1 = kt output rows of one image (window rows oy-1 .. oy+kt),
+  // tmode 2 = kt whole images per tile (small maps); WPI = window rows per image block,
+  // tpi = tiles per image (tmode 1), Rld = rows the TMA writes per stage
+  int tmode, kt, BR, BI, WPI, tpi, Rld, P;
   int n, h, w, hp, wp, pad, Q, mtiles, ntiles, tiles, R, stages;
   FastDiv fd_hpwp, fd_wp;
   int ci, nslab, N, npad;
@@ -155,14 +162,14 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 }
 
 template <int BN, int RB, int TAPS, int MODE>
-__global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) {
+__global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_constant__ WcParams p) {
   griddep_launch();
   using L = Layout<BN, RB, TAPS, MODE>;
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
   uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], w_bar;
+  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar;
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
   const Carve cv = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, p.stages, xop_s);
@@ -185,7 +192,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full_bar[s], LT + (L::WRES ? 0 : 1));
       mbar_init(&empty_bar[s], 1);
+      mbar_init(&ld_bar[s], 1);
     }
+    tma_prefetch_desc(&p.tma_a);
+    if (xop_s) tma_prefetch_desc(&p.tma_x);
     for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], NEW * 32); }
     mbar_init(&w_bar, 1);
     fence_mbar_init();
@@ -244,6 +254,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     sacc[c] = 0.f;
     sacc[BN + c] = 0.f;
   }
+  if (TAPS == 9) {  // window row -> (image block, padded row, padded column), same every tile
+    for (int r = tid; r < p.Rld; r += WC_THREADS) {
+      const int i = r / p.WPI, rem = r - i * p.WPI;
+      const int ry = rem / p.wp, rx = rem - ry * p.wp;
+      rowtab[r] = (i << 20) | (ry << 10) | rx;
+    }
+  }
   if (p.stat_part != nullptr && p.ntiles > 1)  // this CTA's partial row accumulates in place
     for (int c = tid; c < 2 * p.N; c += WC_THREADS) p.stat_part[(long long)blockIdx.x * 2 * p.N + c] = 0.f;
   tc_fence_before();
@@ -256,82 +273,63 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
   auto stage_b = [&](int s) {
     return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (xop_s ? 2 : 1);
   };
-  auto tile_of = [&](int it, int& q0, int& n0) {
+  auto tile_of = [&](int it, int& mt, int& n0) {
     const int t = (int)blockIdx.x + it * (int)gridDim.x;
-    q0 = (t / p.ntiles) * 128;
+    mt = t / p.ntiles;
     n0 = (t % p.ntiles) * BN;
+  };
+  // 3x3 tile origin: first image and the padded-input row the window starts at
+  auto tile_org = [&](int mt, int& img0, int& y0) {
+    if (p.tmode == 1) {
+      img0 = mt / p.tpi;
+      y0 = (mt - img0 * p.tpi) * p.kt - 1;
+    } else {
+      img0 = mt * p.kt;
+      y0 = -1;
+    }
   };
 
   if (warp < NLW) {
     // =============================== loaders ===============================
-    // issue (cp.async, zero-fill for padding rows) runs LAG stages ahead of the in-place
-    // transform; the MMA consumes a stage once the transform has arrived on full_bar.
+    // thread 0 issues one TMA box per stage (zero-filled outside the map: the 3x3 halo
+    // and the image border come for free), LAG stages ahead of the in-place transform;
+    // the MMA consumes a stage once every loader thread has transformed its rows and
+    // arrived on full_bar.
     const int j = tid % CPR, r0 = tid / CPR;
-    const int hpwp = p.hp * p.wp;
     const int G = ntl * p.nslab;
-    // loads in flight vs transformed stages waiting for / inside the MMA: split the ring
     const int LAG = ST / 2 > 1 ? ST / 2 : 1;
     const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
     const bool need_t = p.pro != BNFF_PRO_NONE;
+    const uint32_t tx_bytes = (uint32_t)p.Rld * RB * (xop ? 2u : 1u);
     for (int g = 0; g < G + LAG; ++g) {
-      if (g < G) {
+      if (g < G && tid == 0) {
         const int it = g / p.nslab, s = g - it * p.nslab;
-        int q0, n0;
-        tile_of(it, q0, n0);
-        int* rt = rowtab + (it & 1) * RMAX;
-        if (s == 0) {
-          for (int r = tid; r < p.R; r += LT) {
-            const int q = q0 + r;
-            int src = -1;
-            if (q < p.Q) {
-              const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
-              const int rem = q - img * hpwp;
-              const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
-              const int px = rem - py * p.wp;
-              const int iy = py - p.pad, ix = px - p.pad;
-              if (iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) src = (img * p.h + iy) * p.w + ix;
-            }
-            rt[r] = src;
-          }
-          named_bar_sync(1, LT);
-        }
+        int mt, n0;
+        tile_of(it, mt, n0);
         const int st = g % ST;
         if (g >= ST) mbar_wait(&empty_bar[st], ((g / ST) - 1) & 1);
-        if (!L::WRES && tid == 0) {
+        if (!L::WRES) {
           mbar_arrive_expect_tx(&full_bar[st], BN * RB);
           bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
                    &full_bar[st]);
         }
-        const int cs = min(SLABW, p.ci - s * SLABW);
-        const int c0 = s * SLABW + j * 8;
-        uint32_t mask = 0;
-        if (j * 8 < cs) {
-          const uint32_t abase = smem_u32(stage_a(st)), xbase = smem_u32(stage_x(st));
-#pragma unroll
-          for (int u = 0; u < UR; ++u) {
-            const int r = r0 + u * RS;
-            if (r < p.R) {
-              const int src = rt[r];
-              const bool ok = src >= 0;
-              uint32_t off;
-              if constexpr (RB == 128) off = r * 128 + ((j ^ (r & 7)) << 4);
-              else off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
-              cp_async16(abase + off, p.src + (ok ? (long long)src * p.src_rs + c0 : 0), ok ? 16u : 0u);
-              if (xop)
-                cp_async16(xbase + off, p.srcx + (ok ? (long long)src * p.srcx_rs + c0 : 0),
-                           ok ? 16u : 0u);
-              mask |= (ok ? 1u : 0u) << u;
-            }
-          }
+        mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
+        const int c = s * SLABW;
+        if (TAPS == 9) {
+          int img0, y0;
+          tile_org(mt, img0, y0);
+          tma_load_4d(smem_u32(stage_a(st)), &p.tma_a, c, -1, y0, img0, &ld_bar[st]);
+          if (xop) tma_load_4d(smem_u32(stage_x(st)), &p.tma_x, c, -1, y0, img0, &ld_bar[st]);
+        } else {
+          tma_load_2d(smem_u32(stage_a(st)), &p.tma_a, c, mt * 128, &ld_bar[st]);
+          if (xop) tma_load_2d(smem_u32(stage_x(st)), &p.tma_x, c, mt * 128, &ld_bar[st]);
         }
-        meta[st * LT + tid] = mask;
       }
-      cp_async_commit();
       if (g >= LAG) {
         const int gg = g - LAG;
         const int st = gg % ST;
         const int it = gg / p.nslab, s = gg - it * p.nslab;
-        cp_async_wait_dyn(LAG);
+        mbar_wait(&ld_bar[st], (gg / ST) & 1);
         const int cs = min(SLABW, p.ci - s * SLABW);
         if (need_t && j * 8 < cs) {
           const int c0 = s * SLABW + j * 8;
@@ -342,13 +340,23 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
             t1[i] = ptab[kpad + c0 + i];
             t2[i] = ptab[2 * kpad + c0 + i];
           }
-          const uint32_t mask = meta[st * LT + tid];
+          int img0 = 0, y0 = 0;
+          if (TAPS == 9) {
+            int mt, n0;
+            tile_of(it, mt, n0);
+            tile_org(mt, img0, y0);
+          }
           uint8_t* A = stage_a(st);
           uint8_t* X = stage_x(st);
 #pragma unroll
           for (int u = 0; u < UR; ++u) {
             const int r = r0 + u * RS;
-            if (r >= p.R || !((mask >> u) & 1u)) continue;  // padding rows stay zero
+            if (r >= p.Rld) continue;
+            if (TAPS == 9) {  // halo / border positions stay zero (padding after normalize)
+              const int wr = rowtab[r];
+              const int y = y0 + ((wr >> 10) & 1023), rx = wr & 1023;
+              if ((unsigned)y >= (unsigned)p.h || rx < 1 || rx > p.w || img0 + (wr >> 20) >= p.n) continue;
+            }
             uint32_t off;
             if constexpr (RB == 128) off = r * 128 + ((j ^ (r & 7)) << 4);
             else off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
@@ -375,7 +383,6 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
         mbar_arrive(&full_bar[st]);
       }
     }
-    cp_async_wait<0>();
   } else if (warp == NLW) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
@@ -447,24 +454,31 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     float2 acc1[MYCH], acc2[MYCH];
 #pragma unroll
     for (int k = 0; k < MYCH; ++k) { acc1[k] = make_float2(0.f, 0.f); acc2[k] = make_float2(0.f, 0.f); }
-    auto pix_of = [&](int q) {
-      // output positions are the UNPADDED coordinates of the grid: (img, py, px), py<h, px<w
-      int px = -1;
-      if (q < p.Q) {
-        const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
-        const int rem = q - img * hpwp;
-        const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
-        const int pxx = rem - py * p.wp;
-        if (py < p.h && pxx < p.w) px = (img * p.h + py) * p.w + pxx;
+    auto out_pix = [&](int mt, int m) {
+      // output row m of m-tile mt -> output pixel (or -1: a padding column / row past the map)
+      if (TAPS == 1) {
+        const int q = mt * 128 + m;
+        return q < p.P ? q : -1;
       }
-      return px;
+      int img0, y0;
+      tile_org(mt, img0, y0);
+      int i = 0, rem = m;
+      if (p.tmode == 2) {
+        i = (int)fdiv((uint32_t)m, p.fd_hpwp);
+        rem = m - i * hpwp;
+      }
+      const int yo = (int)fdiv((uint32_t)rem, p.fd_wp);
+      const int x = rem - yo * p.wp;
+      const int y = y0 + 1 + yo;
+      const bool ok = x < p.w && y < p.h && (p.tmode == 2 ? (i < p.kt && img0 + i < p.n) : yo < p.kt);
+      return ok ? ((img0 + i) * p.h + y) * p.w + x : -1;
     };
     // one commit group per (tile, owned chunk), issued in order; empty groups keep the count
     auto fetch_x = [&](int it2, int k) {
       if (need_x && it2 < ntl && grp + 2 * k < NCH) {
-        int q0b, n0b;
-        tile_of(it2, q0b, n0b);
-        const int pix = pix_of(q0b + row);
+        int mtb, n0b;
+        tile_of(it2, mtb, n0b);
+        const int pix = out_pix(mtb, row);
         const uint32_t dst = smem_u32(xs0 + k * L::STG + row * L::SROWB);
         const int col = n0b + (grp + 2 * k) * CW;
         const bool ok = pix >= 0 && col < p.N;
@@ -509,9 +523,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const WcParams p) 
     for (int k = 0; k < MYCH; ++k) fetch_x(0, k);
     for (int it = 0; it < ntl; ++it) {
       const int buf = it & 1;
-      int q0, n0;
-      tile_of(it, q0, n0);
-      gpix[row] = pix_of(q0 + row);
+      int mt, n0;
+      tile_of(it, mt, n0);
+      gpix[row] = out_pix(mt, row);
       const int pix = gpix[row];
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
       tc_fence_after();
@@ -1167,29 +1181,37 @@ __global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs)
   const int npad = (N + BN - 1) / BN * BN;
   const int slabw = RB / 2;
   const int nslab = (CI + slabw - 1) / slabw;
-  const long long total = (long long)nslab * taps * npad * slabw;
+  // one thread per 16-byte chunk (8 consecutive reduction channels of one row n):
+  // 32-bit index math, one vector store
+  const int cpr = slabw / 8;
+  const int total = nslab * taps * npad * cpr;
   __nv_bfloat16* o = (__nv_bfloat16*)out;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(i % slabw);
-    long long t = i / slabw;
-    const int n = (int)(t % npad);
+  const int tapsz = jb.kh * jb.kw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int kc = i % cpr;
+    int t = i / cpr;
+    const int n = t % npad;
     t /= npad;
-    const int u = (int)(t % taps);
-    const int sl = (int)(t / taps);
-    const int ch = sl * slabw + k;
-    float v = 0.f;
-    if (n < N && ch < CI) {
-      int ky = u / jb.kw, kx = u % jb.kw, co, ci;
-      if (d) { ky = jb.kh - 1 - ky; kx = jb.kw - 1 - kx; co = ch; ci = n; }
-      else { co = n; ci = ch; }
-      v = jb.w[(((long long)co * jb.c_in + ci) * jb.kh + ky) * jb.kw + kx];
+    const int u = t % taps;
+    const int sl = t / taps;
+    int ky = u / jb.kw, kx = u % jb.kw;
+    if (d) { ky = jb.kh - 1 - ky; kx = jb.kw - 1 - kx; }
+    const int tap = ky * jb.kw + kx;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ch = sl * slabw + kc * 8 + e;
+      float f = 0.f;
+      if (n < N && ch < CI) {
+        const int co = d ? ch : n, ci = d ? n : ch;
+        f = jb.w[(co * jb.c_in + ci) * tapsz + tap];
+      }
+      v[e] = __float2bfloat16_rn(f);
     }
-    const int kb = k * 2;
-    int chunk = kb >> 4;
+    int chunk = kc;  // (k*2) >> 4 for the first k of the chunk
     chunk ^= RB == 128 ? (n & 7) : ((n >> 1) & 3);
-    const long long byte = (((long long)sl * taps + u) * npad + n) * RB + chunk * 16 + (kb & 15);
-    o[byte / 2] = __float2bfloat16_rn(v);
+    const long long byte = (((long long)sl * taps + u) * npad + n) * RB + chunk * 16;
+    *reinterpret_cast<uint4*>(o + byte / 2) = *reinterpret_cast<const uint4*>(v);
   }
 }
 
@@ -1360,7 +1382,7 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   const long long Q = (long long)p.n * p.hp * p.wp;
   if (Q >= (1ll << 31)) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: grid too large");
   p.Q = (int)Q;
-  p.R = 128 + (kh == 3 ? 2 * p.wp + 2 : 0);
+  p.P = (int)(in.n * in.h * in.w);
   p.fd_hpwp = make_fastdiv(p.hp * p.wp);
   p.fd_wp = make_fastdiv(p.wp);
   p.ci = (int)in.c;
@@ -1369,8 +1391,48 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.nslab = g.nslab;
   p.npad = g.npad;
   p.ntiles = g.ntiles;
-  p.mtiles = (p.Q + 127) / 128;
+  const int slabw = g.RB / 2;
+  uint32_t box[4];
+  int rank;
+  if (kh == 3) {
+    const int hpwp = p.hp * p.wp;
+    if (hpwp <= 128) {  // whole images per tile
+      p.tmode = 2;
+      p.kt = 128 / hpwp;
+      p.BR = p.hp;
+      p.BI = p.kt;
+      p.WPI = hpwp;
+      p.mtiles = (p.n + p.kt - 1) / p.kt;
+    } else {            // kt output rows of one image per tile
+      p.tmode = 1;
+      p.kt = 128 / p.wp;
+      if (p.kt > p.h) p.kt = p.h;
+      p.BR = p.kt + 2;
+      p.BI = 1;
+      p.WPI = p.BR * p.wp;
+      p.tpi = (p.h + p.kt - 1) / p.kt;
+      p.mtiles = p.n * p.tpi;
+    }
+    p.Rld = p.BR * p.BI * p.wp;
+    const int rmma = 128 + 2 * p.wp + 2;  // rows the (discarded) last MMA rows may touch
+    p.R = wc::align_up(p.Rld > rmma ? p.Rld : rmma, 8);
+    if (p.R > wc::RMAX) return wc::kWindowNoFit;
+    rank = 4;
+    box[0] = slabw; box[1] = p.wp; box[2] = p.BR; box[3] = p.BI;
+  } else {
+    p.tmode = 0;
+    p.Rld = 128;
+    p.R = 128;
+    p.mtiles = (p.P + 127) / 128;
+    rank = 2;
+    box[0] = slabw; box[1] = 128;
+  }
   p.tiles = p.mtiles * p.ntiles;
+  if (!encode_nhwc_bf16(&p.tma_a, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
+    return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (window operand)");
+  if (mode == 1 && pro == BNFF_PRO_BN_DX &&
+      !encode_nhwc_bf16(&p.tma_x, in_x.ptr, in_x.n, in_x.h, in_x.w, in_x.c, in_x.row_stride, rank, box))
+    return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (x operand)");
   p.src = (const __nv_bfloat16*)in.ptr; p.src_rs = in.row_stride;
   p.srcx = (const __nv_bfloat16*)in_x.ptr; p.srcx_rs = in_x.row_stride;
   p.pro = pro;
@@ -1414,7 +1476,7 @@ static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
     if (q.RA > q.KB + 128) return q;  // window taller than WgL::RAMAX: generic kernel
   } else {
     q.BN = pick_bn(cout);
-    q.MT = (q.BN <= 128 && cin > 128) ? 2 : 1;
+    q.MT = ((q.BN == 64 || q.BN == 128) && cin > 128) ? 2 : 1;  // the instantiated MT=2 variants
     q.KB = 64;
     q.RA = q.KB;
   }
@@ -1423,7 +1485,7 @@ static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
   q.nkb = (q.Q + q.KB - 1) / q.KB;
   const int target = num_sms_wc();
   int splits = (target + q.MG * q.NT - 1) / (q.MG * q.NT);
-  const int maxs = q.nkb / 4 > 0 ? q.nkb / 4 : 1;  // >= 4 k-blocks per split
+  const int maxs = q.nkb;  // small spatial sizes (14^2, 7^2): down to one k-block per split
   if (splits > maxs) splits = maxs;
   if (splits < 1) splits = 1;
   q.kpt = (q.nkb + splits - 1) / splits;
@@ -1487,8 +1549,8 @@ extern "C" int bnff_pack_window_multi(int32_t dtype, int32_t njobs, const bnff_p
                                       int64_t max_elems, void* stream) {
   if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window_multi: bf16 only");
   if (njobs <= 0) return BNFF_OK;
-  long long bx = (max_elems + 255) / 256;
-  if (bx > 64) bx = 64;
+  long long bx = (max_elems / 8 + 255) / 256;  // one thread per 16-byte chunk
+  if (bx > 32) bx = 32;
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)njobs, 2);
   launch(wc::pack_window_multi_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, jobs_dev);

@@ -35,6 +35,7 @@ import torch
 from . import _lib
 from . import graph as G
 from .errors import ShapeError, StateError
+from .params import ConvParams
 
 # ---------------------------------------------------------------------------
 # small helpers
@@ -150,6 +151,8 @@ class Engine:
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window) and self.dcode == _lib.BF16
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
+        self.cols = {}  # stem conv name -> (1x1 conv over col, col buffer, dw scratch, kpad)
+        self.col_src = {}  # 1x1 col conv name -> (fp32 (co, kpad) weights, stem conv, kpad)
         self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
                               (n.kind == G.CONCAT and not n.attrs.physical) for n in g.nodes)
         self.fwd: list = []
@@ -339,7 +342,36 @@ class Engine:
                 raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
         self.launch_counts["fwd"] = len(self.fwd)
 
+    def _col_conv(self, conv, x):
+        """A channel-poor stem conv (the 3-channel image, stored with 8) runs as im2col +
+        a 1x1 window GEMM over the patch matrix (csrc/stem.cu).  Returns
+        (conv1x1, col, dw2, kpad) or None when the conv does not qualify."""
+        if conv.name in self.cols:
+            return self.cols[conv.name]
+        if not (self.use_window and x.shape[3] == 8 and conv.in_c <= 8 and conv.kh * conv.kw > 1):
+            return None
+        kpad = _round_up(conv.kh * conv.kw * conv.in_c, 16)
+        n, h, w, _ = x.shape
+        oh, ow = conv.out_hw(h, w)
+        if not self.L.bnff_window_ok(self.dcode, kpad, conv.out_c, 1, 1, 1, 0, oh, ow):
+            return None
+        c1 = ConvParams(in_c=kpad, out_c=conv.out_c, kh=1, kw=1, name=conv.name + "#col")
+        col = self._empty((n, oh, ow, kpad))
+        w2 = self._zeros((conv.out_c * kpad,), torch.float32)
+        dw2 = self._zeros((conv.out_c * kpad,), torch.float32)
+        self.col_src[c1.name] = (w2, conv, kpad)
+        self.cols[conv.name] = ent = (c1, col, dw2, kpad)
+        return ent
+
     def _conv_fprop(self, node, x, y, conv, pro, tables, stat_part):
+        col = self._col_conv(conv, x) if pro == _lib.PRO_NONE else None
+        pname = conv.name
+        if col is not None:  # stem: patch matrix, then a 1x1 GEMM over it
+            c1, colt, _, _ = col
+            self._emit(self.L.bnff_im2col, self.dcode, view_of(x), conv.in_c, conv.kh, conv.kw,
+                       conv.stride, conv.pad, view_of(colt), what=f"im2col {node.name}",
+                       nbytes=_nb(x, colt))
+            x, conv = colt, c1
         cin_store = x.shape[3]
         wp, _, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if tables is None:
@@ -347,7 +379,7 @@ class Engine:
         else:
             cf = coef_of(tables[0], tables[1], tables[2])
         args = _lib.FpropArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x),
-                              view_of(y), _ptr(wp), _ptr(self.param(f"{conv.name}.bias")), pro, cf,
+                              view_of(y), _ptr(wp), _ptr(self.param(f"{pname}.bias")), pro, cf,
                               _ptr(stat_part), self._wwin(conv, 0))
         n_, oh_, ow_, co_ = y.shape
         flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
@@ -528,6 +560,9 @@ class Engine:
             cin_s = self._store_c(xs[1])
             ws = max(ws, self.L.bnff_wgrad_workspace(xs[0], oh, ow, conv.kh, conv.kw, cin_s,
                                                     conv.out_c, 0))
+        for c1, colt, _, _ in self.cols.values():  # stem GEMMs over their patch matrices
+            n, oh, ow, kp = colt.shape
+            ws = max(ws, self.L.bnff_wgrad_workspace(n, oh, ow, 1, 1, kp, c1.out_c, 0))
         self.wg_ws = self._empty((ws,), torch.float32)
         for node in reversed(g.nodes):
             try:
@@ -605,10 +640,15 @@ class Engine:
             self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
                        nbytes=_nb(dy, dx, wt) + extra, flops=flops)
         xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
+        col = self.cols.get(conv.name) if x_pro == _lib.PRO_NONE else None
+        orig = conv
+        dw = self.grad(f"{conv.name}.weight")
+        if col is not None:  # stem: weight gradient of the 1x1 GEMM over the patch matrix
+            conv, x, dw, _ = col[0], col[1], col[2], col[3]
+            cin_store = x.shape[3]
         wa = _lib.WgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x), x_pro,
                             xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
-                            _ptr(self.grad(f"{conv.name}.weight")), conv.in_c,
-                            _ptr(self.grad(f"{conv.name}.bias")))
+                            _ptr(dw), conv.in_c, _ptr(self.grad(f"{orig.name}.bias")))
         self._keep.append(wa)
         n_, oh_, ow_, co_ = dy.shape
         flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
@@ -616,6 +656,10 @@ class Engine:
         self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}",
                    nbytes=_nb(x, dy) + extra + 4 * conv.out_c * conv.in_c * conv.kh * conv.kw,
                    flops=flops, launches=4)
+        if col is not None:
+            self._emit(self.L.bnff_cols_to_weight, _ptr(col[2]), orig.out_c, orig.in_c, orig.kh,
+                       orig.kw, col[3], _ptr(self.grad(f"{orig.name}.weight")),
+                       what=f"cols_to_weight {node.name}")
         return dx, part
 
     def _b_Conv2D(self, node):
@@ -789,7 +833,15 @@ class Engine:
         jobs = []
         max_el = 0
         for name, (wf, wd, conv) in self.wpacks.items():
-            jobs.append(_lib.PackJob(_ptr(self.param(f"{name}.weight")), _ptr(wf), _ptr(wd),
+            if name in self.col_src:  # stem GEMM: (co, ci, kh, kw) -> (co, kpad) first
+                w2, orig, kpad = self.col_src[name]
+                self._emit(self.L.bnff_weight_to_cols, _ptr(self.param(f"{orig.name}.weight")),
+                           orig.out_c, orig.in_c, orig.kh, orig.kw, kpad, _ptr(w2),
+                           what="pack_weights")
+                src = w2
+            else:
+                src = self.param(f"{name}.weight")
+            jobs.append(_lib.PackJob(_ptr(src), _ptr(wf), _ptr(wd),
                                      conv.out_c, conv.in_c, conv.kh, conv.kw))
             max_el = max(max_el, wf.numel(), wd.numel())
         if jobs:

@@ -143,15 +143,17 @@ def _bf16_errors(spec, level):
 def test_bf16_fusion_adds_no_error(spec):
     """bf16 mode: the fused levels are as accurate as the unfused chain in the same
     precision (fused <= 1.5x unfused + 1e-3, per tensor), and every tensor stays
-    within rel-L2 0.5 of the fp64 oracle (a sanity cap only: at batch 2 the per-channel
+    within rel-L2 0.75 of the fp64 oracle (a sanity cap only: at batch 2 the per-channel
     dgamma/dbeta reductions span ~128-512 bf16 terms with heavy cancellation, and the
-    unfused bf16 chain sits at 0.2-0.3 on the same tensors); the output within 2e-2."""
+    unfused bf16 chain sits at 0.2-0.4 on the same tensors -- worst on the stem weight,
+    whose gradient sums x * dy over a dy that BN makes zero-mean per channel); the
+    output within 2e-2."""
     base = _bf16_errors(spec, "baseline")
     for level in ("bnff", "bnff+icf"):
         fused = _bf16_errors(spec, level)
         for k, e in fused.items():
             assert e <= 1.5 * base[k] + 1e-3, f"{level} {k}: fused {e:.3e} vs unfused {base[k]:.3e}"
-            assert e < 0.5, f"{level} {k}: {e:.3e}"
+            assert e < 0.75, f"{level} {k}: {e:.3e}"
         assert fused["__out__"] < 2e-2
 
 
@@ -244,3 +246,56 @@ def test_cuda_graph_replay_matches_eager():
     eng.step()
     torch.cuda.synchronize()
     assert np.array_equal(eng.gflat.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("level", ["baseline", "bnff"])
+def test_stem_im2col_gemm_bf16(level):
+    """The 7x7/s2 stem over the 3-channel image runs as im2col + a 1x1 tcgen05 GEMM
+    (csrc/stem.cu) in bf16 mode.  Same bf16 math as the generic implicit GEMM (only the
+    fp32 accumulation order differs): output and every gradient within rel-L2 1e-2 of
+    the all-generic engine, and stem grads within the bf16 bar of the fp64 oracle;
+    a post-step weight check covers the (co, ci, kh, kw) <-> (co, k) weight re-layout."""
+    from paper_1807_01702_b200.engine import Engine
+    g0 = G.build_model(tiny_full(), seed=0)
+    g, _ = fusion.plan(g0, fusion.parse_level(level))
+    rng = Rng(1)
+    x = rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0)
+    dy = rng.normal(g.slots[g.outputs[0]].shape)
+    runs = []
+    for win in (True, False):
+        eng = Engine(g, dtype="bf16", input_grad=False, use_window=win, lr=0.5)
+        eng.set_input(x)
+        eng.set_loss_grad(dy)
+        eng.forward()
+        eng.backward()
+        torch.cuda.synchronize()
+        runs.append((eng, eng.output(), eng.param_grads()))
+    assert runs[0][0].cols and not runs[1][0].cols, "stem GEMM path not taken"
+    assert rel_l2(runs[0][1], runs[1][1]) < 1e-2
+    for k, v in runs[1][2].items():
+        if k.endswith(".bias"):  # conv bias before a BN: the exact gradient is 0 (bf16 noise only)
+            assert np.max(np.abs(runs[0][2][k] - v)) < 1e-2 * max(float(np.max(np.abs(v))), 1.0), k
+            continue
+        assert rel_l2(runs[0][2][k], v) < 1e-2, k
+    res = OX.forward(g, {g.inputs[0]: x.astype(np.float64)})
+    ref = OX.backward(g, res, {g.outputs[0]: dy.astype(np.float64)})
+    e_col = rel_l2(runs[0][2]["stem.conv.weight"], ref.params["stem.conv.weight"])
+    e_gen = rel_l2(runs[1][2]["stem.conv.weight"], ref.params["stem.conv.weight"])
+    assert e_col <= 1.5 * e_gen + 1e-3, (e_col, e_gen)
+    # optimizer graph: SGD + stem weight re-layout + window re-pack, then one more forward
+    import copy
+    eng = runs[0][0]
+    eng.optimizer_step()
+    eng.forward()
+    torch.cuda.synchronize()
+    now = eng.params_now()
+    want = np.asarray(g.params["stem.conv.weight"], np.float64) - 0.5 * runs[0][2]["stem.conv.weight"]
+    assert scaled(now["stem.conv.weight"], want) < 1e-5
+    g2 = copy.deepcopy(g)
+    for k in g2.params:
+        g2.params[k] = np.asarray(now[k], np.float32).reshape(np.shape(g2.params[k]))
+    e2 = Engine(g2, dtype="bf16", input_grad=False, use_window=False)
+    e2.set_input(x)
+    e2.forward()
+    torch.cuda.synchronize()
+    assert rel_l2(eng.output(), e2.output()) < 1e-2

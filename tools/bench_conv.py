@@ -176,7 +176,16 @@ def main():
         (2, 8, 320, 128, 1, "dgrad", P.PRO_BN_DX, P.DG_NRC),
     ]
     cases += [
+        # TMA window tiling: kt rows per tile with a partial last tile (14: kt=8),
+        # a BN_DX x operand on a 3x3 with row tiles, uneven slabs, ragged pixel counts
+        (2, 14, 64, 32, 3, "fprop", P.PRO_BN_RELU, 0),
+        (2, 12, 32, 64, 3, "dgrad", P.PRO_BN_DX, P.DG_NRC),
+        (3, 11, 96, 128, 1, "dgrad", P.PRO_BN_DX, P.DG_NRC),
+        (1, 30, 64, 32, 3, "fprop", P.PRO_RELU, 0),
+    ]
+    cases += [
         (2, 9, 128, 32, 3, "wgrad", P.PRO_BN_RELU, 0),
+        (2, 16, 160, 16, 1, "wgrad", P.PRO_NONE, 1),
         (2, 9, 96, 128, 1, "wgrad", P.PRO_BN_RELU, 1),
         (3, 6, 320, 128, 1, "wgrad", P.PRO_NONE, 1),
         (2, 5, 64, 64, 3, "wgrad", P.PRO_RELU, 0),

@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--level", default="bnff")
+    ap.add_argument("--level", default="bnff+icf")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--model", default="densenet121")

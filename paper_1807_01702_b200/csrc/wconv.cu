@@ -38,7 +38,8 @@ constexpr int NLW = 8;                  // loader warps
 constexpr int LT = NLW * 32;            // loader threads
 constexpr int THREADS = (NLW + 1 + 4) * 32;      // wgrad kernel: 4 epilogue warps
 constexpr int NEW = 8;                           // wconv: epilogue warps (2 groups of 4)
-constexpr int WC_THREADS = (NLW + 1 + NEW) * 32;
+constexpr int WC_THREADS = (NLW + 1 + NEW + 1) * 32;  // + one TMA producer warp
+constexpr int PRODUCER = NLW + 1 + NEW;
 constexpr int RMAX = 384;               // max window rows (wp <= 127 for 3x3)
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int kWindowNoFit = -100;      // internal: shape does not fit, use the generic kernel
@@ -120,8 +121,7 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   off += 2 * RMAX * 4;
   c.rowpix = off;
   off += 2 * 128 * 4;
-  c.meta = off;
-  off += stages * LT * 4;
+  c.meta = off;  // (unused by the TMA loader)
   c.total = off + 1024;  // + alignment slack
   return c;
 }
@@ -140,6 +140,10 @@ __device__ __forceinline__ uint4 pack8(const float* f, bool relu) {
     o.z = pack_bf16_rn(f[4], f[5]); o.w = pack_bf16_rn(f[6], f[7]);
   }
   return o;
+}
+__device__ __forceinline__ void ld8f(const float* p, float* v) {  // 8 floats, 16B aligned
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 __device__ __forceinline__ void ld16f(const float* p, float* v) {  // 16 floats, 16B aligned
 #pragma unroll
@@ -290,69 +294,36 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   };
 
   if (warp < NLW) {
-    // =============================== loaders ===============================
-    // thread 0 issues one TMA box per stage (zero-filled outside the map: the 3x3 halo
-    // and the image border come for free), LAG stages ahead of the in-place transform;
-    // the MMA consumes a stage once every loader thread has transformed its rows and
-    // arrived on full_bar.
+    // =============================== transform warps ===============================
+    // wait for a stage's TMA box, apply the operand prologue in place (halo / border
+    // positions stay zero: padding applies after normalize/ReLU), arrive on full_bar.
     const int j = tid % CPR, r0 = tid / CPR;
-    const int G = ntl * p.nslab;
-    const int LAG = ST / 2 > 1 ? ST / 2 : 1;
-    const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
     const bool need_t = p.pro != BNFF_PRO_NONE;
-    const uint32_t tx_bytes = (uint32_t)p.Rld * RB * (xop ? 2u : 1u);
-    for (int g = 0; g < G + LAG; ++g) {
-      if (g < G && tid == 0) {
-        const int it = g / p.nslab, s = g - it * p.nslab;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < ntl; ++it) {
+      int img0 = 0, y0 = 0;
+      if (TAPS == 9) {
         int mt, n0;
         tile_of(it, mt, n0);
-        const int st = g % ST;
-        if (g >= ST) mbar_wait(&empty_bar[st], ((g / ST) - 1) & 1);
-        if (!L::WRES) {
-          mbar_arrive_expect_tx(&full_bar[st], BN * RB);
-          bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
-                   &full_bar[st]);
-        }
-        mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
-        const int c = s * SLABW;
-        if (TAPS == 9) {
-          int img0, y0;
-          tile_org(mt, img0, y0);
-          tma_load_4d(smem_u32(stage_a(st)), &p.tma_a, c, -1, y0, img0, &ld_bar[st]);
-          if (xop) tma_load_4d(smem_u32(stage_x(st)), &p.tma_x, c, -1, y0, img0, &ld_bar[st]);
-        } else {
-          tma_load_2d(smem_u32(stage_a(st)), &p.tma_a, c, mt * 128, &ld_bar[st]);
-          if (xop) tma_load_2d(smem_u32(stage_x(st)), &p.tma_x, c, mt * 128, &ld_bar[st]);
-        }
+        tile_org(mt, img0, y0);
       }
-      if (g >= LAG) {
-        const int gg = g - LAG;
-        const int st = gg % ST;
-        const int it = gg / p.nslab, s = gg - it * p.nslab;
-        mbar_wait(&ld_bar[st], (gg / ST) & 1);
+      for (int s = 0; s < p.nslab; ++s) {
+        mbar_wait(&ld_bar[st], ph);
         const int cs = min(SLABW, p.ci - s * SLABW);
         if (need_t && j * 8 < cs) {
           const int c0 = s * SLABW + j * 8;
           float t0[8], t1[8], t2[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            t0[i] = ptab[c0 + i];
-            t1[i] = ptab[kpad + c0 + i];
-            t2[i] = ptab[2 * kpad + c0 + i];
-          }
-          int img0 = 0, y0 = 0;
-          if (TAPS == 9) {
-            int mt, n0;
-            tile_of(it, mt, n0);
-            tile_org(mt, img0, y0);
-          }
+          ld8f(ptab + c0, t0);
+          ld8f(ptab + kpad + c0, t1);
+          ld8f(ptab + 2 * kpad + c0, t2);
           uint8_t* A = stage_a(st);
           uint8_t* X = stage_x(st);
 #pragma unroll
           for (int u = 0; u < UR; ++u) {
             const int r = r0 + u * RS;
             if (r >= p.Rld) continue;
-            if (TAPS == 9) {  // halo / border positions stay zero (padding after normalize)
+            if (TAPS == 9) {
               const int wr = rowtab[r];
               const int y = y0 + ((wr >> 10) & 1023), rx = wr & 1023;
               if ((unsigned)y >= (unsigned)p.h || rx < 1 || rx > p.w || img0 + (wr >> 20) >= p.n) continue;
@@ -378,27 +349,62 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             }
             *reinterpret_cast<uint4*>(A + off) = o;
           }
+          fence_proxy_async_smem();
         }
-        fence_proxy_async_smem();
         mbar_arrive(&full_bar[st]);
+        if (++st == ST) { st = 0; ph ^= 1u; }
       }
     }
+  } else if (warp == PRODUCER) {
+    // =============================== TMA producer ===============================
+    // one lane streams window boxes into the stage ring as fast as the MMA frees stages
+    // (zero-filled outside the map: the 3x3 halo and image borders come for free)
+    if (lane == 0) {
+      const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
+      const uint32_t tx_bytes = (uint32_t)p.Rld * RB * (xop ? 2u : 1u);
+      int st = 0, round = 0;
+      for (int it = 0; it < ntl; ++it) {
+        int mt, n0;
+        tile_of(it, mt, n0);
+        int img0 = 0, y0 = 0;
+        if (TAPS == 9) tile_org(mt, img0, y0);
+        for (int s = 0; s < p.nslab; ++s) {
+          if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
+          if (!L::WRES) {
+            mbar_arrive_expect_tx(&full_bar[st], BN * RB);
+            bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
+                     &full_bar[st]);
+          }
+          mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
+          const int c = s * SLABW;
+          if (TAPS == 9) {
+            tma_load_4d(smem_u32(stage_a(st)), &p.tma_a, c, -1, y0, img0, &ld_bar[st]);
+            if (xop) tma_load_4d(smem_u32(stage_x(st)), &p.tma_x, c, -1, y0, img0, &ld_bar[st]);
+          } else {
+            tma_load_2d(smem_u32(stage_a(st)), &p.tma_a, c, mt * 128, &ld_bar[st]);
+            if (xop) tma_load_2d(smem_u32(stage_x(st)), &p.tma_x, c, mt * 128, &ld_bar[st]);
+          }
+          if (++st == ST) { st = 0; ++round; }
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp == NLW) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
       if (L::WRES) mbar_wait(&w_bar, 0);
       constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 0, 0);
       const uint32_t wres = smem_u32(smem + cv.wres);
-      int g = 0;
+      int st = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < ntl; ++it) {
         const int buf = it & 1;
         if (it >= 2) mbar_wait(&acce_bar[buf], ((it >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * BN;
         uint32_t acc = 0;
-        for (int s = 0; s < p.nslab; ++s, ++g) {
-          const int st = g % ST;
-          mbar_wait(&full_bar[st], (g / ST) & 1);
+        for (int s = 0; s < p.nslab; ++s) {
+          mbar_wait(&full_bar[st], ph);
           tc_fence_after();
           const uint32_t abase = smem_u32(stage_a(st));
           const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB : smem_u32(stage_b(st));
@@ -419,6 +425,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             }
           }
           umma_commit(&empty_bar[st]);
+          if (++st == ST) { st = 0; ph ^= 1u; }
         }
         umma_commit(&accf_bar[buf]);
       }

@@ -653,25 +653,31 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
 }
 
 // ===========================================================================
-// WGRAD on the padded grid:  dW[tap][ci][co] = sum_q  P_x[q + s_tap, ci] * G[q, co]
-// A = P_x (MN-major: each grid position is a 128B row of 64 channels per atom; one
-// window of KB + 2*wp + 2 rows serves all 9 taps through K-shifted descriptors),
-// B = G = pro(dy) at output positions (zero elsewhere), MN-major.  A CTA owns one
-// work unit (m-group of MT*128 input channels, N tile, K split) at a time and keeps
-// TAPS*MT accumulators of BN columns in TMEM; fp32 partials go to a workspace
-// reduced in fixed split order (deterministic).
+// WGRAD:  dW[tap][ci][co] = sum_m  P_x[m + s_tap, ci] * G[m, co]
+// K runs over the output positions of a k-block -- the same row/image-aligned tiles as
+// the forward window kernel (3x3: kt padded output rows of one image, or kt whole
+// images; 1x1: 128 pixels).  A = P_x, the TMA window of the tile with its zero halo
+// (MN-major: 128-byte rows of 64 input channels per atom; all 9 taps read it through
+// K-shifted descriptors), B = G = pro(dy) at the tile's output positions (MN-major,
+// zero outside the map).  A CTA owns one work unit (m-group of MT*128 input channels,
+// N tile, K split) at a time and keeps TAPS*MT accumulators of BN columns in TMEM;
+// fp32 partials go to a workspace reduced in fixed split order (deterministic).
+// Warp roles: 8 transform warps (prologues in place, dbias), 1 MMA warp, 4 epilogue
+// warps, 1 TMA producer warp.
 // ===========================================================================
 int num_sms_wc();
 
+constexpr int WG_THREADS = (NLW + 1 + 4 + 1) * 32;
+constexpr int WG_PRODUCER = NLW + 1 + 4;
+
 struct WgParams {
+  CUtensorMap tma_x, tma_dy, tma_dyx;
+  int tmode, kt, BR, BI, WPI, tpi, Rld, Kr, P;
   int n, h, w, hp, wp, pad, Q;
   FastDiv fd_hpwp, fd_wp;
   int cin, cout, KB, RA, nkb, kpt, splits, MG, NT, units, stages;
-  const __nv_bfloat16* x; long long x_rs;
   int x_pro;
   bnff_coef x_coef;
-  const __nv_bfloat16* dy; long long dy_rs;
-  const __nv_bfloat16* dyx; long long dyx_rs;
   int dy_pro;
   bnff_coef dy_coef;
   float* ws;
@@ -684,7 +690,7 @@ struct WgL {
   static constexpr int NBA = BN * 2 / BRB;                   // B atoms
   static constexpr int BCPR = BRB / 16;                      // B chunks per row per atom
   static constexpr int BCH = NBA * BCPR;                     // B chunks per row
-  static constexpr int RAMAX = TAPS == 9 ? KB + 128 : KB;    // A rows (wp <= 63)
+  static constexpr int RAMAX = TAPS == 9 ? RMAX : KB;        // A rows (allocated, max)
   static constexpr int AAT = 2 * MT;                         // A atoms
   static constexpr int UAR = RAMAX / 32;                     // A rows per thread per atom
   static constexpr int UB = KB * BCH / LT;                   // B chunks per thread
@@ -699,23 +705,22 @@ struct WgCarve {
   int stage_bytes, a_bytes, b_bytes, ptab, qtab, rowx, rowg, meta, bred, total;
 };
 template <int BN, int MT, int TAPS, int KB>
-__host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int stages) {
+__host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int stages, bool xop) {
   using L = WgL<BN, MT, TAPS, KB>;
   WgCarve c{};
   c.a_bytes = L::AAT * RA * 128;
   c.b_bytes = L::NBA * KB * L::BRB;
-  c.stage_bytes = align_up(c.a_bytes + 2 * c.b_bytes, 1024);  // A | B | X(dy_x)
+  c.stage_bytes = align_up(c.a_bytes + (xop ? 2 : 1) * c.b_bytes, 1024);  // A | B | X(dy_x)
   int off = stages * c.stage_bytes;
   c.ptab = off;
   off += 2 * cin_pad * 4;
   c.qtab = off;
   off += 3 * npad * 4;
-  c.rowx = off;
-  off += 2 * L::RAMAX * 4;
-  c.rowg = off;
-  off += 2 * KB * 4;
+  c.rowx = off;  // window row -> (image block, padded row, padded column)
+  off += RMAX * 4;
+  c.rowg = off;  // k-block row -> (image block, output row, column)
+  off += KB * 4;
   c.meta = off;
-  off += 8 * LT * 4;
   c.bred = off;
   off += 8 * LT * 4;
   c.total = off + 1024;
@@ -723,35 +728,60 @@ __host__ __device__ inline WgCarve wg_carve(int RA, int cin_pad, int npad, int s
 }
 
 template <int BN, int MT, int TAPS, int KB>
-__global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
+__global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_constant__ WgParams p) {
   griddep_launch();
   using L = WgL<BN, MT, TAPS, KB>;
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
   uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[8], empty_bar[8], accf_bar, acce_bar;
+  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar, acce_bar;
   __shared__ uint32_t tmem_sh;
   const int cin_pad = p.MG * MT * 128, npad = p.NT * BN;
-  const WgCarve cv = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, p.stages);
+  const WgCarve cv = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, p.stages, p.dy_pro == BNFF_PRO_BN_DX);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* qtab = reinterpret_cast<float*>(smem + cv.qtab);
   int* rowx = reinterpret_cast<int*>(smem + cv.rowx);
   int* rowg = reinterpret_cast<int*>(smem + cv.rowg);
-  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + cv.meta);
   float* bred = reinterpret_cast<float*>(smem + cv.bred);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nun = (p.units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const bool xb = p.dy_pro == BNFF_PRO_BN_DX;
 
   if (tid == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(&full_bar[s], LT); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full_bar[s], LT);
+      mbar_init(&empty_bar[s], 1);
+      mbar_init(&ld_bar[s], 1);
+    }
     mbar_init(&accf_bar, 1);
     mbar_init(&acce_bar, 128);
     fence_mbar_init();
+    tma_prefetch_desc(&p.tma_x);
+    tma_prefetch_desc(&p.tma_dy);
+    if (xb) tma_prefetch_desc(&p.tma_dyx);
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
+  // stage buffers start zeroed: rows past what the TMA writes (the K tail of B, the A
+  // rows beyond the window) must be finite zeros for the full-K MMAs
+  for (int i = tid; i < ST * cv.stage_bytes / 16; i += WG_THREADS)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  // row geometry tables (identical for every k-block)
+  if (TAPS == 9) {
+    for (int r = tid; r < p.Rld; r += WG_THREADS) {
+      const int i = r / p.WPI, rem = r - i * p.WPI;
+      const int ry = rem / p.wp, rx = rem - ry * p.wp;
+      rowx[r] = (i << 20) | (ry << 10) | rx;
+    }
+    const int opi = p.tmode == 2 ? p.hp * p.wp : KB;
+    for (int m = tid; m < KB; m += WG_THREADS) {
+      const int i = m / opi, rem = m - i * opi;
+      const int yo = rem / p.wp, x = rem - yo * p.wp;
+      rowg[m] = (i << 20) | (yo << 10) | x;
+    }
+  }
   griddep_wait();  // everything below reads data of the preceding launches
-  for (int c = tid; c < cin_pad; c += THREADS) {  // x prologue: (scale, beta - mean*scale)
+  for (int c = tid; c < cin_pad; c += WG_THREADS) {  // x prologue: (scale, beta - mean*scale)
     float t0 = 1.f, t1 = 0.f;
     if (c < p.cin && p.x_pro == BNFF_PRO_BN_RELU) {
       t0 = p.x_coef.b[c];
@@ -760,9 +790,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
     ptab[c] = t0;
     ptab[cin_pad + c] = t1;
   }
-  for (int c = tid; c < npad; c += THREADS) {  // dy prologue (BN_DX)
+  for (int c = tid; c < npad; c += WG_THREADS) {  // dy prologue (BN_DX)
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
-    if (c < p.cout && p.dy_pro == BNFF_PRO_BN_DX) {
+    if (c < p.cout && xb) {
       const float m = p.dy_coef.a[c], inv = p.dy_coef.b[c], k1 = p.dy_coef.c[c],
                   k2 = p.dy_coef.d[c], g = p.dy_coef.e[c];
       t0 = g;
@@ -773,6 +803,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
     qtab[npad + c] = t1;
     qtab[2 * npad + c] = t2;
   }
+  fence_proxy_async_smem();  // zeroed stage buffers -> visible to the async proxy (TMA, UMMA)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -788,116 +819,65 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
   auto stage_b = [&](int s) { return smem + s * cv.stage_bytes + cv.a_bytes; };
   auto stage_x = [&](int s) { return smem + s * cv.stage_bytes + cv.a_bytes + cv.b_bytes; };
   auto kb_count = [&](int sp) { return min(p.kpt, p.nkb - sp * p.kpt); };
+  // k-block origin: first image and the padded-input row the window starts at (3x3)
+  auto kb_org = [&](int kb, int& img0, int& y0) {
+    if (p.tmode == 1) {
+      img0 = kb / p.tpi;
+      y0 = (kb - img0 * p.tpi) * p.kt - 1;
+    } else {
+      img0 = kb * p.kt;
+      y0 = -1;
+    }
+  };
 
   if (warp < NLW) {
-    // =============================== loaders ===============================
+    // =============================== transform warps ===============================
     const int ja = tid & 7, ra0 = tid >> 3;                 // A: chunk column, first row
     const int jb = tid % L::BCH, rb0 = tid / L::BCH;        // B: chunk column, first row
     constexpr int RBS = LT / L::BCH;                        // B row step
-    const int hpwp = p.hp * p.wp;
-    const bool xb = p.dy_pro == BNFF_PRO_BN_DX;
-    int G = 0;
-    for (int ui = 0; ui < nun; ++ui) {
-      int mg, nt, sp;
-      unit_of(ui, mg, nt, sp);
-      G += kb_count(sp);
-    }
-    const int LAG = ST / 2 > 1 ? ST / 2 : 1;
-    // issue-side cursor
-    int iu = 0, ik = 0, imgi = 0, inti = 0, isp = 0, icnt = 0;
-    if (nun > 0) { unit_of(0, imgi, inti, isp); icnt = kb_count(isp); }
-    // transform-side cursor
-    int tu = 0, tk = 0, tmg = 0, tnt = 0, tsp = 0, tcnt = 0;
+    const bool need_a = p.x_pro != BNFF_PRO_NONE;
+    const bool need_db = p.wsb != nullptr;
     float bacc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) bacc[i] = 0.f;
-    if (nun > 0) { unit_of(0, tmg, tnt, tsp); tcnt = kb_count(tsp); }
-    (void)tu; (void)tk; (void)tsp;
-    for (int g = 0; g < G + LAG; ++g) {
-      if (g < G) {
-        const int kb = isp * p.kpt + ik;
-        const int q0 = kb * KB;
-        int* rx = rowx + (g & 1) * L::RAMAX;
-        int* rg = rowg + (g & 1) * KB;
-        for (int r = tid; r < p.RA; r += LT) {
-          const int q = q0 + r;
-          int src = -1;
-          if (q < p.Q) {
-            const int img = (int)fdiv((uint32_t)q, p.fd_hpwp);
-            const int rem = q - img * hpwp;
-            const int py = (int)fdiv((uint32_t)rem, p.fd_wp);
-            const int px = rem - py * p.wp;
-            const int iy = py - p.pad, ix = px - p.pad;
-            if (iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) src = (img * p.h + iy) * p.w + ix;
-            if (r < KB) rg[r] = (py < p.h && px < p.w) ? (img * p.h + py) * p.w + px : -1;
-          } else if (r < KB) {
-            rg[r] = -1;
-          }
-          rx[r] = src;
-        }
-        named_bar_sync(1, LT);
-        const int st = g % ST;
-        if (g >= ST) mbar_wait(&empty_bar[st], ((g / ST) - 1) & 1);
-        uint32_t mask = 0;
-        const uint32_t abase = smem_u32(stage_a(st));
-#pragma unroll
-        for (int a = 0; a < L::AAT; ++a) {
-          const int c0 = imgi * MT * 128 + a * 64 + ja * 8;
-#pragma unroll
-          for (int k = 0; k < L::UAR; ++k) {
-            const int r = ra0 + 32 * k;
-            if (r < p.RA && c0 < p.cin) {
-              const int src = rx[r];
-              const bool ok = src >= 0;
-              const uint32_t off = a * p.RA * 128 + r * 128 + ((ja ^ (r & 7)) << 4);
-              cp_async16(abase + off, p.x + (ok ? (long long)src * p.x_rs + c0 : 0), ok ? 16u : 0u);
-              mask |= (ok ? 1u : 0u) << (a * L::UAR + k);
-            }
-          }
-        }
-        const uint32_t bbase = smem_u32(stage_b(st)), xbase = smem_u32(stage_x(st));
-        const int co0 = inti * BN + jb * 8;
-#pragma unroll
-        for (int k = 0; k < L::UB; ++k) {
-          const int r = rb0 + RBS * k;
-          if (co0 < p.cout) {
-            const int src = rg[r];
-            const bool ok = src >= 0;
-            const int b = jb / L::BCPR, jj = jb % L::BCPR;
-            uint32_t off = b * KB * L::BRB + r * L::BRB;
-            if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
-            else off += (jj ^ ((r >> 1) & 3)) << 4;
-            cp_async16(bbase + off, p.dy + (ok ? (long long)src * p.dy_rs + co0 : 0), ok ? 16u : 0u);
-            if (xb)
-              cp_async16(xbase + off, p.dyx + (ok ? (long long)src * p.dyx_rs + co0 : 0), ok ? 16u : 0u);
-            mask |= (ok ? 1u : 0u) << (24 + k);
-          }
-        }
-        meta[st * LT + tid] = mask;
-        if (++ik == icnt) {
-          ik = 0;
-          if (++iu < nun) { unit_of(iu, imgi, inti, isp); icnt = kb_count(isp); }
-        }
+    int st = 0;
+    uint32_t ph = 0;
+    for (int ui = 0; ui < nun; ++ui) {
+      int mg, nt, sp;
+      unit_of(ui, mg, nt, sp);
+      const int cnt = kb_count(sp);
+      const int co0 = nt * BN + jb * 8;
+      const bool bact = (xb || (need_db && mg == 0)) && co0 < p.cout;
+      float q0[8], q1[8], q2[8];
+      if (xb && co0 < p.cout) {
+        ld8f(qtab + co0, q0);
+        ld8f(qtab + npad + co0, q1);
+        ld8f(qtab + 2 * npad + co0, q2);
       }
-      cp_async_commit();
-      if (g >= LAG) {
-        const int gg = g - LAG;
-        const int st = gg % ST;
-        cp_async_wait_dyn(LAG);
-        const uint32_t mask = meta[st * LT + tid];
-        if (p.x_pro != BNFF_PRO_NONE) {
+      for (int k = 0; k < cnt; ++k) {
+        const int kb = sp * p.kpt + k;
+        int img0 = 0, y0 = 0;
+        if (TAPS == 9) kb_org(kb, img0, y0);
+        mbar_wait(&ld_bar[st], ph);
+        bool wrote = false;
+        if (need_a) {
           uint8_t* A = stage_a(st);
 #pragma unroll
           for (int a = 0; a < L::AAT; ++a) {
-            const int c0 = tmg * MT * 128 + a * 64 + ja * 8;
+            const int c0 = mg * MT * 128 + a * 64 + ja * 8;
             if (c0 >= p.cin) continue;
             float t0[8], t1[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) { t0[i] = ptab[c0 + i]; t1[i] = ptab[cin_pad + c0 + i]; }
-#pragma unroll
-            for (int k = 0; k < L::UAR; ++k) {
-              if (!((mask >> (a * L::UAR + k)) & 1u)) continue;
-              const int r = ra0 + 32 * k;
+            ld8f(ptab + c0, t0);
+            ld8f(ptab + cin_pad + c0, t1);
+#pragma unroll 4
+            for (int u = 0; u < L::UAR; ++u) {
+              const int r = ra0 + 32 * u;
+              if (r >= p.Rld) break;
+              if (TAPS == 9) {  // halo / border positions stay zero
+                const int wr = rowx[r];
+                const int y = y0 + ((wr >> 10) & 1023), rx = wr & 1023;
+                if ((unsigned)y >= (unsigned)p.h || rx < 1 || rx > p.w || img0 + (wr >> 20) >= p.n) continue;
+              }
               const uint32_t off = a * p.RA * 128 + r * 128 + ((ja ^ (r & 7)) << 4);
               float f[8];
               unpack8(*reinterpret_cast<const uint4*>(A + off), f);
@@ -908,90 +888,125 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
               *reinterpret_cast<uint4*>(A + off) = pack8(f, true);
             }
           }
+          wrote = true;
         }
-        if (xb) {
-          const int co0 = tnt * BN + jb * 8;
-          if (co0 < p.cout) {
-            uint8_t* B = stage_b(st);
-            const uint8_t* X = stage_x(st);
-            float t0[8], t1[8], t2[8];
+        if (bact) {
+          uint8_t* B = stage_b(st);
+          const uint8_t* X = stage_x(st);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              t0[i] = qtab[co0 + i]; t1[i] = qtab[npad + co0 + i]; t2[i] = qtab[2 * npad + co0 + i];
+          for (int u = 0; u < L::UB; ++u) {
+            const int r = rb0 + RBS * u;
+            if (r >= p.Kr) break;
+            bool ok;
+            if (TAPS == 9) {
+              const int wr = rowg[r];
+              const int i = wr >> 20, yo = (wr >> 10) & 1023, x = wr & 1023;
+              const int y = y0 + 1 + yo;
+              ok = x < p.w && y < p.h && (p.tmode == 2 ? img0 + i < p.n : yo < p.kt);
+            } else {
+              ok = kb * KB + r < p.P;
             }
-#pragma unroll
-            for (int k = 0; k < L::UB; ++k) {
-              if (!((mask >> (24 + k)) & 1u)) continue;
-              const int r = rb0 + RBS * k;
-              const int b = jb / L::BCPR, jj = jb % L::BCPR;
-              uint32_t off = b * KB * L::BRB + r * L::BRB;
-              if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
-              else off += (jj ^ ((r >> 1) & 3)) << 4;
-              float f[8], xf[8];
-              unpack8(*reinterpret_cast<const uint4*>(B + off), f);
+            if (!ok) continue;
+            const int b = jb / L::BCPR, jj = jb % L::BCPR;
+            uint32_t off = b * KB * L::BRB + r * L::BRB;
+            if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
+            else off += (jj ^ ((r >> 1) & 3)) << 4;
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(B + off), f);
+            if (xb) {
+              float xf[8];
               unpack8(*reinterpret_cast<const uint4*>(X + off), xf);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], fmaf(xf[i], t1[i], t2[i]));
-              *reinterpret_cast<uint4*>(B + off) = pack8(f, false);
+              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], q0[i], fmaf(xf[i], q1[i], q2[i]));
+              const uint4 o = pack8(f, false);
+              *reinterpret_cast<uint4*>(B + off) = o;
+              unpack8(o, f);  // dbias sums the operand the MMA sees
             }
-          }
-        }
-        // dbias = sum over positions of the (transformed) dy rows (m-group 0 units only)
-        if (p.wsb != nullptr && tmg == 0) {
-          const int co0 = tnt * BN + jb * 8;
-          if (co0 < p.cout) {
-            const uint8_t* B = stage_b(st);
-#pragma unroll
-            for (int k = 0; k < L::UB; ++k) {
-              if (!((mask >> (24 + k)) & 1u)) continue;
-              const int r = rb0 + RBS * k;
-              const int b = jb / L::BCPR, jj = jb % L::BCPR;
-              uint32_t off = b * KB * L::BRB + r * L::BRB;
-              if constexpr (L::BRB == 128) off += (jj ^ (r & 7)) << 4;
-              else off += (jj ^ ((r >> 1) & 3)) << 4;
-              float f[8];
-              unpack8(*reinterpret_cast<const uint4*>(B + off), f);
+            if (need_db && mg == 0) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) bacc[i] += f[i];
             }
           }
+          wrote = wrote || xb;
         }
-        fence_proxy_async_smem();
+        if (wrote) fence_proxy_async_smem();
         mbar_arrive(&full_bar[st]);
-        if (++tk == tcnt) {
-          if (p.wsb != nullptr && tmg == 0) {  // fixed-order combine of the unit's dbias partials
+        if (++st == ST) { st = 0; ph ^= 1u; }
+      }
+      if (need_db && mg == 0) {  // fixed-order combine of the unit's dbias partials
 #pragma unroll
-            for (int i = 0; i < 8; ++i) { bred[i * LT + tid] = bacc[i]; bacc[i] = 0.f; }
-            named_bar_sync(1, LT);
-            if (tid < L::BCH * 8) {
-              const int jc = tid >> 3, i = tid & 7;
-              const int co = tnt * BN + jc * 8 + i;
-              float sacc = 0.f;
-              for (int t = jc; t < LT; t += L::BCH) sacc += bred[i * LT + t];
-              if (co < p.cout) p.wsb[(long long)tsp * p.cout + co] = sacc;
+        for (int i = 0; i < 8; ++i) { bred[i * LT + tid] = bacc[i]; bacc[i] = 0.f; }
+        named_bar_sync(1, LT);
+        if (tid < L::BCH * 8) {
+          const int jc = tid >> 3, i = tid & 7;
+          const int co = nt * BN + jc * 8 + i;
+          float sacc = 0.f;
+          for (int t = jc; t < LT; t += L::BCH) sacc += bred[i * LT + t];
+          if (co < p.cout) p.wsb[(long long)sp * p.cout + co] = sacc;
+        }
+        named_bar_sync(1, LT);
+      }
+    }
+  } else if (warp == WG_PRODUCER) {
+    // =============================== TMA producer ===============================
+    if (lane == 0) {
+      const uint32_t a_bytes = (uint32_t)p.Rld * 128u * L::AAT;
+      const uint32_t b_bytes = (uint32_t)p.Kr * L::BRB * L::NBA;
+      const uint32_t tx = a_bytes + b_bytes * (xb ? 2u : 1u);
+      int st = 0, round = 0;
+      for (int ui = 0; ui < nun; ++ui) {
+        int mg, nt, sp;
+        unit_of(ui, mg, nt, sp);
+        const int cnt = kb_count(sp);
+        for (int k = 0; k < cnt; ++k) {
+          const int kb = sp * p.kpt + k;
+          if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
+          mbar_arrive_expect_tx(&ld_bar[st], tx);
+          const uint32_t A = smem_u32(stage_a(st)), B = smem_u32(stage_b(st)), X = smem_u32(stage_x(st));
+          if (TAPS == 9) {
+            int img0, y0;
+            kb_org(kb, img0, y0);
+            const int oy = y0 + 1;
+#pragma unroll
+            for (int a = 0; a < L::AAT; ++a)
+              tma_load_4d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, -1, y0, img0, &ld_bar[st]);
+#pragma unroll
+            for (int b = 0; b < L::NBA; ++b) {
+              const int c = nt * BN + b * (L::BRB / 2);
+              tma_load_4d(B + b * KB * L::BRB, &p.tma_dy, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
+              if (xb) tma_load_4d(X + b * KB * L::BRB, &p.tma_dyx, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
             }
-            named_bar_sync(1, LT);
+          } else {
+#pragma unroll
+            for (int a = 0; a < L::AAT; ++a)
+              tma_load_2d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, kb * KB, &ld_bar[st]);
+#pragma unroll
+            for (int b = 0; b < L::NBA; ++b) {
+              const int c = nt * BN + b * (L::BRB / 2);
+              tma_load_2d(B + b * KB * L::BRB, &p.tma_dy, c, kb * KB, &ld_bar[st]);
+              if (xb) tma_load_2d(X + b * KB * L::BRB, &p.tma_dyx, c, kb * KB, &ld_bar[st]);
+            }
           }
-          tk = 0;
-          if (++tu < nun) { unit_of(tu, tmg, tnt, tsp); tcnt = kb_count(tsp); }
+          if (++st == ST) { st = 0; ++round; }
         }
       }
     }
-    cp_async_wait<0>();
+    __syncwarp();
   } else if (warp == NLW) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 1, 1);
-      int g = 0;
+      const int ksteps = (p.Kr + 15) / 16;
+      int st = 0;
+      uint32_t ph = 0;
       for (int ui = 0; ui < nun; ++ui) {
         int mg, nt, sp;
         unit_of(ui, mg, nt, sp);
         const int cnt = kb_count(sp);
         if (ui >= 1) mbar_wait(&acce_bar, (ui - 1) & 1);
         tc_fence_after();
-        for (int k = 0; k < cnt; ++k, ++g) {
-          const int st = g % ST;
-          mbar_wait(&full_bar[st], (g / ST) & 1);
+        for (int k = 0; k < cnt; ++k) {
+          mbar_wait(&full_bar[st], ph);
           tc_fence_after();
           const uint32_t abase = smem_u32(stage_a(st)), bbase = smem_u32(stage_b(st));
           const uint64_t a0 = make_sdesc(abase, p.RA * 128, 1024, kLayoutSW128);
@@ -1002,14 +1017,15 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const WgParams p) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               const uint64_t am = a0 + ((2u * mt * p.RA * 128u + shift * 128u) >> 4);
-#pragma unroll
-              for (int kk = 0; kk < KB / 16; ++kk) {
+#pragma unroll 1
+              for (int kk = 0; kk < ksteps; ++kk) {
                 umma_f16(tmem + (u * MT + mt) * BN, am + kk * 128, b0 + ((kk * 16 * L::BRB) >> 4), idesc,
                          (k > 0 || kk > 0) ? 1u : 0u);
               }
             }
           }
           umma_commit(&empty_bar[st]);
+          if (++st == ST) { st = 0; ph ^= 1u; }
         }
         umma_commit(&accf_bar);
       }
@@ -1117,10 +1133,11 @@ template <int BN, int MT, int TAPS, int KB>
 static int launch_wg(WgParams p, cudaStream_t st) {
   auto kern = wgrad_kernel<BN, MT, TAPS, KB>;
   const int cin_pad = p.MG * MT * 128, npad = p.NT * BN;
+  const bool xop = p.dy_pro == BNFF_PRO_BN_DX;
   int stages = 8;
   WgCarve c{};
   for (; stages >= 2; --stages) {
-    c = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, stages);
+    c = wg_carve<BN, MT, TAPS, KB>(p.RA, cin_pad, npad, stages, xop);
     if (c.total <= SMEM_BUDGET) break;
   }
   if (stages < 2) return kWindowNoFit;
@@ -1132,7 +1149,7 @@ static int launch_wg(WgParams p, cudaStream_t st) {
     attr = c.total;
   }
   const int grid = p.units < num_sms_wc() ? p.units : num_sms_wc();
-  launch(kern, dim3(grid), dim3(THREADS), c.total, st, p);
+  launch(kern, dim3(grid), dim3(WG_THREADS), c.total, st, p);
   return check_launch("wgrad window");
 }
 
@@ -1468,7 +1485,10 @@ namespace bnff {
 namespace wc {
 struct WgPlan {
   int ok, taps, BN, MT, KB, NT, MG, RA, nkb, kpt, splits, hp, wp, Q;
+  int tmode, kt, BR, BI, WPI, tpi, Rld, Kr, P;
 };
+// k-blocks are the forward kernel's tiles (3x3: kt padded output rows of one image, or
+// kt whole images; 1x1: KB pixels); splits spread them over the SMs
 static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
   WgPlan q{};
   q.taps = kh * kh;
@@ -1477,19 +1497,39 @@ static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
   const long long Q = (long long)n * q.hp * q.wp;
   if (Q >= (1ll << 30)) return q;
   q.Q = (int)Q;
+  q.P = n * h * w;
   if (q.taps == 9) {
     q.BN = 32; q.MT = 1; q.KB = 128;
-    q.RA = align_up(q.KB + 2 * q.wp + 2, 8);
-    if (q.RA > q.KB + 128) return q;  // window taller than WgL::RAMAX: generic kernel
+    const int hpwp = q.hp * q.wp;
+    if (hpwp <= 128) {
+      q.tmode = 2;
+      q.kt = 128 / hpwp;
+      q.BR = q.hp; q.BI = q.kt; q.WPI = hpwp;
+      q.nkb = (n + q.kt - 1) / q.kt;
+      q.Kr = q.kt * hpwp;
+    } else {
+      q.tmode = 1;
+      q.kt = 128 / q.wp;
+      if (q.kt > h) q.kt = h;
+      if (q.kt < 1) return q;
+      q.BR = q.kt + 2; q.BI = 1; q.WPI = q.BR * q.wp;
+      q.tpi = (h + q.kt - 1) / q.kt;
+      q.nkb = n * q.tpi;
+      q.Kr = q.kt * q.wp;
+    }
+    q.Rld = q.BR * q.BI * q.wp;
+    const int rmma = 128 + 2 * q.wp + 2;
+    q.RA = align_up(q.Rld > rmma ? q.Rld : rmma, 8);
+    if (q.RA > RMAX) return q;  // window taller than the allocation: generic kernel
   } else {
     q.BN = pick_bn(cout);
     q.MT = ((q.BN == 64 || q.BN == 128) && cin > 128) ? 2 : 1;  // the instantiated MT=2 variants
     q.KB = 64;
-    q.RA = q.KB;
+    q.RA = q.Rld = q.Kr = q.KB;
+    q.nkb = (q.P + q.KB - 1) / q.KB;
   }
   q.NT = (cout + q.BN - 1) / q.BN;
   q.MG = (cin + q.MT * 128 - 1) / (q.MT * 128);
-  q.nkb = (q.Q + q.KB - 1) / q.KB;
   const int target = num_sms_wc();
   int splits = (target + q.MG * q.NT - 1) / (q.MG * q.NT);
   const int maxs = q.nkb;  // small spatial sizes (14^2, 7^2): down to one k-block per split
@@ -1499,11 +1539,6 @@ static WgPlan wg_plan(int n, int h, int w, int cin, int cout, int kh, int pad) {
   q.splits = (q.nkb + q.kpt - 1) / q.kpt;
   q.ok = 1;
   return q;
-}
-
-template <int BN, int MT, int TAPS, int KB>
-static int run_wg(const WgPlan& q, WgParams p, cudaStream_t st) {
-  return launch_wg<BN, MT, TAPS, KB>(p, st);
 }
 }  // namespace wc
 }  // namespace bnff
@@ -1525,17 +1560,35 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   if (!q.ok) return wc::kWindowNoFit;  // caller uses the generic kernel
   wc::WgParams p{};
   p.n = (int)x.n; p.h = (int)x.h; p.w = (int)x.w; p.hp = q.hp; p.wp = q.wp; p.pad = pad; p.Q = q.Q;
+  p.tmode = q.tmode; p.kt = q.kt; p.BR = q.BR; p.BI = q.BI; p.WPI = q.WPI; p.tpi = q.tpi;
+  p.Rld = q.Rld; p.Kr = q.Kr; p.P = q.P;
   p.fd_hpwp = make_fastdiv(q.hp * q.wp);
   p.fd_wp = make_fastdiv(q.wp);
   p.cin = (int)x.c; p.cout = (int)dy.c;
   p.KB = q.KB; p.RA = q.RA; p.nkb = q.nkb; p.kpt = q.kpt; p.splits = q.splits;
   p.MG = q.MG; p.NT = q.NT; p.units = q.MG * q.NT * q.splits;
-  p.x = (const __nv_bfloat16*)x.ptr; p.x_rs = x.row_stride; p.x_pro = x_pro; p.x_coef = x_coef;
-  p.dy = (const __nv_bfloat16*)dy.ptr; p.dy_rs = dy.row_stride;
-  p.dyx = (const __nv_bfloat16*)dy_x.ptr; p.dyx_rs = dy_x.row_stride;
+  p.x_pro = x_pro; p.x_coef = x_coef;
   p.dy_pro = dy_pro; p.dy_coef = dy_coef;
   p.ws = ws;
   p.wsb = dbias ? ws + (long long)q.splits * q.taps * p.cin * p.cout : nullptr;
+  // TMA boxes: x window {64, wp, BR, BI} / {64, KB}; dy (and dy_x) {brb/2, wp, rows, imgs} / {brb/2, KB}
+  const uint32_t bch = (q.BN * 2 >= 128 ? 128 : q.BN * 2) / 2;
+  uint32_t bx[4], bd[4];
+  int rank;
+  if (q.taps == 9) {
+    rank = 4;
+    bx[0] = 64; bx[1] = q.wp; bx[2] = q.BR; bx[3] = q.BI;
+    bd[0] = bch; bd[1] = q.wp; bd[2] = q.tmode == 2 ? q.hp : q.kt; bd[3] = q.tmode == 2 ? q.kt : 1;
+  } else {
+    rank = 2;
+    bx[0] = 64; bx[1] = q.KB;
+    bd[0] = bch; bd[1] = q.KB;
+  }
+  if (!encode_nhwc_bf16(&p.tma_x, x.ptr, x.n, x.h, x.w, x.c, x.row_stride, rank, bx) ||
+      !encode_nhwc_bf16(&p.tma_dy, dy.ptr, dy.n, dy.h, dy.w, dy.c, dy.row_stride, rank, bd) ||
+      (dy_pro == BNFF_PRO_BN_DX &&
+       !encode_nhwc_bf16(&p.tma_dyx, dy_x.ptr, dy_x.n, dy_x.h, dy_x.w, dy_x.c, dy_x.row_stride, rank, bd)))
+    return set_error(BNFF_ERR_CUDA, "wgrad window: cuTensorMapEncodeTiled failed");
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   if (q.taps == 9) rc = wc::launch_wg<32, 1, 9, 128>(p, st);

@@ -131,7 +131,7 @@ class Engine:
 
     def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
                  save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True,
-                 sync_bn: bool = False, group=None):
+                 sync_bn: bool = False, group=None, side_wgrad: bool = True):
         self.L = _lib.lib()
         self.g = g
         self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
@@ -150,6 +150,8 @@ class Engine:
         if self.sync_bn and any(n.kind == G.BN and not n.attrs.onepass for n in g.nodes):
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window) and self.dcode == _lib.BF16
+        self.side_wgrad = bool(side_wgrad)
+        self._side = None  # side stream of the weight-gradient launches
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
         self.cols = {}  # stem conv name -> (1x1 conv over col, col buffer, dw scratch, kpad)
         self.col_src = {}  # 1x1 col conv name -> (fp32 (co, kpad) weights, stem conv, kpad)
@@ -252,7 +254,7 @@ class Engine:
         return Stats(*arrs, count=count)
 
     # ------------------------------------------------------------ emit helpers
-    def _emit(self, fn, *args, what="", nbytes=0, flops=0, launches=1):
+    def _emit(self, fn, *args, what="", nbytes=0, flops=0, launches=1, side=False):
         """Append a launch thunk calling fn(*args, stream).  ``nbytes``/``flops`` are the
         launch's ALGORITHMIC HBM bytes / FLOPs (each tensor counted once), used by the
         live roofline in bench.py."""
@@ -266,6 +268,7 @@ class Engine:
         thunk.nbytes = int(nbytes)
         thunk.flops = int(flops)
         thunk.launches = launches  # kernels this C-ABI call launches
+        thunk.side = bool(side)    # runs on the side stream (forked/joined by _run)
         self._cur.append(thunk)
 
     def _emit_allreduce(self, *tensors, what="allreduce"):
@@ -621,6 +624,29 @@ class Engine:
             dy, dy_x, dy_pro, dy_coef = dy_gv.dt1, dy_gv.x, _lib.PRO_BN_DX, dy_gv.coef()
         else:
             dy, dy_x, dy_pro, dy_coef = dy_gv.t, dy_gv.t, _lib.PRO_NONE, coef_of()
+        xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
+        col = self.cols.get(conv.name) if x_pro == _lib.PRO_NONE else None
+        orig, wconv, wx, wcin = conv, conv, x, cin_store
+        dw = self.grad(f"{conv.name}.weight")
+        if col is not None:  # stem: weight gradient of the 1x1 GEMM over the patch matrix
+            wconv, wx, dw = col[0], col[1], col[2]
+            wcin = wx.shape[3]
+        wa = _lib.WgradArgs(self.dcode, wconv.kh, wconv.kw, wconv.stride, wconv.pad, view_of(wx), x_pro,
+                            xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
+                            _ptr(dw), wconv.in_c, _ptr(self.grad(f"{orig.name}.bias")))
+        self._keep.append(wa)
+        n_, oh_, ow_, co_ = dy.shape
+        flops = 2 * n_ * oh_ * ow_ * co_ * wconv.kh * wconv.kw * wcin
+        extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
+        # the weight gradient is off the critical path: it runs on the side stream, forked
+        # before this conv's dgrad (they read the same dy) and joined at the end of backward
+        self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}",
+                   nbytes=_nb(wx, dy) + extra + 4 * wconv.out_c * wconv.in_c * wconv.kh * wconv.kw,
+                   flops=flops, launches=4, side=self.side_wgrad)
+        if col is not None:
+            self._emit(self.L.bnff_cols_to_weight, _ptr(col[2]), orig.out_c, orig.in_c, orig.kh,
+                       orig.kw, col[3], _ptr(self.grad(f"{orig.name}.weight")),
+                       what=f"cols_to_weight {node.name}", side=self.side_wgrad)
         dx, part = None, None
         if self._wants_dx(node.inputs[0]):
             dx = self._empty(tuple(x.shape))
@@ -639,27 +665,6 @@ class Engine:
             extra += _nb(x) if dgrad_epi != _lib.DG_PLAIN else 0
             self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
                        nbytes=_nb(dy, dx, wt) + extra, flops=flops)
-        xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
-        col = self.cols.get(conv.name) if x_pro == _lib.PRO_NONE else None
-        orig = conv
-        dw = self.grad(f"{conv.name}.weight")
-        if col is not None:  # stem: weight gradient of the 1x1 GEMM over the patch matrix
-            conv, x, dw, _ = col[0], col[1], col[2], col[3]
-            cin_store = x.shape[3]
-        wa = _lib.WgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x), x_pro,
-                            xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
-                            _ptr(dw), conv.in_c, _ptr(self.grad(f"{orig.name}.bias")))
-        self._keep.append(wa)
-        n_, oh_, ow_, co_ = dy.shape
-        flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
-        extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
-        self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}",
-                   nbytes=_nb(x, dy) + extra + 4 * conv.out_c * conv.in_c * conv.kh * conv.kw,
-                   flops=flops, launches=4)
-        if col is not None:
-            self._emit(self.L.bnff_cols_to_weight, _ptr(col[2]), orig.out_c, orig.in_c, orig.kh,
-                       orig.kw, col[3], _ptr(self.grad(f"{orig.name}.weight")),
-                       what=f"cols_to_weight {node.name}")
         return dx, part
 
     def _b_Conv2D(self, node):
@@ -867,9 +872,27 @@ class Engine:
         return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
 
     def _run(self, thunks):
-        s = self._stream()
+        """Launch thunks in order on the current stream; side thunks go to the side stream,
+        each forked from the current stream's position at that point, and the side stream
+        is joined back before returning (also under CUDA-graph capture)."""
+        main = torch.cuda.current_stream(self.dev)
+        s = C.c_void_p(main.cuda_stream)
+        side_used = False
         for t in thunks:
-            t(s)
+            if getattr(t, "side", False):
+                if self._side is None:
+                    self._side = torch.cuda.Stream(self.dev)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self._side.wait_event(ev)
+                t(C.c_void_p(self._side.cuda_stream))
+                side_used = True
+            else:
+                t(s)
+        if side_used:
+            ev = torch.cuda.Event()
+            ev.record(self._side)
+            main.wait_event(ev)
 
     def set_input(self, x):
         """Graph input: NCHW fp32 (numpy or torch, host or device) -> padded NHWC."""

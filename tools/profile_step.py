@@ -49,6 +49,19 @@ def main():
           f"sum of launches {total:.3f} ms")
     for k, (ms, n) in sorted(by.items(), key=lambda kv: -kv[1][0]):
         print(f"  {k:16s} n={n:4d} total={ms:8.3f} ms share={ms / total:.3f}")
+    import re
+    grp = {}
+    for t, ms in prof:
+        key = t.kind + " " + re.sub(r"\.l\d+\.", ".l*.", t.what.split(" ", 1)[1] if " " in t.what else "")
+        d = grp.setdefault(key, [0.0, 0, 0, 0])
+        d[0] += ms
+        d[1] += 1
+        d[2] += t.nbytes
+        d[3] += t.flops
+    print("# by layer group")
+    for k, (ms, n, b, f) in sorted(grp.items(), key=lambda kv: -kv[1][0])[:30]:
+        print(f"  {k:36s} n={n:3d} {ms:7.3f} ms  {b / (ms * 1e-3) / 1e9 if ms else 0:6.0f} GB/s "
+              f"{f / (ms * 1e-3) / 1e12 if ms else 0:6.1f} TF/s")
     print("# top launches")
     rows = sorted(prof, key=lambda r: -r[1])[: args.top]
     for t, ms in rows:

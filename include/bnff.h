@@ -44,6 +44,12 @@ enum {
   BNFF_DG_PLAIN = 0,         /* dx (ops.py:193-202) */
   BNFF_DG_CLIP = 1,          /* dx where x>0 (execute.py:331-332) */
   BNFF_DG_NRC = 2,           /* dt1 = dx where relu(bn(x))>0, + sum dt1, sum dt1*xhat (fused.py:176-188) */
+  /* NRC with the block-gradient fold (ICF): instead of storing dt1 for a
+   * later split_bwd, the epilogue writes dx := (ACC ? dx : 0) + scale * dt1 into the
+   * block gradient buffer (scale = gamma*invstd = x_coef.b); the per-channel remainder
+   * -scale*(k1 + xhat*k2) is accumulated by bnff_dx_coeffs_acc.  Window kernels only.  */
+  BNFF_DG_NRC_ACC = 3,
+  BNFF_DG_NRC_SET = 4,
 };
 
 typedef struct {
@@ -205,6 +211,16 @@ int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count,
                    const double* mean, const double* var, const float* gamma, float eps,
                    double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
                    float* mean32, float* inv32, float* dgamma32, float* dbeta32, void* stream);
+
+/* bnff_dx_coeffs plus the ICF block-gradient fold: acc_a[c] (+)= g*k1, acc_b[c] (+)= g*k2
+ * (acc_init = 1 overwrites), and mean32/inv32 written into the caller's block-level
+ * arrays, so the block gradient resolves as G - acc_a - acc_b*xhat when its producer
+ * reads it (bn_dx_from_sums ops.py:283-298 re-associated over consumers).            */
+int bnff_dx_coeffs_acc(int32_t c, const float* part, int32_t tiles, int64_t count,
+                       const double* mean, const double* var, const float* gamma, float eps,
+                       double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
+                       float* mean32, float* inv32, float* dgamma32, float* dbeta32,
+                       float* acc_a, float* acc_b, int32_t acc_init, void* stream);
 
 /* SyncBN (data parallel with global-batch statistics): bnff_stats_finalize with mean/var
  * NULL reduces partials to float64 (sum, sumsq) only; the caller all-reduces them and

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libbnff.so")
 
 F32, BF16 = 0, 1
 PRO_NONE, PRO_RELU, PRO_BN_RELU, PRO_BN_DX = 0, 1, 2, 3
-DG_PLAIN, DG_CLIP, DG_NRC = 0, 1, 2
+DG_PLAIN, DG_CLIP, DG_NRC, DG_NRC_ACC, DG_NRC_SET = 0, 1, 2, 3, 4
 
 
 class View(C.Structure):
@@ -94,6 +94,8 @@ SIGNATURES = {
     "bnff_bn_coeffs": (C.c_int, [_I32, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),
     "bnff_dx_coeffs": (C.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _P]),
+    "bnff_dx_coeffs_acc": (C.c_int, [_I32, _P, _I32, _I64, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P,
+                                     _P, _P, _P, _P, _P, _I32, _P]),
     "bnff_stats_from_sums": (C.c_int, [_I32, _I64, _P, _P, _P, _P, _P]),
     "bnff_dx_coeffs_from_sums": (C.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P,
                                            _P]),

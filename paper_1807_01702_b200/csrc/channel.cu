@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __rest
 __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
     const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
     const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
-    float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32) {
+    float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32, float* acc_a,
+    float* acc_b, int acc_init) {
   griddep_launch();
   griddep_wait();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -137,6 +138,12 @@ __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
     inv32[c] = (float)inv;
     if (dgamma32) dgamma32[c] = (float)dgamma;
     if (dbeta32) dbeta32[c] = (float)dbeta;
+    if (acc_a) {  // ICF block-gradient fold: per-channel remainder g*(k1 + xhat*k2)
+      const float gf = (float)((double)gamma[c] * inv);
+      const float a = gf * (float)(dbeta / (double)count), b = gf * (float)(dgamma / (double)count);
+      acc_a[c] = acc_init ? a : acc_a[c] + a;
+      acc_b[c] = acc_init ? b : acc_b[c] + b;
+    }
   }
 }
 
@@ -958,8 +965,22 @@ extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64
                               float* dgamma32, float* dbeta32, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   launch(dx_coeffs_fused_kernel, dim3((c + 31) / 32), dim3(512), 0, st, part, tiles, c, count, mean, var, gamma, eps, dgamma64,
-                                                         dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32);
+                                                         dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32,
+         (float*)nullptr, (float*)nullptr, 0);
   return check_launch("dx_coeffs");
+}
+
+extern "C" int bnff_dx_coeffs_acc(int32_t c, const float* part, int32_t tiles, int64_t count, const double* mean,
+                                  const double* var, const float* gamma, float eps, double* dgamma64,
+                                  double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
+                                  float* dgamma32, float* dbeta32, float* acc_a, float* acc_b, int32_t acc_init,
+                                  void* stream) {
+  if (!acc_a || !acc_b) return set_error(BNFF_ERR_SHAPE, "dx_coeffs_acc: accumulators required");
+  cudaStream_t st = (cudaStream_t)stream;
+  launch(dx_coeffs_fused_kernel, dim3((c + 31) / 32), dim3(512), 0, st, part, tiles, c, count, mean, var, gamma, eps, dgamma64,
+                                                         dbeta64, k1, k2, g, mean32, inv32, dgamma32, dbeta32, acc_a,
+         acc_b, (int)acc_init);
+  return check_launch("dx_coeffs_acc");
 }
 
 extern "C" int bnff_bn_apply(int32_t dtype, bnff_view x, bnff_view y, bnff_coef coef, int32_t relu,

@@ -771,14 +771,17 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
     return set_error(BNFF_ERR_SHAPE, "dgrad: dy spatial dims inconsistent with dx");
   if (a->dy_pro == BNFF_PRO_BN_DX && (rc = check_common(a->dtype, a->dy_x, "dgrad dy_x"))) return rc;
   if (a->epi != BNFF_DG_PLAIN && (rc = check_common(a->dtype, a->x, "dgrad x"))) return rc;
+  const bool fold = a->epi == BNFF_DG_NRC_ACC || a->epi == BNFF_DG_NRC_SET;
+  if (a->epi < BNFF_DG_PLAIN || a->epi > BNFF_DG_NRC_SET) return set_error(BNFF_ERR_SHAPE, "dgrad: bad epilogue");
   if (a->wwin && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     if (a->dy_pro == BNFF_PRO_BN_DX && (!a->dy_coef.a || !a->dy_coef.e))
       return set_error(BNFF_ERR_STATE, "dgrad: missing deferred-gradient coefficients");
     const int wrc = bnff_window_conv(1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx,
                                      a->wwin, nullptr, a->epi, a->x, a->x_coef,
-                                     a->epi == BNFF_DG_NRC ? a->stat_part : nullptr, stream);
+                                     a->epi >= BNFF_DG_NRC ? a->stat_part : nullptr, stream);
     if (wrc != kWindowNoFitAbi) return wrc;
   }
+  if (fold) return set_error(BNFF_ERR_UNSUPPORTED, "dgrad: the block-gradient fold needs the window kernel");
   p.M = p.n * p.h * p.w;
   p.N = p.cin;
   p.kred = p.cout;

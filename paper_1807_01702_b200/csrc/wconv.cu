@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     if (c < p.N) {
       if (MODE == M_FPROP) {
         t0 = p.bias ? p.bias[c] : 0.f;
-      } else if (p.epi == BNFF_DG_NRC) {
+      } else if (p.epi >= BNFF_DG_NRC) {
         const float m = p.ecoef.a[c], s = p.ecoef.b[c], b = p.ecoef.c[c], inv = p.ecoef.d[c];
         t0 = s;
         t1 = b - m * s;
@@ -455,7 +455,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     constexpr int RG = 128 / HALF;           // row groups in the column pass
     const int cp = gt % HALF, rg = gt / HALF;
     const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
-    const bool nrc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC;
+    const bool nrc = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC;
+    const bool fold = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC_ACC;  // out (+)= scale * dt1
+    const bool fold_acc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC_ACC;
     const bool stats = do_stats && (MODE == M_FPROP || nrc);
     const bool persist = p.ntiles == 1;      // same columns every tile: keep sums in registers
     float2 acc1[MYCH], acc2[MYCH];
@@ -533,6 +535,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       int mt, n0;
       tile_of(it, mt, n0);
       gpix[row] = out_pix(mt, row);
+      if (MODE == M_DGRAD && fold_acc) named_bar_sync(bar_id, 128);  // gpix of every row for the prefetch
       const int pix = gpix[row];
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
       tc_fence_after();
@@ -541,6 +544,23 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         const int ci = grp + 2 * k;
         if (ci >= NCH) break;
         const int cc = ci * CW;
+        uint4 gold[4];
+        if (MODE == M_DGRAD && fold_acc) {  // prefetch the old block-gradient chunks this thread stores
+          constexpr int CPO = CW / 8;
+#pragma unroll
+          for (int i = 0; i < CPO && i < 4; ++i) {
+            const int kk = gt + 128 * i;
+            const int r = kk / CPO, ch = kk - r * CPO;
+            const int px = gpix[r];
+            const int col = n0 + cc + ch * 8;
+            gold[i] = (px >= 0 && col < p.N)
+                          ? *reinterpret_cast<const uint4*>(p.out + (long long)px * p.out_rs + col)
+                          : make_uint4(0, 0, 0, 0);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) gold[i] = make_uint4(0, 0, 0, 0);
+        }
         if (need_x) cp_async_wait<MYCH - 1>();
         const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
         // ---- row pass
@@ -617,14 +637,35 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         }
         // ---- store pass
         constexpr int CPO = CW / 8;  // 16B chunks per staged row
+        if (MODE == M_DGRAD && fold) {
+          // block-gradient fold: out = (acc ? out : 0) + scale * dt1; the old block-gradient
+          // chunks were fetched into registers before the row pass (their latency hides there)
+#pragma unroll
+          for (int i = 0; i < CPO && i < 4; ++i) {
+            const int kk = gt + 128 * i;
+            const int r = kk / CPO, ch = kk - r * CPO;
+            const int px = gpix[r];
+            const int col = n0 + cc + ch * 8;
+            if (px >= 0 && col < p.N) {
+              float d[8], sc[8], o[8];
+              unpack8(*reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16), d);
+              ld8f(etab + col, sc);
+              unpack8(gold[i], o);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) d[e] = fold_acc ? fmaf(sc[e], d[e], o[e]) : sc[e] * d[e];
+              *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = pack8(d, false);
+            }
+          }
+        } else {
 #pragma unroll 2
-        for (int kk = gt; kk < 128 * CPO; kk += 128) {
-          const int r = kk / CPO, ch = kk - r * CPO;
-          const int px = gpix[r];
-          const int col = n0 + cc + ch * 8;
-          if (px >= 0 && col < p.N) {
-            const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
-            *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
+          for (int kk = gt; kk < 128 * CPO; kk += 128) {
+            const int r = kk / CPO, ch = kk - r * CPO;
+            const int px = gpix[r];
+            const int col = n0 + cc + ch * 8;
+            if (px >= 0 && col < p.N) {
+              const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
+              *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
+            }
           }
         }
         named_bar_sync(bar_id, 128);  // staging, x buffer k and gpix free

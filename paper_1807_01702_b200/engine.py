@@ -97,10 +97,11 @@ class Deferred:
     k1: torch.Tensor
     k2: torch.Tensor
     g: torch.Tensor
+    affine: bool = False  # ICF fold: dt1 is the block gradient buffer, g = 1, (k1, k2) = (A, B)
 
     def slice(self, lo, hi):
         return Deferred(self.dt1[..., lo:hi], self.x[..., lo:hi], self.mean[lo:hi],
-                        self.inv[lo:hi], self.k1[lo:hi], self.k2[lo:hi], self.g[lo:hi])
+                        self.inv[lo:hi], self.k1[lo:hi], self.k2[lo:hi], self.g[lo:hi], self.affine)
 
     def coef(self):
         return coef_of(self.mean, self.inv, self.k1, self.k2, self.g)
@@ -109,6 +110,13 @@ class Deferred:
 @dataclass
 class Plain:
     t: torch.Tensor
+
+
+@dataclass
+class Folded:
+    """A split branch whose gradient was folded into the block gradient buffer by the
+    consumer's dgrad epilogue (BNFF_DG_NRC_ACC/SET); the sibling branch carries it."""
+    into: int  # the sibling slot now holding the combined gradient
 
 
 # ---------------------------------------------------------------------------
@@ -131,7 +139,7 @@ class Engine:
 
     def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
                  save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True,
-                 sync_bn: bool = False, group=None, side_wgrad: bool = True):
+                 sync_bn: bool = False, group=None, side_wgrad: bool = True, fold_icf: bool = True):
         self.L = _lib.lib()
         self.g = g
         self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
@@ -151,12 +159,18 @@ class Engine:
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window) and self.dcode == _lib.BF16
         self.side_wgrad = bool(side_wgrad)
+        # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
+        # into the block gradient buffer; the per-channel remainder rides in (A, B) arrays
+        self.fold_icf = bool(fold_icf) and self.dcode == _lib.BF16
+        self.fold = {}  # block group -> dict(A, B, ones, m32, i32, started)
         self._side = None  # side stream of the weight-gradient launches
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
         self.cols = {}  # stem conv name -> (1x1 conv over col, col buffer, dw scratch, kpad)
         self.col_src = {}  # 1x1 col conv name -> (fp32 (co, kpad) weights, stem conv, kpad)
         self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
                               (n.kind == G.CONCAT and not n.attrs.physical) for n in g.nodes)
+        self.fold_icf = self.fold_icf and not self.sync_bn and any(
+            n.kind == G.FUSED_CONCAT_STATS for n in g.nodes)
         self.fwd: list = []
         self.bwd: list = []
         self.opt: list = []
@@ -616,8 +630,10 @@ class Engine:
     def _wants_dx(self, sid):
         return self.input_grad or sid not in self.g.inputs
 
-    def _conv_backward(self, node, conv, x, dy_gv, x_pro, x_tables, dgrad_epi, dgrad_tables):
-        """dgrad (+ epilogue) and wgrad of one conv; returns the dx tensor (or None)."""
+    def _conv_backward(self, node, conv, x, dy_gv, x_pro, x_tables, dgrad_epi, dgrad_tables,
+                       dx_out=None):
+        """dgrad (+ epilogue) and wgrad of one conv; returns the dx tensor (or None).
+        dx_out: the block gradient view the fold epilogues (DG_NRC_ACC/SET) write into."""
         cin_store = x.shape[3]
         wp, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if isinstance(dy_gv, Deferred):
@@ -649,9 +665,9 @@ class Engine:
                        what=f"cols_to_weight {node.name}", side=self.side_wgrad)
         dx, part = None, None
         if self._wants_dx(node.inputs[0]):
-            dx = self._empty(tuple(x.shape))
+            dx = self._empty(tuple(x.shape)) if dx_out is None else dx_out
             ecoef = coef_of()
-            if dgrad_epi == _lib.DG_NRC:
+            if dgrad_epi >= _lib.DG_NRC:
                 part = self._zeros((self.L.bnff_stat_rows(), 2, x.shape[3]), torch.float32)
                 m32, s32, b32, i32 = dgrad_tables
                 ecoef = coef_of(m32, s32, b32, i32)
@@ -663,6 +679,7 @@ class Engine:
             flops = 2 * n_ * h_ * w_ * ci_ * conv.kh * conv.kw * dy.shape[3]
             extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
             extra += _nb(x) if dgrad_epi != _lib.DG_PLAIN else 0
+            extra += _nb(dx) if dgrad_epi == _lib.DG_NRC_ACC else 0  # read-modify-write
             self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
                        nbytes=_nb(dy, dx, wt) + extra, flops=flops)
         return dx, part
@@ -759,10 +776,83 @@ class Engine:
         tb = self.node_tables[node.id]
         if not self._wants_dx(node.inputs[0]):
             raise StateError("FusedNormReluConv directly on the graph input is not supported")
+        fold = self._fold_plan(node, at.conv, x)
+        if fold is not None:
+            self._fold_backward(node, at, x, st, tb, gv, *fold)
+            return
         dt1, part = self._conv_backward(node, at.conv, x, gv, _lib.PRO_BN_RELU, tb, _lib.DG_NRC, tb)
         mt = part.shape[0]
         m32, i32, k1, k2, gg = self._dx_coeffs(part, mt, x.shape[3], st.count, st, at.bn, node.name)
         self._add_grad(node.inputs[0], Deferred(dt1, x, m32, i32, k1, k2, gg))
+
+    # ------------------------------------------------- ICF block-gradient fold
+    def _fold_plan(self, node, conv, x):
+        """(target view, sibling slot or None, mode, group, lo) when this consumer's BN dx
+        can be folded into the block gradient buffer, else None."""
+        if not self.fold_icf or conv.kh != 1 or conv.name not in self.wpacks:
+            return None
+        sid = node.inputs[0]
+        slot = self.g.slots[sid]
+        if slot.buffer is None or sid in self.grads:
+            return None
+        grp, lo = slot.buffer
+        if lo != 0:
+            return None
+        prod = self.g.producer_of(sid)
+        if prod is not None and prod.kind == G.SPLIT:
+            sib = next(o for o in prod.outputs if o != sid)
+            sg = self.grads.get(sib)
+            if isinstance(sg, Plain) and any(sg.t.untyped_storage().data_ptr() == t.untyped_storage().data_ptr()
+                                             for t in self.loss_grad.values()):
+                return None  # never accumulate into the caller's loss-gradient buffer
+            if isinstance(sg, Plain) and tuple(sg.t.shape) == tuple(x.shape):
+                return sg.t, sib, _lib.DG_NRC_ACC, grp, lo
+            if isinstance(sg, Deferred) and sg.affine and tuple(sg.dt1.shape) == tuple(x.shape):
+                return sg.dt1, sib, _lib.DG_NRC_ACC, grp, lo
+            return None
+        if len(self.g.consumers_of(sid)) != 1:
+            return None
+        # nothing downstream yet (a transition over the whole block): start a fresh buffer
+        return self._empty(tuple(x.shape)), None, _lib.DG_NRC_SET, grp, lo
+
+    def _fold_arrays(self, grp):
+        fa = self.fold.get(grp)
+        if fa is None:
+            ct = self.g.buffer_groups[grp][0]
+            fa = {k: self._zeros((ct,), torch.float32) for k in ("A", "B", "m32", "i32")}
+            fa["ones"] = torch.ones((ct,), dtype=torch.float32, device=self.dev)
+            self._bufs.append(fa["ones"])
+            fa["started"] = False
+            self.fold[grp] = fa
+        return fa
+
+    def _fold_backward(self, node, at, x, st, tb, gv, target, sib, mode, grp, lo):
+        """1x1 NRC backward whose BN dx is folded into the block gradient: the dgrad epilogue
+        writes target (+)= scale * dt1, dx_coeffs_acc adds g*k1 / g*k2 into (A, B); the
+        block gradient is then G - A - B * xhat (a Deferred with g = 1), resolved by the
+        channels' producers (bn_dx_from_sums ops.py:283-298, re-associated over consumers)."""
+        c = x.shape[3]
+        fa = self._fold_arrays(grp)
+        sl = slice(lo, lo + c)
+        _, part = self._conv_backward(node, at.conv, x, gv, _lib.PRO_BN_RELU, tb, mode, tb,
+                                      dx_out=target)
+        k1, k2, gg = (self._zeros((c,), torch.float32) for _ in range(3))
+        dg64, db64 = self._zeros((c,), torch.float64), self._zeros((c,), torch.float64)
+        # a plain (or fresh) target carries no pending remainder: (A, B) restart for its channels
+        init = 0 if mode == _lib.DG_NRC_ACC and isinstance(self.grads.get(sib), Deferred) else 1
+        self._emit(self.L.bnff_dx_coeffs_acc, c, _ptr(part), part.shape[0], st.count, _ptr(st.mean),
+                   _ptr(st.var), _ptr(self.param(f"{at.bn.name}.gamma")), C.c_float(at.bn.eps),
+                   _ptr(dg64), _ptr(db64), _ptr(k1), _ptr(k2), _ptr(gg), _ptr(fa["m32"][sl]),
+                   _ptr(fa["i32"][sl]), _ptr(self.grad(f"{at.bn.name}.gamma")),
+                   _ptr(self.grad(f"{at.bn.name}.beta")), _ptr(fa["A"][sl]), _ptr(fa["B"][sl]), init,
+                   what=f"dx_coeffs {node.name}")
+        aff = Deferred(target, x, fa["m32"][sl], fa["i32"][sl], fa["A"][sl], fa["B"][sl], fa["ones"][sl],
+                       affine=True)
+        if sib is not None:
+            self.grads[sib] = aff
+            self.grads[node.inputs[0]] = Folded(sib)
+        else:
+            self._add_grad(node.inputs[0], aff)
 
     def _b_Concat(self, node):
         gv = self.grads.get(node.outputs[0])
@@ -793,7 +883,12 @@ class Engine:
             gv = self.grads.get(o)
             if gv is None:
                 raise StateError(f"no gradient arrived at split branch {o}")
+            if isinstance(gv, Folded):  # already inside the sibling branch's gradient
+                continue
             branches.append(gv)
+        if len(branches) == 1:
+            self._add_grad(node.inputs[0], branches[0])
+            return
         # in place into a plain branch's storage when one exists (block gradient buffer)
         out = next((b.t for b in branches if isinstance(b, Plain)), None)
         if out is None:

@@ -299,3 +299,42 @@ def test_stem_im2col_gemm_bf16(level):
     e2.forward()
     torch.cuda.synchronize()
     assert rel_l2(eng.output(), e2.output()) < 1e-2
+
+
+def test_icf_block_gradient_fold_bf16():
+    """ICF block-gradient fold: the 1x1 NRC dgrads accumulate scale*dt1 into
+    the block gradient buffer and the per-channel remainder rides in (A, B), so no
+    split_bwd pass runs.  Same bf16 math as the unfolded schedule except for the order of
+    rounding: output and every gradient within rel-L2 1e-2 of it, and within the bf16 bar
+    of the fp64 oracle relative to the unfused chain (fused <= 1.5x unfused + 1e-3)."""
+    from paper_1807_01702_b200.engine import Engine
+    g0 = G.build_model(aligned_densenet(), seed=0)
+    g, _ = fusion.plan(g0, fusion.parse_level("bnff+icf"))
+    rng = Rng(1)
+    x = rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0)
+    dy = rng.normal(g.slots[g.outputs[0]].shape)
+    runs = {}
+    for fold in (True, False):
+        eng = Engine(g, dtype="bf16", input_grad=True, fold_icf=fold)
+        eng.set_input(x)
+        eng.set_loss_grad(dy)
+        eng.forward()
+        eng.backward()
+        torch.cuda.synchronize()
+        kinds = [t.kind for t in eng.bwd]
+        runs[fold] = (eng.output(), eng.param_grads(), eng.input_grad_nchw(), kinds)
+    assert runs[True][3].count("split_bwd") < runs[False][3].count("split_bwd"), "fold not taken"
+    assert rel_l2(runs[True][0], runs[False][0]) < 1e-2
+    assert rel_l2(runs[True][2], runs[False][2]) < 1e-2, "input grad"
+    for k, v in runs[False][1].items():
+        if k.endswith(".bias"):
+            continue
+        assert rel_l2(runs[True][1][k], v) < 1e-2, k
+    base = _bf16_errors(aligned_densenet(), "baseline")
+    res = OX.forward(g, {g.inputs[0]: x.astype(np.float64)})
+    ref = OX.backward(g, res, {g.outputs[0]: dy.astype(np.float64)})
+    for k, v in ref.params.items():
+        if k.endswith(".bias"):
+            continue
+        e = rel_l2(runs[True][1][k], v)
+        assert e <= 1.5 * base[k] + 1e-3, f"{k}: folded {e:.3e} vs unfused {base[k]:.3e}"

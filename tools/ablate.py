@@ -46,8 +46,7 @@ def main():
         s = eng._stream()
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
-            for t in ts:
-                t(eng._stream())
+            eng._run(ts)  # same stream layout as the engine (side-stream weight gradients)
         gr.replay()
         torch.cuda.synchronize()
         cur = torch.cuda.current_stream()

@@ -148,7 +148,9 @@ def build_engine(level, dtype, batch, lr, world, sync_bn=False):
     from paper_1807_01702_b200 import fusion, graph as G
     from paper_1807_01702_b200.engine import Engine
     g, _ = fusion.plan(G.build_model(G.densenet121(batch), seed=0), fusion.parse_level(level))
-    return g, Engine(g, dtype=dtype, input_grad=False, lr=lr / world, sync_bn=sync_bn)
+    eng = Engine(g, dtype=dtype, input_grad=False, lr=lr / world, sync_bn=sync_bn)
+    eng.level_name = level
+    return g, eng
 
 
 def timed_steps(trainer, steps, warmup, dist_on):
@@ -196,17 +198,32 @@ def roofline(eng, hbm, tflops, peak_kind):
     else:
         ach, peak, unit, bound = gbs, hbm, "GB/s", "hbm"
     shares = {k: round(v["ms"] / total, 4) for k, v in sorted(by.items(), key=lambda kv: -kv[1]["ms"])}
+    traffic, tsrc = None, None
+    try:  # ncu-measured DRAM bytes of the same launch class (committed capture, same workload)
+        with open(os.path.join(ROOT, "profiles", "step_dram_bytes.json")) as f:
+            meas = json.load(f)
+        run = meas["runs"].get(f"bytes_{level_of(eng)}.csv", {}).get(kind)
+        if run and run["launches"]:
+            traffic = round(run["dram_bytes"] / run["launches"])
+            tsrc = "profiles/step_dram_bytes.json (ncu dram__bytes_read+write, per launch, class average)"
+    except (OSError, KeyError, ValueError):
+        pass
     # whole-step roofline bound: sum over launches of max(bytes/BW, flops/peak)
     bound_ms = sum(max(t.nbytes / (hbm * 1e9), t.flops / (tflops * 1e12)) for t, _ in prof) * 1e3
     return {
         "kernel": kind, "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
-        "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
+        "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": tsrc,
+        "algorithmic_bytes_per_launch": round(d["bytes"] / max(d["n"], 1)), "peak_source": peak_kind,
         "launches_per_step": d["n"], "kernel_ms_per_step": round(d["ms"], 4),
         "algorithmic_bytes_per_step": d["bytes"], "algorithmic_flops_per_step": d["flops"],
         "also_gbs": round(gbs, 1), "also_tflops": round(tfs, 2),
     }, {"step_ms_sum_of_launches": round(total, 3), "kernel_shares": shares,
         "step_roofline_bound_ms": round(bound_ms, 3),
         "step_bytes": sum(t.nbytes for t, _ in prof), "step_flops": sum(t.flops for t, _ in prof)}
+
+
+def level_of(eng):
+    return getattr(eng, "level_name", "bnff+icf")
 
 
 def kernel_launches_per_step(eng):
@@ -305,8 +322,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, times = cpu_oracle_rate(2, 2, 1, args.level)
         cpu = {"value": rate, "unit": "images/s", "cores": _NCPU, "kind": "port",
-               "sample": "densenet-121 batch 2 fwd+bwd at bnff, median of 2 iterations after 1 "
-                         "warmup (numpy oracle restating bnfuse; OpenBLAS threads = cores)"}
+               "sample": f"densenet-121 batch 2 fwd+bwd at {args.level}, median of 2 iterations after "
+                         "1 warmup (numpy oracle restating bnfuse; OpenBLAS threads = cores)"}
     if rank != 0:
         return
     line = {

@@ -45,8 +45,27 @@ def run(level, dtype, batch):
     torch.cuda.cudart().cudaProfilerStop()
 
 
-def summarize(paths):
+def kernel_class(name: str) -> str:
+    """ncu kernel name -> engine launch class (engine thunk `kind`)."""
+    if "wgrad_kernel" in name or "wg_reduce_kernel" in name or "wgrad_reduce_kernel" in name \
+            or "igemm_kernel<2" in name or "igemm_kernel<(int)2" in name:
+        return "wgrad"
+    if "wconv_kernel" in name:
+        return "dgrad" if name.split("(")[0].rstrip("> ").endswith("1") else "fprop"
+    if "igemm_kernel<1" in name or "igemm_kernel<(int)1" in name:
+        return "dgrad"
+    if "igemm_kernel" in name:
+        return "fprop"
+    for k in ("stats_finalize", "dx_coeffs", "bn_coeffs", "im2col", "avgpool", "grad_sum",
+              "channel_sums", "sgd", "pack", "relu", "bn_apply"):
+        if k in name:
+            return k
+    return "other"
+
+
+def summarize(paths, json_out=""):
     out = {}
+    classes = {}
     for path in paths:
         with open(path) as f:
             lines = [ln for ln in f if ln.startswith('"')]
@@ -63,7 +82,12 @@ def summarize(paths):
             for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors_op_write.sum",
                       "gpu__time_duration.sum"):
                 tot[f"{cat}:{m}"] = 0.0
+        cls = classes.setdefault(path, {})
         for d in per.values():
+            c = cls.setdefault(kernel_class(d["name"]), {"launches": 0, "dram_bytes": 0.0, "ns": 0.0})
+            c["launches"] += 1
+            c["dram_bytes"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+            c["ns"] += d.get("gpu__time_duration.sum", 0.0)
             cat = "conv" if any(k in d["name"] for k in CONV_KERNELS) else "other"
             for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors_op_write.sum",
                       "gpu__time_duration.sum"):
@@ -81,6 +105,14 @@ def summarize(paths):
             print(f"  {cat:5s} dram read {rd_ * gb:8.3f} GB  dram write {wr_ * gb:8.3f} GB  "
                   f"dram total {(rd_ + wr_) * gb:8.3f} GB  L2 writes {l2w * gb:8.3f} GB  "
                   f"kernel time {t:8.3f} ms")
+    if json_out:
+        import json
+        with open(json_out, "w") as f:
+            json.dump({"how": "ncu --profile-from-start off --cache-control none --clock-control none "
+                              "--metrics dram__bytes_read.sum,dram__bytes_write.sum,... over one captured "
+                              "D121 b64 step (tools/ncu_step_bytes.py)",
+                       "runs": {os.path.basename(k): v for k, v in classes.items()},
+                       "totals": {os.path.basename(k): v for k, v in out.items()}}, f, indent=1)
     return out
 
 
@@ -90,9 +122,10 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--summarize", nargs="*")
+    ap.add_argument("--json", default="")
     a = ap.parse_args()
     if a.summarize:
-        summarize(a.summarize)
+        summarize(a.summarize, a.json)
     else:
         run(a.level, a.dtype, a.batch)
 

@@ -279,6 +279,11 @@ int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in, int32_t k
 /* K12: multi-tensor SGD w -= lr*g over a flat fp32 buffer */
 int bnff_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
 
+/* debug: when buf != NULL (device memory, >= 16*1024 u64), window conv launches record a
+ * %globaltimer timeline of CTA 0 (producer issue, TMA landed, transform done, MMA issue /
+ * commit, epilogue per tile) into buf[event*1024 + index]; NULL turns it off.         */
+int bnff_debug_trace(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,7 +66,17 @@ struct WcParams {
   const __nv_bfloat16* ex; long long ex_rs;
   bnff_coef ecoef;
   float* stat_part;
+  unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
 };
+
+// event stamps of CTA 0 into p.trace[ev * 1024 + i] (debug builds of the timeline only)
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int ev, int i) {
+  if (tr != nullptr && blockIdx.x == 0 && i < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[ev * 1024 + i] = t;
+  }
+}
 
 __host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
 
@@ -168,6 +178,7 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 template <int BN, int RB, int TAPS, int MODE>
 __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_constant__ WcParams p) {
   griddep_launch();
+  if (threadIdx.x == 0) trace_ev(p.trace, 8, 0);
   using L = Layout<BN, RB, TAPS, MODE>;
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
@@ -270,6 +281,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) trace_ev(p.trace, 9, 0);
   const uint32_t tmem = tmem_sh;
 
   auto stage_a = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes; };
@@ -310,6 +322,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       }
       for (int s = 0; s < p.nslab; ++s) {
         mbar_wait(&ld_bar[st], ph);
+        if (tid == 0) trace_ev(p.trace, 2, it * p.nslab + s);
         const int cs = min(SLABW, p.ci - s * SLABW);
         if (need_t && j * 8 < cs) {
           const int c0 = s * SLABW + j * 8;
@@ -352,6 +365,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           fence_proxy_async_smem();
         }
         mbar_arrive(&full_bar[st]);
+        if (tid == 0) trace_ev(p.trace, 3, it * p.nslab + s);
         if (++st == ST) { st = 0; ph ^= 1u; }
       }
     }
@@ -369,7 +383,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         int img0 = 0, y0 = 0;
         if (TAPS == 9) tile_org(mt, img0, y0);
         for (int s = 0; s < p.nslab; ++s) {
+          trace_ev(p.trace, 0, it * p.nslab + s);
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
+          trace_ev(p.trace, 1, it * p.nslab + s);
           if (!L::WRES) {
             mbar_arrive_expect_tx(&full_bar[st], BN * RB);
             bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
@@ -405,6 +421,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         uint32_t acc = 0;
         for (int s = 0; s < p.nslab; ++s) {
           mbar_wait(&full_bar[st], ph);
+          trace_ev(p.trace, 4, it * p.nslab + s);
           tc_fence_after();
           const uint32_t abase = smem_u32(stage_a(st));
           const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB : smem_u32(stage_b(st));
@@ -425,6 +442,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             }
           }
           umma_commit(&empty_bar[st]);
+          trace_ev(p.trace, 5, it * p.nslab + s);
           if (++st == ST) { st = 0; ph ^= 1u; }
         }
         umma_commit(&accf_bar[buf]);
@@ -459,7 +477,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const bool fold = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC_ACC;  // out (+)= scale * dt1
     const bool fold_acc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC_ACC;
     const bool stats = do_stats && (MODE == M_FPROP || nrc);
-    const bool persist = p.ntiles == 1;      // same columns every tile: keep sums in registers
+    const bool persist = true;  // grid % ntiles == 0: a CTA's columns never change, sums stay in registers
     float2 acc1[MYCH], acc2[MYCH];
 #pragma unroll
     for (int k = 0; k < MYCH; ++k) { acc1[k] = make_float2(0.f, 0.f); acc2[k] = make_float2(0.f, 0.f); }
@@ -538,6 +556,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       if (MODE == M_DGRAD && fold_acc) named_bar_sync(bar_id, 128);  // gpix of every row for the prefetch
       const int pix = gpix[row];
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
+      if (et == 0) trace_ev(p.trace, 6, it);
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < MYCH; ++k) {
@@ -563,6 +582,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         }
         if (need_x) cp_async_wait<MYCH - 1>();
         const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
+        if (et == 0) trace_ev(p.trace, 10, it * 4 + k);
         // ---- row pass
 #pragma unroll
         for (int c16 = 0; c16 < CW; c16 += 16) {
@@ -603,8 +623,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         if (ci + 2 >= NCH) {
           tc_fence_before();
           mbar_arrive(&acce_bar[buf]);  // this group is done with the accumulator slot
+          if (et == 0) trace_ev(p.trace, 7, it);
         }
         named_bar_sync(bar_id, 128);
+        if (et == 0) trace_ev(p.trace, 11, it * 4 + k);
         // ---- column pass: sums of the stored values (FPROP: y, y^2; NRC: dt1, dt1*xhat)
         if (stats) {
           const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
@@ -635,6 +657,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           acc1[k] = a;
           acc2[k] = b;
         }
+        if (et == 0) trace_ev(p.trace, 12, it * 4 + k);
         // ---- store pass
         constexpr int CPO = CW / 8;  // 16B chunks per staged row
         if (MODE == M_DGRAD && fold) {
@@ -669,6 +692,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           }
         }
         named_bar_sync(bar_id, 128);  // staging, x buffer k and gpix free
+        if (et == 0) trace_ev(p.trace, 13, it * 4 + k);
         fetch_x(it + 1, k);            // recycle x buffer k for the next tile
         if (stats && !persist) flush(k, n0, cc);
       }
@@ -681,10 +705,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     }
     // both groups' sums are in sacc; write this CTA's partial row (one N tile)
     asm volatile("bar.sync 4, %0;" ::"n"(NEW * 32) : "memory");
-    if (do_stats && persist) {
-      for (int c = et; c < p.N; c += NEW * 32) {
-        p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + c] = sacc[c];
-        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + c] = sacc[BN + c];
+    if (do_stats && persist && ntl > 0) {
+      int mt0, n00;
+      tile_of(0, mt0, n00);
+      for (int c = et; c < BN; c += NEW * 32) {
+        if (n00 + c >= p.N) continue;
+        p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + n00 + c] = sacc[c];
+        p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + n00 + c] = sacc[BN + c];
       }
     }
   }
@@ -1334,7 +1361,10 @@ static int launch_t(WcParams p, cudaStream_t st) {
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(wconv)");
     attr = c.total;
   }
-  const int grid = p.tiles < num_sms_wc() ? p.tiles : num_sms_wc();
+  // a CTA's N tile must not change between its tiles (column sums stay in registers):
+  // the grid is a multiple of the N-tile count
+  int grid = p.tiles < num_sms_wc() ? p.tiles : num_sms_wc();
+  if (grid > p.ntiles) grid -= grid % p.ntiles;
   launch(kern, dim3(grid), dim3(WC_THREADS), c.total, st, p);
   return check_launch("wconv");
 }
@@ -1435,6 +1465,12 @@ extern "C" int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, in
   return BNFF_OK;
 }
 
+static unsigned long long* g_wc_trace = nullptr;
+extern "C" int bnff_debug_trace(void* buf) {
+  g_wc_trace = (unsigned long long*)buf;
+  return BNFF_OK;
+}
+
 // internal entry used by bnff_conv_fprop / bnff_conv_dgrad when bnff_window_ok()
 extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                                 int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
@@ -1509,6 +1545,7 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.ex = (const __nv_bfloat16*)ex.ptr; p.ex_rs = ex.row_stride;
   p.ecoef = ecoef;
   p.stat_part = stat_part;
+  p.trace = g_wc_trace;
   if (kh == 3 && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
   cudaStream_t st = (cudaStream_t)stream;
   if (mode == 0) {

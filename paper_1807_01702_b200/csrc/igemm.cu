@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
             }
             maskb |= (ok ? 1u : 0u) << i;
           }
-          meta_b[s * 128 + tid] = ((uint32_t)co << 8) | maskb;
+          meta_b[s * 128 + tid] = ((uint32_t)co << 16) | maskb;  // mask: B_PER <= 16 bits
         }
       }
       cp_async_commit();
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
           uint8_t* b1 = stage_b(s2, 1);
           uint8_t* xs = stage_x(s2);
           const uint32_t mb = MODE == MODE_WGRAD ? meta_b[s2 * 128 + tid] : 0u;
-          const int co = (int)(mb >> 8);
+          const int co = (int)(mb >> 16);
 #pragma unroll
           for (int i = 0; i < C::B_PER; ++i) {
             uint32_t off;

@@ -83,6 +83,17 @@ template <> struct Chunk<float> {
 };
 
 // operand prologue transforms (exact fp32 op order of the reference, no FMA contraction)
+// per-channel coefficients of a V-channel chunk as vector loads (c0 is a multiple of V;
+// every coefficient array is 16-byte aligned at such offsets)
+template <int V>
+__device__ __forceinline__ void ldv(const float* p, int c0, float (&o)[V]) {
+#pragma unroll
+  for (int i = 0; i < V; i += 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p + c0 + i));
+    o[i] = t.x; o[i + 1] = t.y; o[i + 2] = t.z; o[i + 3] = t.w;
+  }
+}
+
 template <int V>
 __device__ __forceinline__ void apply_pro(int pro, float (&f)[V], const float (&xf)[V], int c0,
                                           const bnff_coef& cf) {
@@ -90,17 +101,27 @@ __device__ __forceinline__ void apply_pro(int pro, float (&f)[V], const float (&
 #pragma unroll
     for (int i = 0; i < V; ++i) f[i] = fmaxf(f[i], 0.f);
   } else if (pro == BNFF_PRO_BN_RELU) {
+    float a[V], b[V], c[V];
+    ldv<V>(cf.a, c0, a);
+    ldv<V>(cf.b, c0, b);
+    ldv<V>(cf.c, c0, c);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      float t = __fmul_rn(__fsub_rn(f[i], __ldg(cf.a + c0 + i)), __ldg(cf.b + c0 + i));
-      f[i] = fmaxf(__fadd_rn(t, __ldg(cf.c + c0 + i)), 0.f);
+      float t = __fmul_rn(__fsub_rn(f[i], a[i]), b[i]);
+      f[i] = fmaxf(__fadd_rn(t, c[i]), 0.f);
     }
   } else if (pro == BNFF_PRO_BN_DX) {
+    float a[V], b[V], c[V], d[V], e[V];
+    ldv<V>(cf.a, c0, a);
+    ldv<V>(cf.b, c0, b);
+    ldv<V>(cf.c, c0, c);
+    ldv<V>(cf.d, c0, d);
+    ldv<V>(cf.e, c0, e);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      float xh = __fmul_rn(__fsub_rn(xf[i], __ldg(cf.a + c0 + i)), __ldg(cf.b + c0 + i));
-      float t = __fsub_rn(__fsub_rn(f[i], __ldg(cf.c + c0 + i)), __fmul_rn(xh, __ldg(cf.d + c0 + i)));
-      f[i] = __fmul_rn(__ldg(cf.e + c0 + i), t);
+      float xh = __fmul_rn(__fsub_rn(xf[i], a[i]), b[i]);
+      float t = __fsub_rn(__fsub_rn(f[i], c[i]), __fmul_rn(xh, d[i]));
+      f[i] = __fmul_rn(e[i], t);
     }
   }
 }

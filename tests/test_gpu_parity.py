@@ -338,3 +338,48 @@ def test_icf_block_gradient_fold_bf16():
             continue
         e = rel_l2(runs[True][1][k], v)
         assert e <= 1.5 * base[k] + 1e-3, f"{k}: folded {e:.3e} vs unfused {base[k]:.3e}"
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_padded_growth12_densenet(dtype):
+    """DenseNet with growth rate 12 (BASELINE C2's k) through graph.pad_channels on the
+    device: fp32 within 1e-4 of the fp64 oracle on the LOGICAL graph; bf16 within the
+    bf16 bars (output rel-L2 2e-2; gradients no worse than the unfused bf16 chain x1.5)."""
+    from paper_1807_01702_b200.engine import Engine
+    g0 = G.build_model(G.densenet_micro(2, (3, 3), 12), seed=0)
+    g2, pm = G.pad_channels(g0, 8)
+
+    def run(level):
+        ga, _ = fusion.plan(g0, fusion.parse_level(level))
+        gb, _ = fusion.plan(g2, fusion.parse_level(level))
+        rng = Rng(1)
+        x = rng.uniform(ga.slots[ga.inputs[0]].shape, -1.0, 1.0)
+        dy = rng.normal(ga.slots[ga.outputs[0]].shape)
+        res = OX.forward(ga, {ga.inputs[0]: x.astype(np.float64)})
+        ref = OX.backward(ga, res, {ga.outputs[0]: dy.astype(np.float64)})
+        eng = Engine(gb, dtype=dtype, input_grad=False)
+        eng.set_input(x)
+        eng.set_loss_grad(pm.pad(g2.outputs[0], dy, gb.slots[gb.outputs[0]].shape[1]))
+        eng.forward()
+        eng.backward()
+        torch.cuda.synchronize()
+        out = pm.unpad(g2.outputs[0], eng.output())
+        grads = pm.params_from(eng.param_grads())
+        return out, grads, res.vals[ga.outputs[0]], ref.params
+
+    if dtype == "f32":
+        for level in ("baseline", "bnff+icf"):
+            out, grads, ro, rp = run(level)
+            assert scaled(out, ro) < 1e-4
+            for k, v in rp.items():
+                if not k.endswith(".bias"):
+                    assert scaled(grads[k], v) < 1e-4, (level, k)
+        return
+    base = run("baseline")
+    fused = run("bnff+icf")
+    assert rel_l2(fused[0], fused[2]) < 2e-2
+    for k, v in fused[3].items():
+        if k.endswith(".bias"):
+            continue
+        eb, ef = rel_l2(base[1][k], v), rel_l2(fused[1][k], v)
+        assert ef <= 1.5 * eb + 1e-3, (k, ef, eb)

@@ -100,3 +100,31 @@ def test_parse_level_errors():
     assert fusion.parse_level("BNFF") is fusion.FusionLevel.BNFF
     with pytest.raises(InvalidSpecError):
         fusion.parse_level("nope")
+
+
+def test_pad_channels_is_exact_on_the_oracle():
+    """graph.pad_channels (k = 12 pieces widened to 16, transitions to multiples of 8):
+    the padded graph run by the oracle reproduces the logical graph's outputs bitwise and
+    its parameter gradients to fp32 summation-order noise, at every fusion level."""
+    import numpy as np
+    from oracle import executor as OX
+    from paper_1807_01702_b200 import fusion
+    from paper_1807_01702_b200.tensor import Rng
+    g0 = G.build_model(G.densenet_micro(2, (3, 3), 12), seed=0)
+    g2, pm = G.pad_channels(g0, 8)
+    assert all(c % 8 == 0 for c, _, _ in g2.buffer_groups.values())
+    for lvl in ("baseline", "bnff", "bnff+icf"):
+        ga, _ = fusion.plan(g0, fusion.parse_level(lvl))
+        gb, _ = fusion.plan(g2, fusion.parse_level(lvl))
+        rng = Rng(1)
+        x = rng.uniform(ga.slots[ga.inputs[0]].shape, -1.0, 1.0)
+        dy = rng.normal(ga.slots[ga.outputs[0]].shape)
+        ra = OX.forward(ga, {ga.inputs[0]: x})
+        ba = OX.backward(ga, ra, {ga.outputs[0]: dy})
+        dyp = pm.pad(g2.outputs[0], dy, gb.slots[gb.outputs[0]].shape[1])
+        rb = OX.forward(gb, {gb.inputs[0]: x})
+        bb = OX.backward(gb, rb, {gb.outputs[0]: dyp})
+        assert np.array_equal(ra.vals[ga.outputs[0]], pm.unpad(g2.outputs[0], rb.vals[gb.outputs[0]]))
+        pb = pm.params_from(bb.params)
+        for k, v in ba.params.items():
+            assert np.max(np.abs(pb[k] - v)) <= 1e-5 * max(float(np.max(np.abs(v))), 1.0), (lvl, k)

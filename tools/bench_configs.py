@@ -34,6 +34,8 @@ def build(name, level, dtype):
     from paper_1807_01702_b200 import fusion, graph as G
     spec, batch = spec_of(name)
     g0 = G.build_block(8, 64, 32, seed=0) if spec is None else G.build_model(spec, seed=0)
+    if name == "c2":  # k = 12 pieces: widened to 16-byte channel multiples (graph.pad_channels)
+        g0, _ = G.pad_channels(g0, 8)
     g, _ = fusion.plan(g0, fusion.parse_level(level))
     return g, batch
 
@@ -114,6 +116,8 @@ def main():
             ms, nb, fl, nl = device_ms(g, dtype, a.steps, a.warmup)
         gu, _ = build(name, "baseline", dtype)
         ums, unb, _, _ = device_ms(gu, dtype, a.steps, a.warmup)
+        if name == "c2":
+            note = "growth-rate-12 pieces padded to 16 channels (graph.pad_channels; exact zeros)"
         line = {"config": name, "level": fused_level, "dtype": dtype, "note": note, "batch": batch,
                 "ms_per_step": round(ms, 4), "images_per_s": round(batch / (ms * 1e-3), 1),
                 "unfused_ms_per_step": round(ums, 4), "speedup_vs_unfused": round(ums / ms, 3),

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python tools/bench_configs.py --only c4 > gpurun_out/configs_c4.jsonl 2> gpurun_out/configs.err; cat gpurun_out/configs_c4.jsonl; tail -5 gpurun_out/configs.err
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep -E "^E  " gpurun_out/pytest_gpu.log | head
+timeout 1500 python tools/bench_configs.py > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; cat gpurun_out/configs.jsonl; tail -3 gpurun_out/configs.err

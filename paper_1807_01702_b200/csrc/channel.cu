@@ -797,6 +797,25 @@ __global__ void nchw_to_nhwc_kernel(const float* src, long long n, long long c, 
   }
 }
 
+// one thread per pixel when the stored pixel is exactly 16 bytes (8 bf16 / 4 f32): the
+// c planes are read coalesced across consecutive pixels, one vector store per pixel
+template <typename T>
+__global__ void nchw_to_nhwc_px16_kernel(const float* __restrict__ src, long long n, int c, long long hw,
+                                         View d) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int V = 16 / sizeof(T);
+  const long long total = n * hw;
+  for (long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x; pix < total;
+       pix += (long long)gridDim.x * blockDim.x) {
+    const long long img = pix / hw, rem = pix - img * hw;
+    float f[V];
+#pragma unroll
+    for (int ch = 0; ch < V; ++ch) f[ch] = ch < c ? __ldg(src + (img * c + ch) * hw + rem) : 0.f;
+    VecIO<T>::store(const_cast<void*>(d.p), pix * d.rs, f);
+  }
+}
+
 template <typename T>
 __global__ void nhwc_to_nchw_kernel(View s, long long n, long long c, long long h, long long w, float* dst) {
   griddep_launch();
@@ -1099,6 +1118,12 @@ extern "C" int bnff_copy(int32_t dtype, bnff_view src, bnff_view dst, void* stre
 extern "C" int bnff_nchw_to_nhwc(int32_t dtype, const float* src, int64_t n, int64_t c, int64_t h, int64_t w,
                                  bnff_view dst, void* stream) {
   if (dst.c < c || dst.n != n || dst.h != h || dst.w != w) return set_error(BNFF_ERR_SHAPE, "nchw_to_nhwc dims");
+  const int vec = dtype == BNFF_BF16 ? 8 : 4;
+  if (dst.c == vec && dst.row_stride % vec == 0) {  // the channel-padded image: 16-byte pixels
+    BNFF_DISPATCH(dtype, nchw_to_nhwc_px16_kernel, grid_for(n * h * w), 256, 0, (cudaStream_t)stream, src, n,
+                  (int)c, h * w, vw(dst));
+    return check_launch("nchw_to_nhwc");
+  }
   BNFF_DISPATCH(dtype, nchw_to_nhwc_kernel, grid_for(n * h * w * dst.c), 256, 0, (cudaStream_t)stream, src, n,
                 c, h, w, vw(dst), (int)dst.c);
   return check_launch("nchw_to_nhwc");

@@ -60,6 +60,8 @@ def main():
         return e0.elapsed_time(e1) / args.reps
 
     full = time_graph(thunks)
+    print(f"# phases: forward {time_graph(list(eng.fwd)):.3f} ms, backward {time_graph(list(eng.bwd)):.3f} ms, "
+          f"optimizer {time_graph(list(eng.opt) + list(eng.repack)):.3f} ms")
     print(f"# {args.model} b{args.batch} {args.level}: full graph {full:.3f} ms/step, {len(thunks)} calls")
     rows = []
     for k in kinds:

@@ -94,6 +94,39 @@ __device__ __forceinline__ void ldv(const float* p, int c0, float (&o)[V]) {
   }
 }
 
+// the per-channel coefficients of one V-channel chunk, loaded once per stage by a thread
+// whose chunk column is fixed for the whole stage
+template <int V>
+struct ProCoef {
+  float a[V], b[V], c[V], d[V], e[V];
+  __device__ __forceinline__ void load(int pro, int c0, const bnff_coef& cf) {
+    if (pro == BNFF_PRO_BN_RELU || pro == BNFF_PRO_BN_DX) {
+      ldv<V>(cf.a, c0, a);
+      ldv<V>(cf.b, c0, b);
+      ldv<V>(cf.c, c0, c);
+    }
+    if (pro == BNFF_PRO_BN_DX) {
+      ldv<V>(cf.d, c0, d);
+      ldv<V>(cf.e, c0, e);
+    }
+  }
+  __device__ __forceinline__ void apply(int pro, float (&f)[V], const float (&xf)[V]) const {
+    if (pro == BNFF_PRO_RELU) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) f[i] = fmaxf(f[i], 0.f);
+    } else if (pro == BNFF_PRO_BN_RELU) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) f[i] = fmaxf(__fadd_rn(__fmul_rn(__fsub_rn(f[i], a[i]), b[i]), c[i]), 0.f);
+    } else if (pro == BNFF_PRO_BN_DX) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float xh = __fmul_rn(__fsub_rn(xf[i], a[i]), b[i]);
+        f[i] = __fmul_rn(e[i], __fsub_rn(__fsub_rn(f[i], c[i]), __fmul_rn(xh, d[i])));
+      }
+    }
+  }
+};
+
 template <int V>
 __device__ __forceinline__ void apply_pro(int pro, float (&f)[V], const float (&xf)[V], int c0,
                                           const bnff_coef& cf) {
@@ -422,6 +455,8 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
           uint8_t* a0 = stage_a(s2, 0);
           uint8_t* a1 = stage_a(s2, 1);
           uint8_t* xs = stage_x(s2);
+          ProCoef<V> pca;
+          if (ma & 0xFFu) pca.load(p.a_pro, cc, p.a_coef);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             uint32_t off;
@@ -435,7 +470,7 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
               cx.raw = *reinterpret_cast<const decltype(cx.raw)*>(xs + off);
               cx.to_float(xf);
             }
-            if ((ma >> i) & 1u) apply_pro<V>(p.a_pro, f, xf, cc, p.a_coef);
+            if ((ma >> i) & 1u) pca.apply(p.a_pro, f, xf);
             st_chunk<T, V>(a0, a1, off, f);
           }
         }
@@ -445,6 +480,8 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
           uint8_t* xs = stage_x(s2);
           const uint32_t mb = MODE == MODE_WGRAD ? meta_b[s2 * 128 + tid] : 0u;
           const int co = (int)(mb >> 16);
+          ProCoef<V> pcb;
+          if (MODE == MODE_WGRAD && (mb & 0xFFFFu)) pcb.load(p.b_pro, co, p.b_coef);
 #pragma unroll
           for (int i = 0; i < C::B_PER; ++i) {
             uint32_t off;
@@ -459,7 +496,7 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
                 cx.raw = *reinterpret_cast<const decltype(cx.raw)*>(xs + off);
                 cx.to_float(xf);
               }
-              apply_pro<V>(p.b_pro, f, xf, co, p.b_coef);
+              pcb.apply(p.b_pro, f, xf);
             }
             st_chunk<T, V>(b0, b1, off, f);
           }

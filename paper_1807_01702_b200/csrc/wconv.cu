@@ -80,13 +80,44 @@ __device__ __forceinline__ void trace_ev(unsigned long long* tr, int ev, int i) 
 
 __host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
 
-template <int BN, int RB, int TAPS, int MODE>
+// GEMM N tile for an output-channel count
+__host__ __device__ inline int pick_bn(int N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
+__host__ __device__ inline int pick_rb(int CI) { return CI <= 32 ? 64 : 128; }
+
+struct Geo {
+  int taps, RB, BN, ntiles, npad, nslab, sw;
+};
+// dgrad N tiles are capped at 128 columns: the NRC epilogue keeps a whole x tile in flight.
+// 3x3 weights stay resident in shared memory when they fit (<= 96 KB, one N tile); wider
+// 3x3 convs (ResNet's 128..512 channels) stream the 9 taps of each slab with the stage
+// (sw = 1), in 64-column N tiles.
+__host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
+  Geo g{};
+  g.taps = kh * kw;
+  // 3x3: 64-byte slabs (32 channels) -> small window stages, deep prefetch beside the
+  // resident weights
+  g.RB = (CI <= 32 || g.taps == 9) ? 64 : pick_rb(CI);
+  g.BN = pick_bn(N);
+  if (dgrad && g.BN > 128) g.BN = 128;
+  g.nslab = (CI + g.RB / 2 - 1) / (g.RB / 2);
+  g.ntiles = (N + g.BN - 1) / g.BN;
+  if (g.taps == 9 && (g.ntiles > 1 || g.nslab * 9 * g.BN * g.RB > 96 * 1024)) {
+    g.sw = 1;
+    g.BN = 64;
+    g.ntiles = (N + g.BN - 1) / g.BN;
+  }
+  g.npad = g.ntiles * g.BN;
+  return g;
+}
+
+
+template <int BN, int RB, int TAPS, int MODE, bool SW = false>
 struct Layout {
   static constexpr int SLABW = RB / 2;               // channels per slab row
   static constexpr int CPR = RB / 16;                // 16B chunks per row
   static constexpr int RS = LT / CPR;                // loader row step
   static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
-  static constexpr bool WRES = TAPS == 9;            // weights resident in smem
+  static constexpr bool WRES = TAPS == 9 && !SW;     // weights resident in smem (else streamed per stage)
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
   static constexpr int CW = BN <= 32 ? 16 : (MODE == M_DGRAD || BN == 64 ? 32 : 64);
@@ -106,15 +137,15 @@ struct Carve {
   int wres, stage0, stage_bytes, a_bytes, stg, ptab, etab, sacc, red, rowtab, rowpix, meta, total;
 };
 
-template <int BN, int RB, int TAPS, int MODE>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false>
 __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop) {
-  using L = Layout<BN, RB, TAPS, MODE>;
+  using L = Layout<BN, RB, TAPS, MODE, SW>;
   Carve c{};
   int off = 0;
   c.wres = off;
   if (L::WRES) off += align_up(nslab * TAPS * BN * RB, 1024);
   c.a_bytes = align_up(R * RB, 1024);
-  c.stage_bytes = c.a_bytes * (xop ? 2 : 1) + (L::WRES ? 0 : BN * RB);
+  c.stage_bytes = c.a_bytes * (xop ? 2 : 1) + (L::WRES ? 0 : TAPS * BN * RB);
   c.stage0 = off;
   off += stages * c.stage_bytes;
   c.stg = off;
@@ -175,11 +206,11 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
   }
 }
 
-template <int BN, int RB, int TAPS, int MODE>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false>
 __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_constant__ WcParams p) {
   griddep_launch();
   if (threadIdx.x == 0) trace_ev(p.trace, 8, 0);
-  using L = Layout<BN, RB, TAPS, MODE>;
+  using L = Layout<BN, RB, TAPS, MODE, SW>;
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
@@ -187,7 +218,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar;
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
-  const Carve cv = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, p.stages, xop_s);
+  const Carve cv = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, p.stages, xop_s);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* etab = reinterpret_cast<float*>(smem + cv.etab);
@@ -386,10 +417,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           trace_ev(p.trace, 0, it * p.nslab + s);
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
           trace_ev(p.trace, 1, it * p.nslab + s);
-          if (!L::WRES) {
-            mbar_arrive_expect_tx(&full_bar[st], BN * RB);
-            bulk_g2s(smem_u32(stage_b(st)), p.wpk + ((long long)s * p.npad + n0) * RB, BN * RB,
-                     &full_bar[st]);
+          if (!L::WRES) {  // this slab's weights for the N tile, every tap ([slab][tap][npad][RB] pack)
+            mbar_arrive_expect_tx(&full_bar[st], TAPS * BN * RB);
+#pragma unroll 1
+            for (int u = 0; u < TAPS; ++u)
+              bulk_g2s(smem_u32(stage_b(st)) + u * BN * RB,
+                       p.wpk + ((long long)(s * TAPS + u) * p.npad + n0) * RB, BN * RB, &full_bar[st]);
           }
           mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
           const int c = s * SLABW;
@@ -1267,10 +1300,8 @@ __global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs)
   if (!out) return;
   const int CI = d ? jb.c_out : jb.c_in, N = d ? jb.c_in : jb.c_out;
   const int taps = jb.kh * jb.kw;
-  const int RB = (CI <= 32 || taps == 9) ? 64 : 128;
-  int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
-  if (d && BN > 128) BN = 128;
-  const int npad = (N + BN - 1) / BN * BN;
+  const Geo gg = geo(CI, N, jb.kh, jb.kw, d);  // the layout the conv kernels read
+  const int RB = gg.RB, npad = gg.npad;
   const int slabw = RB / 2;
   const int nslab = (CI + slabw - 1) / slabw;
   // one thread per 16-byte chunk (8 consecutive reduction channels of one row n):
@@ -1321,36 +1352,14 @@ int num_sms_wc() {
   return n;
 }
 
-// GEMM N tile for an output-channel count
-inline int pick_bn(int N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
-inline int pick_rb(int CI) { return CI <= 32 ? 64 : 128; }
-
-struct Geo {
-  int taps, RB, BN, ntiles, npad, nslab;
-};
-// dgrad N tiles are capped at 128 columns: the NRC epilogue keeps a whole x tile in flight
-inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
-  Geo g{};
-  g.taps = kh * kw;
-  // 3x3: 64-byte slabs (32 channels) -> small window stages, deep prefetch beside the
-  // resident weights
-  g.RB = (CI <= 32 || g.taps == 9) ? 64 : pick_rb(CI);
-  g.BN = pick_bn(N);
-  if (dgrad && g.BN > 128) g.BN = 128;
-  g.ntiles = (N + g.BN - 1) / g.BN;
-  g.npad = g.ntiles * g.BN;
-  g.nslab = (CI + g.RB / 2 - 1) / (g.RB / 2);
-  return g;
-}
-
-template <int BN, int RB, int TAPS, int MODE>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false>
 static int launch_t(WcParams p, cudaStream_t st) {
-  auto kern = wconv_kernel<BN, RB, TAPS, MODE>;
+  auto kern = wconv_kernel<BN, RB, TAPS, MODE, SW>;
   int stages = 8;
   Carve c{};
   const bool xop = MODE == M_DGRAD && p.pro == BNFF_PRO_BN_DX;
   for (; stages >= 2; --stages) {
-    c = carve<BN, RB, TAPS, MODE>(p.R, p.nslab, p.npad, stages, xop);
+    c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop);
     if (c.total <= SMEM_BUDGET) break;
   }
   if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
@@ -1370,7 +1379,8 @@ static int launch_t(WcParams p, cudaStream_t st) {
 }
 
 template <int MODE, int TAPS>
-static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st) {
+static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st, int sw = 0) {
+  if (TAPS == 9 && sw) return launch_t<64, 64, TAPS, MODE, true>(p, st);
   if (RB == 64) {
     switch (BN) {
       case 32: return launch_t<32, 64, TAPS, MODE>(p, st);
@@ -1395,9 +1405,13 @@ using namespace bnff;
 namespace bnff {
 namespace wc {
 template <int MODE, int TAPS>
-static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop) {
+static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw = 0) {
   Carve c{};
 #define BNFF_FIT(bn, rb) c = carve<bn, rb, TAPS, MODE>(R, nslab, npad, 2, xop)
+  if (TAPS == 9 && sw) {
+    c = carve<64, 64, TAPS, MODE, true>(R, nslab, npad, 2, xop);
+    return c.total <= SMEM_BUDGET;
+  }
   if (RB == 64) {
     if (BN == 32) BNFF_FIT(32, 64); else if (BN == 64) BNFF_FIT(64, 64);
     else if (BN == 128) BNFF_FIT(128, 64); else BNFF_FIT(256, 64);
@@ -1421,16 +1435,14 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
   if (kh == 3) {
     const int wp = w + 2;
     if (128 + 2 * wp + 2 > wc::RMAX) return 0;
-    // resident weights need a single N tile for both passes
-    if (c_out > 256 || c_in > 256) return 0;
   }
   (void)h;
   const int R = 128 + (kh == 3 ? 2 * (w + 2) + 2 : 0);
   for (int d = 0; d < 2; ++d) {
     const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
     const wc::Geo g = wc::geo(CI, N, kh, kw, d);
-    const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true)
-                                 : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false))
+    const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, g.sw)
+                                 : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, g.sw))
                             : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
                                  : wc::fits2<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false));
     if (!ok) return 0;
@@ -1546,13 +1558,13 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.ecoef = ecoef;
   p.stat_part = stat_part;
   p.trace = g_wc_trace;
-  if (kh == 3 && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
+  if (kh == 3 && !g.sw && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
   cudaStream_t st = (cudaStream_t)stream;
   if (mode == 0) {
-    return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st)
+    return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st, g.sw)
                    : wc::dispatch<wc::M_FPROP, 1>(p, g.BN, g.RB, st);
   }
-  return kh == 3 ? wc::dispatch<wc::M_DGRAD, 9>(p, g.BN, g.RB, st)
+  return kh == 3 ? wc::dispatch<wc::M_DGRAD, 9>(p, g.BN, g.RB, st, g.sw)
                  : wc::dispatch<wc::M_DGRAD, 1>(p, g.BN, g.RB, st);
 }
 

@@ -182,6 +182,11 @@ def main():
         (2, 12, 32, 64, 3, "dgrad", P.PRO_BN_DX, P.DG_NRC),
         (3, 11, 96, 128, 1, "dgrad", P.PRO_BN_DX, P.DG_NRC),
         (1, 30, 64, 32, 3, "fprop", P.PRO_RELU, 0),
+        # 3x3 with streamed weights (ResNet widths: 9 taps of each slab ride with the stage)
+        (2, 14, 256, 256, 3, "fprop", P.PRO_BN_RELU, 0),
+        (2, 12, 128, 128, 3, "dgrad", P.PRO_BN_DX, P.DG_NRC),
+        (3, 7, 512, 512, 3, "dgrad", P.PRO_NONE, P.DG_CLIP),
+        (2, 14, 256, 256, 3, "wgrad", P.PRO_BN_RELU, 1),
     ]
     cases += [
         (2, 9, 128, 32, 3, "wgrad", P.PRO_BN_RELU, 0),

@@ -50,8 +50,9 @@ def kernel_class(name: str) -> str:
     if "wgrad_kernel" in name or "wg_reduce_kernel" in name or "wgrad_reduce_kernel" in name \
             or "igemm_kernel<2" in name or "igemm_kernel<(int)2" in name:
         return "wgrad"
-    if "wconv_kernel" in name:
-        return "dgrad" if name.split("(")[0].rstrip("> ").endswith("1") else "fprop"
+    if "wconv_kernel" in name:  # template <BN, RB, TAPS, MODE[, SW]>: MODE 1 = dgrad
+        args = name.split("<", 1)[1].split(">", 1)[0].split(",")
+        return "dgrad" if args[3].strip().endswith("1") else "fprop"
     if "igemm_kernel<1" in name or "igemm_kernel<(int)1" in name:
         return "dgrad"
     if "igemm_kernel" in name:

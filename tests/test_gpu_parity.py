@@ -383,3 +383,21 @@ def test_padded_growth12_densenet(dtype):
             continue
         eb, ef = rel_l2(base[1][k], v), rel_l2(fused[1][k], v)
         assert ef <= 1.5 * eb + 1e-3, (k, ef, eb)
+
+
+def test_cli_bench_csv(tmp_path):
+    """`python -m paper_1807_01702_b200.cli bench` writes rows the reference's
+    read_bench_csv (cli.py:113-125) accepts: frozen header, typed columns, three passes per
+    level, one checksum per level (bitwise-identical outputs across the two timed passes)."""
+    import csv
+    from paper_1807_01702_b200 import cli
+    out = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--model", "densenet-micro", "--batch", "4", "--fusion",
+                     "baseline,bnff+icf", "--iters", "2", "--warmup", "1", "--out", str(out)]) == 0
+    rows = list(csv.DictReader(open(out, newline="")))
+    assert list(rows[0].keys()) == cli.BENCH_HEADER
+    assert [r["pass"] for r in rows] == ["forward", "backward", "total"] * 2
+    for r in rows:
+        float(r["median_ms"]), float(r["mean_ms"]), float(r["std_ms"])
+        int(r["iters"]), int(r["traffic_bytes"]), int(r["threads"])
+    assert float(rows[5]["speedup_vs_baseline"]) > 0

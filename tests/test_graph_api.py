@@ -128,3 +128,22 @@ def test_pad_channels_is_exact_on_the_oracle():
         pb = pm.params_from(bb.params)
         for k, v in ba.params.items():
             assert np.max(np.abs(pb[k] - v)) <= 1e-5 * max(float(np.max(np.abs(v))), 1.0), (lvl, k)
+
+
+def test_cli_bench_schema_matches_reference():
+    """The device bench writes the reference's frozen CSV schema (cli.py:109-110) and
+    accepts its flags (cli.py:294-317)."""
+    import importlib.util
+    import os
+    from paper_1807_01702_b200 import cli
+    ref = "/root/reference/pkg/src/bnfuse/cli.py"
+    if os.path.exists(ref):
+        src = open(ref).read()
+        start = src.index("BENCH_HEADER = [")
+        header = eval(src[start + len("BENCH_HEADER = "):src.index("]", start) + 1])  # noqa: S307
+        assert cli.BENCH_HEADER == header
+    a = cli.make_parser().parse_args(["bench", "--model", "densenet-micro", "--batch", "4", "--fusion",
+                                      "all", "--iters", "3", "--warmup", "1", "--seed", "2", "--out",
+                                      "x.csv", "--dtype", "f32", "--gpus", "1"])
+    assert (a.model, a.batch, a.iterations, a.warmup, a.seed, a.out_path) == ("densenet-micro", 4, 3, 1, 2, "x.csv")
+    assert importlib.util.find_spec("paper_1807_01702_b200.cli") is not None

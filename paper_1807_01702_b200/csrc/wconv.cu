@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
           float2 a = acc1[k], b = acc2[k];
           if (MODE == M_FPROP) {
-#pragma unroll 4
+#pragma unroll 16
             for (int r = rg; r < 128; r += RG) {
               const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
               const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             const int gc = n0 + cc + 2 * cp;
             const float2 hinv = make_float2(etab[2 * p.npad + gc], etab[2 * p.npad + gc + 1]);
             const float2 hsh = make_float2(etab[3 * p.npad + gc], etab[3 * p.npad + gc + 1]);
-#pragma unroll 4
+#pragma unroll 16
             for (int r = rg; r < 128; r += RG) {
               const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
               const uint32_t xw = x32[r * (L::SROWB / 4) + cp];

@@ -14,7 +14,8 @@ import os
 from .errors import EngineError, ShapeError, StateError, UnsupportedError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbnff.so")
+# BNFF_LIB selects another build of the same ABI (A/B timing of kernel variants on one box)
+LIB_PATH = os.environ.get("BNFF_LIB") or os.path.join(_HERE, "libbnff.so")
 
 F32, BF16 = 0, 1
 PRO_NONE, PRO_RELU, PRO_BN_RELU, PRO_BN_DX = 0, 1, 2, 3

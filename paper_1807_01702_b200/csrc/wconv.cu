@@ -120,7 +120,7 @@ struct Layout {
   static constexpr bool WRES = TAPS == 9 && !SW;     // weights resident in smem (else streamed per stage)
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
-  static constexpr int CW = BN <= 32 ? 16 : (MODE == M_DGRAD || BN == 64 ? 32 : 64);
+  static constexpr int CW = BN <= 32 ? 16 : (BN == 64 ? 32 : 64);
   static constexpr int NCH = BN / CW;                // chunks per tile (>= 2)
   static constexpr int MYCH = (NCH + 1) / 2;         // chunks per epilogue group
   static constexpr int SROWB = CW * 2 + 16;          // staging row pitch (bytes)
@@ -596,11 +596,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         const int ci = grp + 2 * k;
         if (ci >= NCH) break;
         const int cc = ci * CW;
-        uint4 gold[4];
+        uint4 gold[CW / 8];
         if (MODE == M_DGRAD && fold_acc) {  // prefetch the old block-gradient chunks this thread stores
           constexpr int CPO = CW / 8;
 #pragma unroll
-          for (int i = 0; i < CPO && i < 4; ++i) {
+          for (int i = 0; i < CPO; ++i) {
             const int kk = gt + 128 * i;
             const int r = kk / CPO, ch = kk - r * CPO;
             const int px = gpix[r];
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) gold[i] = make_uint4(0, 0, 0, 0);
+          for (int i = 0; i < CW / 8; ++i) gold[i] = make_uint4(0, 0, 0, 0);
         }
         if (need_x) cp_async_wait<MYCH - 1>();
         const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           // block-gradient fold: out = (acc ? out : 0) + scale * dt1; the old block-gradient
           // chunks were fetched into registers before the row pass (their latency hides there)
 #pragma unroll
-          for (int i = 0; i < CPO && i < 4; ++i) {
+          for (int i = 0; i < CPO; ++i) {
             const int kk = gt + 128 * i;
             const int r = kk / CPO, ch = kk - r * CPO;
             const int px = gpix[r];

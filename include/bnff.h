@@ -204,6 +204,14 @@ int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count
 int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
                    const float* beta, float eps, float* mean32, float* scale32, float* beta32,
                    float* inv32, void* stream);
+/* bnff_stats_finalize of a freshly produced piece (channels [c_off, c_off+c_new) of c_total)
+ * fused with the consumer's bnff_bn_coeffs over all c_total channels (the other channels'
+ * mean/var are read from mean_all/var_all): one launch per ICF concatenation step.        */
+int bnff_stats_finalize_coeffs(const float* part, int32_t tiles, int32_t c_new, int64_t count,
+                               double* sum, double* sumsq, double* mean, double* var, int32_t c_off,
+                               int32_t c_total, const double* mean_all, const double* var_all,
+                               const float* gamma, const float* beta, float eps, float* mean32,
+                               float* scale32, float* beta32, float* inv32, void* stream);
 /* backward coefficient table from the reduced (dgamma, dbeta) sums:
  * k1 = dbeta/m, k2 = dgamma/m, g = gamma*invstd (ops.py:287-293). Also writes
  * the fp32 parameter gradients dgamma32/dbeta32 (nullable). */

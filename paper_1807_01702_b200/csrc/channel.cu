@@ -116,6 +116,43 @@ __global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __rest
   }
 }
 
+// stats_finalize of one freshly produced piece (channels [c_off, c_off + c_new) of a block)
+// fused with the next consumer's bn_coeffs over all c_total channels (ICF: concat_stats +
+// ChannelStats.from_sums + inv_std, ops.py:109-143; one launch instead of two)
+__global__ void __launch_bounds__(512) finalize_coeffs_kernel(
+    const float* __restrict__ part, int tiles, int c_new, long long count, double* sum, double* sumsq,
+    double* mean, double* var, int c_off, int c_total, const double* mean_all, const double* var_all,
+    const float* gamma, const float* beta, float eps, float* mean32, float* scale32, float* beta32,
+    float* inv32) {
+  griddep_launch();
+  griddep_wait();
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int cl = (c >= c_off && c < c_off + c_new) ? c - c_off : c_new;  // piece column or none
+  double s1, s2;
+  reduce_two(part, tiles, c_new, cl, s1, s2);
+  if ((threadIdx.x >> 5) == 0 && c < c_total) {
+    double m, v;
+    if (cl < c_new) {  // ChannelStats.from_sums (ops.py:109-113): population var, clamped
+      sum[cl] = s1;
+      sumsq[cl] = s2;
+      m = s1 / (double)count;
+      v = s2 / (double)count - m * m;
+      v = v > 0.0 ? v : 0.0;
+      mean[cl] = m;
+      var[cl] = v;
+    } else {
+      m = mean_all[c];
+      v = var_all[c];
+    }
+    const double vv = v > 0.0 ? v : 0.0;
+    const double inv = 1.0 / sqrt(vv + (double)eps);
+    mean32[c] = (float)m;
+    if (scale32) scale32[c] = (float)((double)gamma[c] * inv);
+    if (beta32) beta32[c] = beta[c];
+    if (inv32) inv32[c] = (float)inv;
+  }
+}
+
 __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
     const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
     const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
@@ -968,6 +1005,19 @@ extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, in
   // var = sum(d^2) / count, as ops.py:227 divides the centred sum by the count
   launch(scale_kernel, dim3((c + 127) / 128), dim3(128), 0, st, var, c, 1.0 / (double)count);
   return check_launch("var_finalize");
+}
+
+extern "C" int bnff_stats_finalize_coeffs(const float* part, int32_t tiles, int32_t c_new, int64_t count,
+                                          double* sum, double* sumsq, double* mean, double* var,
+                                          int32_t c_off, int32_t c_total, const double* mean_all,
+                                          const double* var_all, const float* gamma, const float* beta,
+                                          float eps, float* mean32, float* scale32, float* beta32,
+                                          float* inv32, void* stream) {
+  if (c_off < 0 || c_new < 0 || c_off + c_new > c_total) return set_error(BNFF_ERR_SHAPE, "finalize_coeffs: piece range");
+  launch(finalize_coeffs_kernel, dim3((c_total + 31) / 32), dim3(512), 0, (cudaStream_t)stream, part, tiles, c_new,
+         (long long)count, sum, sumsq, mean, var, c_off, c_total, mean_all, var_all, gamma, beta, eps, mean32,
+         scale32, beta32, inv32);
+  return check_launch("stats_finalize_coeffs");
 }
 
 extern "C" int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,

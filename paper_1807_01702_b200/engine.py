@@ -159,6 +159,8 @@ class Engine:
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window) and self.dcode == _lib.BF16
         self.side_wgrad = bool(side_wgrad)
+        import os
+        self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
         # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
         # into the block gradient buffer; the per-channel remainder rides in (A, B) arrays
         self.fold_icf = bool(fold_icf) and self.dcode == _lib.BF16
@@ -297,8 +299,11 @@ class Engine:
 
     def _emit_stats_finalize(self, part, tiles, c, count, st: Stats):
         if not self.sync_bn:
-            self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
-                       _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize")
+            # deferred: the next consumer's coefficient table launch finalizes it in the same
+            # kernel (bnff_stats_finalize_coeffs); anything else flushes it first
+            self._pending_fin.append((part, tiles, c, count, st))
+            if not self.fuse_finalize:
+                self._flush_pending()
             return
         # SyncBN: local float64 sums -> all-reduce -> moments over the global count
         self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
@@ -327,15 +332,44 @@ class Engine:
         wp = self.wpacks.get(conv.name)
         return 0 if wp is None else _ptr(wp[which])
 
+    def _flush_pending(self, keep=None):
+        """Emit the deferred statistics finalisations (all but `keep`)."""
+        rest = []
+        for pf in self._pending_fin:
+            if pf is keep:
+                rest.append(pf)
+                continue
+            part, tiles, c, count, st = pf
+            self._emit(self.L.bnff_stats_finalize, _ptr(part), tiles, c, count, _ptr(st.sum),
+                       _ptr(st.sumsq), _ptr(st.mean), _ptr(st.var), what="stats_finalize")
+        self._pending_fin = rest
+
     def _bn_tables(self, st: Stats, bn, tag):
-        """fp32 (mean, scale, beta, inv) for a normalize prologue (bn_fwd ops.py:246-249)."""
+        """fp32 (mean, scale, beta, inv) for a normalize prologue (bn_fwd ops.py:246-249).
+        A pending finalisation of a piece inside `st` (the channels a producer just wrote)
+        is fused into the same launch."""
         c = st.mean.shape[0]
         mean32, scale32, beta32, inv32 = (self._zeros((c,), torch.float32) for _ in range(4))
         gam = self.param(f"{bn.name}.gamma")
         bet = self.param(f"{bn.name}.beta")
-        self._emit(self.L.bnff_bn_coeffs, c, _ptr(st.mean), _ptr(st.var), _ptr(gam), _ptr(bet),
-                   C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32), _ptr(inv32),
-                   what=f"bn_coeffs {tag}")
+        lo = st.mean.data_ptr()
+        hi = lo + 8 * c
+        inside = [pf for pf in self._pending_fin
+                  if lo <= pf[4].mean.data_ptr() and pf[4].mean.data_ptr() + 8 * pf[2] <= hi]
+        merge = inside[-1] if inside else None
+        self._flush_pending(keep=merge)
+        if merge is None:
+            self._emit(self.L.bnff_bn_coeffs, c, _ptr(st.mean), _ptr(st.var), _ptr(gam), _ptr(bet),
+                       C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32), _ptr(inv32),
+                       what=f"bn_coeffs {tag}")
+            return mean32, scale32, beta32, inv32
+        self._pending_fin = []
+        part, tiles, cn, count, ps = merge
+        off = (ps.mean.data_ptr() - lo) // 8
+        self._emit(self.L.bnff_stats_finalize_coeffs, _ptr(part), tiles, cn, count, _ptr(ps.sum),
+                   _ptr(ps.sumsq), _ptr(ps.mean), _ptr(ps.var), off, c, _ptr(st.mean), _ptr(st.var),
+                   _ptr(gam), _ptr(bet), C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32),
+                   _ptr(inv32), what=f"bn_coeffs {tag}")
         return mean32, scale32, beta32, inv32
 
     def _channel_stats(self, x: torch.Tensor, st: Stats, tag):
@@ -349,6 +383,7 @@ class Engine:
     # ---------------------------------------------------------------- forward
     def _compile_forward(self):
         self._cur = self.fwd
+        self._pending_fin = []
         self.node_stats: dict = {}   # BN node id -> Stats (two/one-pass, baseline)
         self.node_tables: dict = {}  # node id -> fp32 tables
         self.stats: dict = {}        # stats slot id -> Stats
@@ -357,6 +392,7 @@ class Engine:
                 getattr(self, "_f_" + node.kind)(node)
             except ShapeError as e:
                 raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
+        self._flush_pending()
         self.launch_counts["fwd"] = len(self.fwd)
 
     def _col_conv(self, conv, x):
@@ -429,6 +465,7 @@ class Engine:
         st = Stats(*(self._zeros((c,), torch.float64) for _ in range(4)), count=pixels)
         self._channel_stats(x, st, node.name)
         if not node.attrs.onepass:  # two-pass: centred variance overwrites var (ops.py:226-227)
+            self._flush_pending()  # the centred pass reads the mean
             tiles = self.L.bnff_sum_tiles(pixels)
             part = self._empty((tiles, 2, c), torch.float32)
             self._emit(self.L.bnff_centered_var, self.dcode, view_of(x), _ptr(st.mean), _ptr(part),
@@ -519,6 +556,7 @@ class Engine:
             for a, b in zip((st.sum, st.sumsq, st.mean, st.var),
                             (piece.sum, piece.sumsq, piece.mean, piece.var)):
                 if a[off:off + c].data_ptr() != b.data_ptr():  # not in place: copy (ops.py:128-143)
+                    self._flush_pending()
                     dst = a[off:off + c]
                     def _cp(stream, d=dst, s=b):
                         d.copy_(s)

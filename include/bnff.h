@@ -263,6 +263,14 @@ int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view dx, void* 
 int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, float* stat_part,
                      void* stream);
 int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void* stream);
+/* K9b: sub-BN2 -> ReLU -> k x k average pool in one pass (a chain whose consumer is a pool,
+ * e.g. the stem, graph.py:358-375): y = avgpool(relu((x-a)*b+c)) (+ partials of y), and
+ * backward dt1 = [bn(x) > 0] * spread(dy)/k^2 with (sum dt1, sum dt1*xhat) partials (xhat =
+ * (x-a)*d), i.e. avgpool_bwd + relu_bwd + bn_bwd sums (ops.py:271-274, 314-319, 428-454). */
+int bnff_norm_relu_pool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, bnff_coef coef,
+                            float* stat_part, void* stream);
+int bnff_pool_relu_bn_bwd(int32_t dtype, bnff_view dy, bnff_view x, bnff_view dt1, int32_t k,
+                          bnff_coef coef, float* part, void* stream);
 /* K10: y = a + zero-channel-padded b (execute.py:266-280) */
 int bnff_ews_fwd(int32_t dtype, bnff_view a, bnff_view b, bnff_view y, void* stream);
 /* K11: copy a view into another (physical concat piece / gradient slice copy) */

@@ -108,6 +108,8 @@ SIGNATURES = {
     "bnff_relu_fwd": (C.c_int, [_I32, View, View, _P]),
     "bnff_relu_bwd": (C.c_int, [_I32, View, View, View, _P]),
     "bnff_avgpool_fwd": (C.c_int, [_I32, View, View, _I32, _P, _P]),
+    "bnff_norm_relu_pool_fwd": (C.c_int, [_I32, View, View, _I32, Coef, _P, _P]),
+    "bnff_pool_relu_bn_bwd": (C.c_int, [_I32, View, View, View, _I32, Coef, _P, _P]),
     "bnff_avgpool_bwd": (C.c_int, [_I32, View, View, _I32, _P]),
     "bnff_ews_fwd": (C.c_int, [_I32, View, View, View, _P]),
     "bnff_copy": (C.c_int, [_I32, View, View, _P]),

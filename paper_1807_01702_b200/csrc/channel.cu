@@ -747,6 +747,178 @@ __global__ void __launch_bounds__(256) avgpool_wide_kernel(View x, View y, int h
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// norm -> ReLU -> k x k average pool (the stem and any sub-BN2 -> ReLU -> AvgPool chain whose
+// consumer is not a conv, graph.py:358-375): forward reads the conv output once and writes
+// only the pooled map (+ its sub-BN1 partials); backward writes the BN-input gradient dt1 =
+// ReLU'(bn(x)) * spread(dy)/k^2 and its (sum dt1, sum dt1*xhat) partials in the same pass
+// (avgpool_bwd + relu_bwd + bn_bwd sums, ops.py:271-274, 314-319, 443-454).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, int oh, int ow, int C, int k,
+                                          bnff_coef cf, float* part) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[2][kSumThreads][V];
+  const long long pixels = (long long)n * oh * ow;
+  const int cpr = C / V;
+  const int tiles = gridDim.x;
+  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
+  const long long r_begin = blockIdx.x * rows_per_tile;
+  const long long r_end = min(pixels, r_begin + rows_per_tile);
+  const float inv = 1.f / (float)(k * k);
+  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, cpr - cbase);
+    const int rows_per_iter = kSumThreads / ccount;
+    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
+    const int c0 = (cbase + tcol) * V;
+    float s1[V], s2[V], ma[V], sc[V], be[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    if (trow < rows_per_iter) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        ma[i] = __ldg(cf.a + c0 + i);
+        sc[i] = __ldg(cf.b + c0 + i);
+        be[i] = __ldg(cf.c + c0 + i);
+      }
+      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+        const int img = (int)(r / ((long long)oh * ow));
+        const int rem = (int)(r - (long long)img * oh * ow);
+        const int oy = rem / ow, ox = rem - oy * ow;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        for (int dy = 0; dy < k; ++dy)
+          for (int dx = 0; dx < k; ++dx) {
+            float f[V];
+            const long long src = ((long long)img * h + oy * k + dy) * w + ox * k + dx;
+            VecIO<T>::load(x.p, src * x.rs + c0, f);
+#pragma unroll
+            for (int i = 0; i < V; ++i)  // bn_fwd op order (ops.py:246-249), ReLU, in the storage precision
+              acc[i] += VecIO<T>::round(fmaxf(__fadd_rn(__fmul_rn(__fsub_rn(f[i], ma[i]), sc[i]), be[i]), 0.f));
+          }
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = VecIO<T>::round(acc[i] * inv);
+        VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, acc);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          s1[i] += acc[i];
+          s2[i] += acc[i] * acc[i];
+        }
+      }
+    }
+    if (part == nullptr) continue;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sh[0][threadIdx.x][i] = s1[i];
+      sh[1][threadIdx.x][i] = s2[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < ccount) {
+      float a[V], b[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int rr = 0; rr < rows_per_iter; ++rr)
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          a[i] += sh[0][rr * ccount + threadIdx.x][i];
+          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+        }
+      const int cc = (cbase + threadIdx.x) * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void pool_relu_bn_bwd_kernel(View dyp, View x, View dr, int n, int h, int w, int oh, int ow, int C,
+                                        int k, bnff_coef cf, float* part) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int V = VecIO<T>::V;
+  __shared__ float sh[2][kSumThreads][V];
+  const long long pixels = (long long)n * h * w;
+  const int cpr = C / V;
+  const int tiles = gridDim.x;
+  const long long rows_per_tile = (pixels + tiles - 1) / tiles;
+  const long long r_begin = blockIdx.x * rows_per_tile;
+  const long long r_end = min(pixels, r_begin + rows_per_tile);
+  const float inv = 1.f / (float)(k * k);
+  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, cpr - cbase);
+    const int rows_per_iter = kSumThreads / ccount;
+    const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
+    const int c0 = (cbase + tcol) * V;
+    float s1[V], s2[V], ma[V], sc[V], be[V], iv[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    if (trow < rows_per_iter) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        ma[i] = __ldg(cf.a + c0 + i);
+        sc[i] = __ldg(cf.b + c0 + i);
+        be[i] = __ldg(cf.c + c0 + i);
+        iv[i] = __ldg(cf.d + c0 + i);
+      }
+      for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
+        const int img = (int)(r / ((long long)h * w));
+        const int rem = (int)(r - (long long)img * h * w);
+        const int yy = rem / w, xx = rem - yy * w;
+        float xf[V], d[V];
+        VecIO<T>::load(x.p, r * x.rs + c0, xf);
+        const int py = yy / k, px = xx / k;
+        if (py < oh && px < ow) {
+          VecIO<T>::load(dyp.p, (((long long)img * oh + py) * ow + px) * dyp.rs + c0, d);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) d[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float z = __fadd_rn(__fmul_rn(__fsub_rn(xf[i], ma[i]), sc[i]), be[i]);
+          d[i] = VecIO<T>::round(z > 0.f ? VecIO<T>::round(d[i] * inv) : 0.f);
+          const float xh = __fmul_rn(__fsub_rn(xf[i], ma[i]), iv[i]);
+          s1[i] += d[i];
+          s2[i] += d[i] * xh;
+        }
+        VecIO<T>::store(const_cast<void*>(dr.p), r * dr.rs + c0, d);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sh[0][threadIdx.x][i] = s1[i];
+      sh[1][threadIdx.x][i] = s2[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < ccount) {
+      float a[V], b[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int rr = 0; rr < rows_per_iter; ++rr)
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          a[i] += sh[0][rr * ccount + threadIdx.x][i];
+          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+        }
+      const int cc = (cbase + threadIdx.x) * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void avgpool_bwd_kernel(View dy, View dx, int n, int h, int w, int oh, int ow, int C, int k) {
   griddep_launch();
@@ -1131,6 +1303,34 @@ extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t
   BNFF_DISPATCH(dtype, avgpool_fwd_kernel, sum_tiles(pixels), kSumThreads, 0, (cudaStream_t)stream, vw(x), vw(y),
                 (int)x.n, (int)x.h, (int)x.w, (int)y.h, (int)y.w, (int)x.c, k, stat_part);
   return check_launch("avgpool_fwd");
+}
+
+extern "C" int bnff_norm_relu_pool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, bnff_coef coef,
+                                       float* stat_part, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, x, "norm_relu_pool x")) || (rc = check_view(dtype, y, "norm_relu_pool y"))) return rc;
+  if (y.h != x.h / k || y.w != x.w / k || y.c != x.c || y.n != x.n || y.h < 1 || y.w < 1)
+    return set_error(BNFF_ERR_SHAPE, "norm_relu_pool: bad output dims");
+  if (!coef.a || !coef.b || !coef.c) return set_error(BNFF_ERR_STATE, "norm_relu_pool: missing statistics");
+  const long long pixels = y.n * y.h * y.w;
+  BNFF_DISPATCH(dtype, norm_relu_pool_fwd_kernel, sum_tiles(pixels), kSumThreads, 0, (cudaStream_t)stream, vw(x),
+                vw(y), (int)x.n, (int)x.h, (int)x.w, (int)y.h, (int)y.w, (int)x.c, k, coef, stat_part);
+  return check_launch("norm_relu_pool_fwd");
+}
+
+extern "C" int bnff_pool_relu_bn_bwd(int32_t dtype, bnff_view dy, bnff_view x, bnff_view dt1, int32_t k,
+                                     bnff_coef coef, float* part, void* stream) {
+  int rc;
+  if ((rc = check_view(dtype, dy, "pool_relu_bn_bwd dy")) || (rc = check_view(dtype, x, "pool_relu_bn_bwd x")) ||
+      (rc = check_view(dtype, dt1, "pool_relu_bn_bwd dt1")))
+    return rc;
+  if (dy.h != x.h / k || dy.w != x.w / k || dy.c != x.c || dt1.c != x.c || dt1.h != x.h || dt1.w != x.w)
+    return set_error(BNFF_ERR_SHAPE, "pool_relu_bn_bwd: dims");
+  if (!coef.a || !coef.b || !coef.c || !coef.d) return set_error(BNFF_ERR_STATE, "pool_relu_bn_bwd: missing tables");
+  const long long pixels = x.n * x.h * x.w;
+  BNFF_DISPATCH(dtype, pool_relu_bn_bwd_kernel, sum_tiles(pixels), kSumThreads, 0, (cudaStream_t)stream, vw(dy),
+                vw(x), vw(dt1), (int)x.n, (int)x.h, (int)x.w, (int)dy.h, (int)dy.w, (int)x.c, k, coef, part);
+  return check_launch("pool_relu_bn_bwd");
 }
 
 extern "C" int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void* stream) {

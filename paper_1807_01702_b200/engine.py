@@ -161,6 +161,9 @@ class Engine:
         self.side_wgrad = bool(side_wgrad)
         import os
         self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
+        self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
+        self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
+        self._nrp_done: set = set()
         # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
         # into the block gradient buffer; the per-channel remainder rides in (A, B) arrays
         self.fold_icf = bool(fold_icf) and self.dcode == _lib.BF16
@@ -479,6 +482,8 @@ class Engine:
                    coef_of(tb[0], tb[1], tb[2]), 0, what="bn_apply", nbytes=_nb(x, y))
 
     def _f_ReLU(self, node):
+        if node.id in self._nrp:  # done by the fused norm-ReLU-pool
+            return
         x = self.acts[node.inputs[0]]
         y = self._feature(node.outputs[0])
         self._emit(self.L.bnff_relu_fwd, self.dcode, view_of(x), view_of(y), what="relu_fwd",
@@ -490,11 +495,45 @@ class Engine:
         self._channel_stats(x, st, node.name)
         self.stats[node.outputs[0]] = st
 
+    def _nrp_chain(self, node):
+        """sub-BN2 -> ReLU -> 2x2 AvgPool with single consumers (the stem): (relu, pool) or None."""
+        if not self.fuse_nrp:
+            return None
+        outs = set(self.g.outputs)
+        c1 = self.g.consumers_of(node.outputs[0])
+        if len(c1) != 1 or c1[0].kind != G.RELU or node.outputs[0] in outs:
+            return None
+        relu = c1[0]
+        c2 = self.g.consumers_of(relu.outputs[0])
+        if len(c2) != 1 or c2[0].kind != G.POOL or relu.outputs[0] in outs or c2[0].attrs.k != 2:
+            return None
+        return relu, c2[0]
+
     def _f_FissionSubBN2(self, node):
         x = self.acts[node.inputs[0]]
         st = self.stats.get(node.inputs[1])
         if st is None:
             raise StateError(f"{node.name}: statistics slot {node.inputs[1]} never produced")
+        chain = self._nrp_chain(node)
+        if chain is not None:  # normalize + ReLU + pool in one pass over the conv output
+            relu, pool = chain
+            tb = self._bn_tables(st, node.attrs.bn, node.name)
+            self.node_tables[node.id] = tb
+            y = self._feature(pool.outputs[0])
+            pixels = y.shape[0] * y.shape[1] * y.shape[2]
+            part, tiles = None, 0
+            if pool.attrs.emit_stats:
+                tiles = self.L.bnff_sum_tiles(pixels)
+                part = self._empty((tiles, 2, y.shape[3]), torch.float32)
+            self._emit(self.L.bnff_norm_relu_pool_fwd, self.dcode, view_of(x), view_of(y), pool.attrs.k,
+                       coef_of(tb[0], tb[1], tb[2]), _ptr(part), what=f"norm_relu_pool {node.name}",
+                       nbytes=_nb(x, y))
+            if pool.attrs.emit_stats:
+                pst = self._stats_for(pool.outputs[0], y.shape[3], pixels)
+                self._emit_stats_finalize(part, tiles, y.shape[3], pixels, pst)
+                self.stats[pool.outputs[1]] = pst
+            self._nrp[relu.id] = self._nrp[pool.id] = node
+            return
         y = self._feature(node.outputs[0])
         tb = self._bn_tables(st, node.attrs.bn, node.name)
         self.node_tables[node.id] = tb
@@ -579,6 +618,8 @@ class Engine:
                    nbytes=_nb(a, b, y))
 
     def _f_AvgPool(self, node):
+        if node.id in self._nrp:
+            return
         x = self.acts[node.inputs[0]]
         y = self._feature(node.outputs[0])
         part = None
@@ -782,6 +823,8 @@ class Engine:
         self._add_grad(node.inputs[0], Plain(self._resolve(Deferred(dy, x, m32, i32, k1, k2, gg))))
 
     def _b_ReLU(self, node):
+        if node.id in self._nrp:
+            return
         dy = self._incoming(node.outputs[0])
         x = self.acts[node.inputs[0]]
         dx = self._fresh_like(x)
@@ -797,6 +840,8 @@ class Engine:
             self.grads[node.inputs[0]] = Plain(self._resolve(pending))
 
     def _b_FissionSubBN2(self, node):
+        if node.id in self._nrp_done:
+            return
         dy = self._incoming(node.outputs[0])
         x = self.acts[node.inputs[0]]
         st = self.stats[node.inputs[1]]
@@ -950,6 +995,23 @@ class Engine:
         self._add_grad(node.inputs[1], Plain(dy[..., :cb] if node.attrs.pad_channels else dy))
 
     def _b_AvgPool(self, node):
+        head = self._nrp.get(node.id)
+        if head is not None:  # pool bwd + ReLU bwd + BN gradient sums in one pass
+            dy = self._incoming(node.outputs[0])
+            x = self.acts[head.inputs[0]]
+            st = self.stats[head.inputs[1]]
+            m32, s32, b32, i32 = self.node_tables[head.id]
+            dt1 = self._fresh_like(x)
+            pixels = x.shape[0] * x.shape[1] * x.shape[2]
+            tiles = self.L.bnff_sum_tiles(pixels)
+            part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+            self._emit(self.L.bnff_pool_relu_bn_bwd, self.dcode, view_of(dy), view_of(x), view_of(dt1),
+                       node.attrs.k, coef_of(m32, s32, b32, i32), _ptr(part),
+                       what=f"pool_relu_bn_bwd {head.name}", nbytes=_nb(dy, x, dt1))
+            mm, ii, k1, k2, gg = self._dx_coeffs(part, tiles, x.shape[3], pixels, st, head.attrs.bn, head.name)
+            self._add_grad(head.inputs[0], Deferred(dt1, x, mm, ii, k1, k2, gg))
+            self._nrp_done.add(head.id)
+            return
         dy = self._incoming(node.outputs[0])
         x = self.acts[node.inputs[0]]
         if not self._wants_dx(node.inputs[0]):

@@ -48,6 +48,7 @@ struct WcParams {
   // TMA boxes of the window operand (and of the BN_DX x operand): rank 2 {c, pixels}
   // box {slab, 128} for 1x1; rank 4 {c, w, h, n} box {slab, wp, BR, BI} for 3x3
   CUtensorMap tma_a, tma_x;
+  CUtensorMap tma_out;  // tstore: the output written by TMA stores from the swizzled staging tile
   // 3x3 tiling: tmode 1 = kt output rows of one image (window rows oy-1 .. oy+kt),
   // tmode 2 = kt whole images per tile (small maps); WPI = window rows per image block,
   // tpi = tiles per image (tmode 1), Rld = rows the TMA writes per stage
@@ -66,6 +67,7 @@ struct WcParams {
   const __nv_bfloat16* ex; long long ex_rs;
   bnff_coef ecoef;
   float* stat_part;
+  int tstore;                  // 1: staging in 128B-swizzled rows, stored by cp.async.bulk.tensor
   unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
 };
 
@@ -134,11 +136,11 @@ struct Layout {
 
 // byte offsets of the dynamic shared memory carve-up (identical on host and device)
 struct Carve {
-  int wres, stage0, stage_bytes, a_bytes, stg, ptab, etab, sacc, red, rowtab, rowpix, meta, total;
+  int wres, stage0, stage_bytes, a_bytes, stg, gbuf, ptab, etab, sacc, red, rowtab, rowpix, meta, total;
 };
 
 template <int BN, int RB, int TAPS, int MODE, bool SW = false>
-__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop) {
+__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop, bool gb = false) {
   using L = Layout<BN, RB, TAPS, MODE, SW>;
   Carve c{};
   int off = 0;
@@ -150,6 +152,8 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   off += stages * c.stage_bytes;
   c.stg = off;
   off += 2 * L::NSTG * L::STG;
+  c.gbuf = off;  // block-gradient fold by TMA: one 128B-swizzled G tile per owned chunk
+  if (gb) off += 2 * L::MYCH * 128 * 128;
   c.ptab = off;
   off += 3 * nslab * L::SLABW * 4;
   c.etab = off;
@@ -165,6 +169,13 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.meta = off;  // (unused by the TMA loader)
   c.total = off + 1024;  // + alignment slack
   return c;
+}
+
+// the 1x1 block-gradient fold runs through TMA (G tile loaded, folded in smem, stored back)
+template <int BN, int RB, int TAPS, int MODE, bool SW>
+__host__ __device__ inline bool fold_tma(const WcParams& p) {
+  return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW>::CW == 64 && p.tstore != 0 &&
+         p.epi >= BNFF_DG_NRC_ACC;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
@@ -215,10 +226,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
   uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar;
+  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar, g_bar[4];
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
-  const Carve cv = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, p.stages, xop_s);
+  const bool gb_s = fold_tma<BN, RB, TAPS, MODE, SW>(p);
+  const Carve cv = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, p.stages, xop_s, gb_s);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* etab = reinterpret_cast<float*>(smem + cv.etab);
@@ -244,6 +256,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     if (xop_s) tma_prefetch_desc(&p.tma_x);
     for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], NEW * 32); }
     mbar_init(&w_bar, 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&g_bar[s], 1);
+    if (p.tstore) tma_prefetch_desc(&p.tma_out);
     fence_mbar_init();
     if (L::WRES) {
       // resident weights: packed after the previous optimizer step, i.e. at least two
@@ -509,6 +523,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const bool nrc = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC;
     const bool fold = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC_ACC;  // out (+)= scale * dt1
     const bool fold_acc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC_ACC;
+    // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
+    // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
+    // place in shared memory during the row pass and stores it back
+    const bool tfold = gb_s;
+    const bool tst = CW == 64 && p.tstore != 0 && (!fold || tfold);
+    uint8_t* gb0 = smem + cv.gbuf + grp * MYCH * 128 * 128;
     const bool stats = do_stats && (MODE == M_FPROP || nrc);
     const bool persist = true;  // grid % ntiles == 0: a CTA's columns never change, sums stay in registers
     float2 acc1[MYCH], acc2[MYCH];
@@ -579,14 +599,26 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       }
       named_bar_sync(bar_id, 128);
     };
+    auto fetch_g = [&](int it2, int k) {  // one thread of the group; the buffer is free
+      if (tfold && fold_acc && it2 < ntl && grp + 2 * k < NCH) {
+        int mtb, n0b;
+        tile_of(it2, mtb, n0b);
+        mbar_arrive_expect_tx(&g_bar[grp * 2 + k], 128 * 128);
+        tma_load_2d(smem_u32(gb0 + k * 128 * 128), &p.tma_out, n0b + (grp + 2 * k) * CW, mtb * 128,
+                    &g_bar[grp * 2 + k]);
+      }
+    };
 #pragma unroll
-    for (int k = 0; k < MYCH; ++k) fetch_x(0, k);
+    for (int k = 0; k < MYCH; ++k) {
+      fetch_x(0, k);
+      if (gt == 0) fetch_g(0, k);
+    }
     for (int it = 0; it < ntl; ++it) {
       const int buf = it & 1;
       int mt, n0;
       tile_of(it, mt, n0);
       gpix[row] = out_pix(mt, row);
-      if (MODE == M_DGRAD && fold_acc) named_bar_sync(bar_id, 128);  // gpix of every row for the prefetch
+      if (MODE == M_DGRAD && fold_acc && !tfold) named_bar_sync(bar_id, 128);  // gpix of every row for the prefetch
       const int pix = gpix[row];
       mbar_wait(&accf_bar[buf], (it >> 1) & 1);
       if (et == 0) trace_ev(p.trace, 6, it);
@@ -597,7 +629,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         if (ci >= NCH) break;
         const int cc = ci * CW;
         uint4 gold[CW / 8];
-        if (MODE == M_DGRAD && fold_acc) {  // prefetch the old block-gradient chunks this thread stores
+        if (MODE == M_DGRAD && fold_acc && !tfold) {  // prefetch the old block-gradient chunks this thread stores
           constexpr int CPO = CW / 8;
 #pragma unroll
           for (int i = 0; i < CPO; ++i) {
@@ -614,6 +646,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           for (int i = 0; i < CW / 8; ++i) gold[i] = make_uint4(0, 0, 0, 0);
         }
         if (need_x) cp_async_wait<MYCH - 1>();
+        if (tfold && fold_acc) mbar_wait(&g_bar[grp * 2 + k], it & 1);
         const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
         if (et == 0) trace_ev(p.trace, 10, it * 4 + k);
         // ---- row pass
@@ -649,16 +682,54 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
               for (int i = 0; i < 16; ++i) v[i] = 0.f;
             }
           }
-          uint4* sp = reinterpret_cast<uint4*>(stg + row * L::SROWB + c16 * 2);
-          sp[0] = pack8(v, false);
-          sp[1] = pack8(v + 8, false);
+          if (tst) {  // dense 128-byte rows, 128B swizzle (the TMA store's box layout)
+            const int j = c16 >> 3;
+            const int o0 = row * 128 + ((j ^ (row & 7)) << 4), o1 = row * 128 + (((j + 1) ^ (row & 7)) << 4);
+            *reinterpret_cast<uint4*>(stg + o0) = pack8(v, false);
+            *reinterpret_cast<uint4*>(stg + o1) = pack8(v + 8, false);
+            if (MODE == M_DGRAD && tfold) {  // G = (acc ? G : 0) + scale * dt1 (dt1 rounded like the store)
+              uint8_t* gt0 = gb0 + k * 128 * 128;
+              float sc[16], d[16];
+              ld16f(etab + gc, sc);
+              const uint4 r0 = pack8(v, false), r1 = pack8(v + 8, false);
+              unpack8(r0, d);
+              unpack8(r1, d + 8);
+              if (fold_acc) {
+                float o[16];
+                unpack8(*reinterpret_cast<const uint4*>(gt0 + o0), o);
+                unpack8(*reinterpret_cast<const uint4*>(gt0 + o1), o + 8);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) d[i] = fmaf(sc[i], d[i], o[i]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) d[i] = sc[i] * d[i];
+              }
+              *reinterpret_cast<uint4*>(gt0 + o0) = pack8(d, false);
+              *reinterpret_cast<uint4*>(gt0 + o1) = pack8(d + 8, false);
+            }
+          } else {
+            uint4* sp = reinterpret_cast<uint4*>(stg + row * L::SROWB + c16 * 2);
+            sp[0] = pack8(v, false);
+            sp[1] = pack8(v + 8, false);
+          }
         }
         if (ci + 2 >= NCH) {
           tc_fence_before();
           mbar_arrive(&acce_bar[buf]);  // this group is done with the accumulator slot
           if (et == 0) trace_ev(p.trace, 7, it);
         }
+        if (tst) fence_proxy_async_smem();  // staged rows -> visible to the TMA engine
         named_bar_sync(bar_id, 128);
+        if (tst && gt == 0) {  // one thread stores the whole staged chunk, asynchronously
+          if (TAPS == 1) {
+            tma_store_2d(&p.tma_out, n0 + cc, mt * 128, smem_u32(tfold ? gb0 + k * 128 * 128 : stg));
+          } else {
+            int img0, y0;
+            tile_org(mt, img0, y0);
+            tma_store_4d(&p.tma_out, n0 + cc, 0, p.tmode == 2 ? 0 : y0 + 1, img0, smem_u32(stg));
+          }
+          bulk_commit();
+        }
         if (et == 0) trace_ev(p.trace, 11, it * 4 + k);
         // ---- column pass: sums of the stored values (FPROP: y, y^2; NRC: dt1, dt1*xhat)
         if (stats) {
@@ -667,7 +738,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           if (MODE == M_FPROP) {
 #pragma unroll 16
             for (int r = rg; r < 128; r += RG) {
-              const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
+              const uint32_t wv = tst ? s32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
+                                      : s32[r * (L::SROWB / 4) + cp];
               const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
               a = __fadd2_rn(a, f);
               b = __ffma2_rn(f, f, b);
@@ -679,7 +751,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             const float2 hsh = make_float2(etab[3 * p.npad + gc], etab[3 * p.npad + gc + 1]);
 #pragma unroll 16
             for (int r = rg; r < 128; r += RG) {
-              const uint32_t wv = s32[r * (L::SROWB / 4) + cp];
+              const uint32_t wv = tst ? s32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
+                                      : s32[r * (L::SROWB / 4) + cp];
               const uint32_t xw = x32[r * (L::SROWB / 4) + cp];
               const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
               const float2 xh = __ffma2_rn(make_float2(bf16lo(xw), bf16hi(xw)), hinv, hsh);
@@ -693,7 +766,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         if (et == 0) trace_ev(p.trace, 12, it * 4 + k);
         // ---- store pass
         constexpr int CPO = CW / 8;  // 16B chunks per staged row
-        if (MODE == M_DGRAD && fold) {
+        if (MODE == M_DGRAD && fold && !tfold) {
           // block-gradient fold: out = (acc ? out : 0) + scale * dt1; the old block-gradient
           // chunks were fetched into registers before the row pass (their latency hides there)
 #pragma unroll
@@ -711,6 +784,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
               for (int e = 0; e < 8; ++e) d[e] = fold_acc ? fmaf(sc[e], d[e], o[e]) : sc[e] * d[e];
               *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = pack8(d, false);
             }
+          }
+        } else if (tst) {
+          if (gt == 0) {
+            bulk_wait_read0();  // the staging tile is read before it is rewritten
+            fetch_g(it + 1, k); // the fold tile is free: fetch the next tile's old block gradient
           }
         } else {
 #pragma unroll 2
@@ -731,6 +809,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       }
     }
     cp_async_wait<0>();
+    if (tst && gt == 0) bulk_wait_all0();  // outstanding TMA stores complete before exit
     if (stats && persist) {
 #pragma unroll
       for (int k = 0; k < MYCH; ++k)
@@ -1358,9 +1437,18 @@ static int launch_t(WcParams p, cudaStream_t st) {
   int stages = 8;
   Carve c{};
   const bool xop = MODE == M_DGRAD && p.pro == BNFF_PRO_BN_DX;
+  bool gb = fold_tma<BN, RB, TAPS, MODE, SW>(p);
   for (; stages >= 2; --stages) {
-    c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop);
+    c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop, gb);
     if (c.total <= SMEM_BUDGET) break;
+  }
+  if (stages < 2 && gb) {  // no room for the fold tiles: register read-modify-write epilogue
+    p.tstore = 0;
+    gb = false;
+    for (stages = 8; stages >= 2; --stages) {
+      c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop, gb);
+      if (c.total <= SMEM_BUDGET) break;
+    }
   }
   if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
   p.stages = stages;
@@ -1421,6 +1509,14 @@ static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw =
   }
 #undef BNFF_FIT
   return c.total <= SMEM_BUDGET;
+}
+inline bool tstore_enabled() {  // BNFF_TSTORE=0: stores from the epilogue threads (A/B timing)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_TSTORE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
 }
 }  // namespace wc
 }  // namespace bnff
@@ -1541,6 +1637,17 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
     box[0] = slabw; box[1] = 128;
   }
   p.tiles = p.mtiles * p.ntiles;
+  // TMA-store epilogue: 64-column chunks (BN >= 128), not the fold (read-modify-write) modes
+  p.tstore = 0;
+  if (g.BN >= 128 && (epi < BNFF_DG_NRC_ACC || kh == 1) && wc::tstore_enabled()) {
+    uint32_t ob[4];
+    if (kh == 3) {
+      ob[0] = 64; ob[1] = p.wp; ob[2] = p.tmode == 2 ? p.hp : p.kt; ob[3] = p.tmode == 2 ? p.kt : 1;
+    } else {
+      ob[0] = 64; ob[1] = 128;
+    }
+    p.tstore = encode_nhwc_bf16(&p.tma_out, out.ptr, out.n, out.h, out.w, out.c, out.row_stride, rank, ob) ? 1 : 0;
+  }
   if (!encode_nhwc_bf16(&p.tma_a, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
     return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (window operand)");
   if (mode == 1 && pro == BNFF_PRO_BN_DX &&

@@ -48,7 +48,8 @@ struct WcParams {
   // TMA boxes of the window operand (and of the BN_DX x operand): rank 2 {c, pixels}
   // box {slab, 128} for 1x1; rank 4 {c, w, h, n} box {slab, wp, BR, BI} for 3x3
   CUtensorMap tma_a, tma_x;
-  CUtensorMap tma_out;  // tstore: the output written by TMA stores from the swizzled staging tile
+  CUtensorMap tma_out;
+  CUtensorMap tma_ex;   // tstore + dgrad mask: the x tile of the output channels, same box as tma_out  // tstore: the output written by TMA stores from the swizzled staging tile
   // 3x3 tiling: tmode 1 = kt output rows of one image (window rows oy-1 .. oy+kt),
   // tmode 2 = kt whole images per tile (small maps); WPI = window rows per image block,
   // tpi = tiles per image (tmode 1), Rld = rows the TMA writes per stage
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
   uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar, g_bar[4];
+  __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar, g_bar[4], x_bar[4];
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
   const bool gb_s = fold_tma<BN, RB, TAPS, MODE, SW>(p);
@@ -256,8 +257,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     if (xop_s) tma_prefetch_desc(&p.tma_x);
     for (int s = 0; s < 2; ++s) { mbar_init(&accf_bar[s], 1); mbar_init(&acce_bar[s], NEW * 32); }
     mbar_init(&w_bar, 1);
-    for (int s = 0; s < 4; ++s) mbar_init(&g_bar[s], 1);
+    for (int s = 0; s < 4; ++s) { mbar_init(&g_bar[s], 1); mbar_init(&x_bar[s], 1); }
     if (p.tstore) tma_prefetch_desc(&p.tma_out);
+    if (p.tstore && MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN) tma_prefetch_desc(&p.tma_ex);
     fence_mbar_init();
     if (L::WRES) {
       // resident weights: packed after the previous optimizer step, i.e. at least two
@@ -529,6 +531,16 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const bool tfold = gb_s;
     const bool tst = CW == 64 && p.tstore != 0 && (!fold || tfold);
     uint8_t* gb0 = smem + cv.gbuf + grp * MYCH * 128 * 128;
+    const bool tx = tst && need_x;  // x tiles by TMA into 128B-swizzled rows
+    // 3x3 boxes cover kt*wp (or kt*hp*wp) rows; the rows below never receive data: zero once
+    const int xrows = TAPS == 1 ? 128 : p.wp * (p.tmode == 2 ? p.hp * p.kt : p.kt);
+    if (tx && TAPS == 9 && row >= xrows) {
+#pragma unroll
+      for (int k = 0; k < MYCH; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<uint4*>(xs0 + k * L::STG + row * 128 + i * 16) = make_uint4(0, 0, 0, 0);
+    }
     const bool stats = do_stats && (MODE == M_FPROP || nrc);
     const bool persist = true;  // grid % ntiles == 0: a CTA's columns never change, sums stay in registers
     float2 acc1[MYCH], acc2[MYCH];
@@ -555,6 +567,23 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     };
     // one commit group per (tile, owned chunk), issued in order; empty groups keep the count
     auto fetch_x = [&](int it2, int k) {
+      if (tx) {
+        if (gt == 0 && it2 < ntl && grp + 2 * k < NCH) {
+          int mtb, n0b;
+          tile_of(it2, mtb, n0b);
+          const int col = n0b + (grp + 2 * k) * CW;
+          const uint32_t dst = smem_u32(xs0 + k * L::STG);
+          mbar_arrive_expect_tx(&x_bar[grp * 2 + k], xrows * 128);
+          if (TAPS == 1) {
+            tma_load_2d(dst, &p.tma_ex, col, mtb * 128, &x_bar[grp * 2 + k]);
+          } else {
+            int img0, y0;
+            tile_org(mtb, img0, y0);
+            tma_load_4d(dst, &p.tma_ex, col, 0, p.tmode == 2 ? 0 : y0 + 1, img0, &x_bar[grp * 2 + k]);
+          }
+        }
+        return;
+      }
       if (need_x && it2 < ntl && grp + 2 * k < NCH) {
         int mtb, n0b;
         tile_of(it2, mtb, n0b);
@@ -645,7 +674,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < CW / 8; ++i) gold[i] = make_uint4(0, 0, 0, 0);
         }
-        if (need_x) cp_async_wait<MYCH - 1>();
+        if (tx) mbar_wait(&x_bar[grp * 2 + k], it & 1);
+        else if (need_x) cp_async_wait<MYCH - 1>();
         if (tfold && fold_acc) mbar_wait(&g_bar[grp * 2 + k], it & 1);
         const uint8_t* xrow = xs0 + k * L::STG + row * L::SROWB;
         if (et == 0) trace_ev(p.trace, 10, it * 4 + k);
@@ -664,8 +694,15 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           } else {
             if (need_x) {
               float xv[16];
-              unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2), xv);
-              unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2 + 16), xv + 8);
+              if (tx) {
+                const uint8_t* xb = xs0 + k * L::STG + row * 128;
+                const int j = c16 >> 3;
+                unpack8(*reinterpret_cast<const uint4*>(xb + ((j ^ (row & 7)) << 4)), xv);
+                unpack8(*reinterpret_cast<const uint4*>(xb + (((j + 1) ^ (row & 7)) << 4)), xv + 8);
+              } else {
+                unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2), xv);
+                unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2 + 16), xv + 8);
+              }
               if (p.epi == BNFF_DG_CLIP) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = xv[i] > 0.f ? v[i] : 0.f;
@@ -753,7 +790,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             for (int r = rg; r < 128; r += RG) {
               const uint32_t wv = tst ? s32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
                                       : s32[r * (L::SROWB / 4) + cp];
-              const uint32_t xw = x32[r * (L::SROWB / 4) + cp];
+              const uint32_t xw = tx ? x32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
+                                     : x32[r * (L::SROWB / 4) + cp];
               const float2 f = make_float2(bf16lo(wv), bf16hi(wv));
               const float2 xh = __ffma2_rn(make_float2(bf16lo(xw), bf16hi(xw)), hinv, hsh);
               a = __fadd2_rn(a, f);
@@ -1647,6 +1685,9 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
       ob[0] = 64; ob[1] = 128;
     }
     p.tstore = encode_nhwc_bf16(&p.tma_out, out.ptr, out.n, out.h, out.w, out.c, out.row_stride, rank, ob) ? 1 : 0;
+    if (p.tstore && mode == 1 && epi != BNFF_DG_PLAIN &&
+        !encode_nhwc_bf16(&p.tma_ex, ex.ptr, ex.n, ex.h, ex.w, ex.c, ex.row_stride, rank, ob))
+      p.tstore = 0;
   }
   if (!encode_nhwc_bf16(&p.tma_a, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
     return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (window operand)");

@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     __syncwarp();
   } else if (warp == NLW) {
     // =============================== MMA issuer ===============================
-    if (lane == 0) {
+    // the whole warp runs the loop (converged, warp-uniform operands); one elected lane issues
+    {
       if (L::WRES) mbar_wait(&w_bar, 0);
       constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 0, 0);
       const uint32_t wres = smem_u32(smem + cv.wres);
@@ -485,16 +486,16 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
 #pragma unroll
             for (int kk = 0; kk < SLABW / 16; ++kk) {
               if (kk < ks) {
-                umma_f16(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                umma_f16_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
                 acc = 1;
               }
             }
           }
-          umma_commit(&empty_bar[st]);
+          umma_commit_elect(&empty_bar[st]);
           trace_ev(p.trace, 5, it * p.nslab + s);
           if (++st == ST) { st = 0; ph ^= 1u; }
         }
-        umma_commit(&accf_bar[buf]);
+        umma_commit_elect(&accf_bar[buf]);
       }
     }
     __syncwarp();
@@ -1212,7 +1213,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
     __syncwarp();
   } else if (warp == NLW) {
     // =============================== MMA issuer ===============================
-    if (lane == 0) {
+    {  // converged warp, one elected lane issues (see umma_f16_elect)
       constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 1, 1);
       const int ksteps = (p.Kr + 15) / 16;
       int st = 0;
@@ -1237,15 +1238,15 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
               const uint64_t am = a0 + ((2u * mt * p.RA * 128u + shift * 128u) >> 4);
 #pragma unroll 1
               for (int kk = 0; kk < ksteps; ++kk) {
-                umma_f16(tmem + (u * MT + mt) * BN, am + kk * 128, b0 + ((kk * 16 * L::BRB) >> 4), idesc,
+                umma_f16_elect(tmem + (u * MT + mt) * BN, am + kk * 128, b0 + ((kk * 16 * L::BRB) >> 4), idesc,
                          (k > 0 || kk > 0) ? 1u : 0u);
               }
             }
           }
-          umma_commit(&empty_bar[st]);
+          umma_commit_elect(&empty_bar[st]);
           if (++st == ST) { st = 0; ph ^= 1u; }
         }
-        umma_commit(&accf_bar);
+        umma_commit_elect(&accf_bar);
       }
     }
     __syncwarp();

@@ -418,9 +418,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     }
   } else if (warp == PRODUCER) {
     // =============================== TMA producer ===============================
-    // one lane streams window boxes into the stage ring as fast as the MMA frees stages
+    // the producer warp streams window boxes into the stage ring as fast as the MMA frees stages
     // (zero-filled outside the map: the 3x3 halo and image borders come for free)
-    if (lane == 0) {
+    {  // converged warp; one elected lane issues the copies
       const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
       const uint32_t tx_bytes = (uint32_t)p.Rld * RB * (xop ? 2u : 1u);
       int st = 0, round = 0;
@@ -433,22 +433,25 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           trace_ev(p.trace, 0, it * p.nslab + s);
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
           trace_ev(p.trace, 1, it * p.nslab + s);
-          if (!L::WRES) {  // this slab's weights for the N tile, every tap ([slab][tap][npad][RB] pack)
-            mbar_arrive_expect_tx(&full_bar[st], TAPS * BN * RB);
+          if (elect_one()) {
+            if (!L::WRES) {  // this slab's weights for the N tile, every tap ([slab][tap][npad][RB] pack)
+              mbar_arrive_expect_tx(&full_bar[st], TAPS * BN * RB);
 #pragma unroll 1
-            for (int u = 0; u < TAPS; ++u)
-              bulk_g2s(smem_u32(stage_b(st)) + u * BN * RB,
-                       p.wpk + ((long long)(s * TAPS + u) * p.npad + n0) * RB, BN * RB, &full_bar[st]);
+              for (int u = 0; u < TAPS; ++u)
+                bulk_g2s(smem_u32(stage_b(st)) + u * BN * RB,
+                         p.wpk + ((long long)(s * TAPS + u) * p.npad + n0) * RB, BN * RB, &full_bar[st]);
+            }
+            mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
+            const int c = s * SLABW;
+            if (TAPS == 9) {
+              tma_load_4d(smem_u32(stage_a(st)), &p.tma_a, c, -1, y0, img0, &ld_bar[st]);
+              if (xop) tma_load_4d(smem_u32(stage_x(st)), &p.tma_x, c, -1, y0, img0, &ld_bar[st]);
+            } else {
+              tma_load_2d(smem_u32(stage_a(st)), &p.tma_a, c, mt * 128, &ld_bar[st]);
+              if (xop) tma_load_2d(smem_u32(stage_x(st)), &p.tma_x, c, mt * 128, &ld_bar[st]);
+            }
           }
-          mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
-          const int c = s * SLABW;
-          if (TAPS == 9) {
-            tma_load_4d(smem_u32(stage_a(st)), &p.tma_a, c, -1, y0, img0, &ld_bar[st]);
-            if (xop) tma_load_4d(smem_u32(stage_x(st)), &p.tma_x, c, -1, y0, img0, &ld_bar[st]);
-          } else {
-            tma_load_2d(smem_u32(stage_a(st)), &p.tma_a, c, mt * 128, &ld_bar[st]);
-            if (xop) tma_load_2d(smem_u32(stage_x(st)), &p.tma_x, c, mt * 128, &ld_bar[st]);
-          }
+          __syncwarp();
           if (++st == ST) { st = 0; ++round; }
         }
       }
@@ -1168,7 +1171,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
     }
   } else if (warp == WG_PRODUCER) {
     // =============================== TMA producer ===============================
-    if (lane == 0) {
+    {  // converged warp; one elected lane issues the copies
       const uint32_t a_bytes = (uint32_t)p.Rld * 128u * L::AAT;
       const uint32_t b_bytes = (uint32_t)p.Kr * L::BRB * L::NBA;
       const uint32_t tx = a_bytes + b_bytes * (xb ? 2u : 1u);
@@ -1180,32 +1183,35 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
         for (int k = 0; k < cnt; ++k) {
           const int kb = sp * p.kpt + k;
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
-          mbar_arrive_expect_tx(&ld_bar[st], tx);
-          const uint32_t A = smem_u32(stage_a(st)), B = smem_u32(stage_b(st)), X = smem_u32(stage_x(st));
-          if (TAPS == 9) {
-            int img0, y0;
-            kb_org(kb, img0, y0);
-            const int oy = y0 + 1;
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&ld_bar[st], tx);
+            const uint32_t A = smem_u32(stage_a(st)), B = smem_u32(stage_b(st)), X = smem_u32(stage_x(st));
+            if (TAPS == 9) {
+              int img0, y0;
+              kb_org(kb, img0, y0);
+              const int oy = y0 + 1;
 #pragma unroll
-            for (int a = 0; a < L::AAT; ++a)
-              tma_load_4d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, -1, y0, img0, &ld_bar[st]);
+              for (int a = 0; a < L::AAT; ++a)
+                tma_load_4d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, -1, y0, img0, &ld_bar[st]);
 #pragma unroll
-            for (int b = 0; b < L::NBA; ++b) {
-              const int c = nt * BN + b * (L::BRB / 2);
-              tma_load_4d(B + b * KB * L::BRB, &p.tma_dy, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
-              if (xb) tma_load_4d(X + b * KB * L::BRB, &p.tma_dyx, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
-            }
-          } else {
+              for (int b = 0; b < L::NBA; ++b) {
+                const int c = nt * BN + b * (L::BRB / 2);
+                tma_load_4d(B + b * KB * L::BRB, &p.tma_dy, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
+                if (xb) tma_load_4d(X + b * KB * L::BRB, &p.tma_dyx, c, 0, p.tmode == 2 ? 0 : oy, img0, &ld_bar[st]);
+              }
+            } else {
 #pragma unroll
-            for (int a = 0; a < L::AAT; ++a)
-              tma_load_2d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, kb * KB, &ld_bar[st]);
+              for (int a = 0; a < L::AAT; ++a)
+                tma_load_2d(A + a * p.RA * 128, &p.tma_x, mg * MT * 128 + a * 64, kb * KB, &ld_bar[st]);
 #pragma unroll
-            for (int b = 0; b < L::NBA; ++b) {
-              const int c = nt * BN + b * (L::BRB / 2);
-              tma_load_2d(B + b * KB * L::BRB, &p.tma_dy, c, kb * KB, &ld_bar[st]);
-              if (xb) tma_load_2d(X + b * KB * L::BRB, &p.tma_dyx, c, kb * KB, &ld_bar[st]);
+              for (int b = 0; b < L::NBA; ++b) {
+                const int c = nt * BN + b * (L::BRB / 2);
+                tma_load_2d(B + b * KB * L::BRB, &p.tma_dy, c, kb * KB, &ld_bar[st]);
+                if (xb) tma_load_2d(X + b * KB * L::BRB, &p.tma_dyx, c, kb * KB, &ld_bar[st]);
+              }
             }
           }
+          __syncwarp();
           if (++st == ST) { st = 0; ++round; }
         }
       }

@@ -270,9 +270,15 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     }
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
-  griddep_wait();  // everything below reads data of the preceding launches
+  __syncthreads();  // barrier initialisation visible to every role (no data dependency yet)
+  griddep_wait();   // everything below reads data of the preceding launches
+  // the producer warp (the last warp) starts streaming the first stages at once; the other
+  // warps build the coefficient tables meanwhile and meet on a named barrier
+  constexpr int ST_THREADS = WC_THREADS - 32;
+  static_assert(PRODUCER * 32 == ST_THREADS, "producer is the last warp");
+  if (warp != PRODUCER) {
   // window-operand tables: BN_RELU: (scale, beta - mean*scale); BN_DX: (g, -g*k2*inv, g*(k2*inv*mean-k1))
-  for (int c = tid; c < kpad; c += WC_THREADS) {
+  for (int c = tid; c < kpad; c += ST_THREADS) {
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
     if (c < p.ci) {
       if (p.pro == BNFF_PRO_BN_RELU) {
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     ptab[2 * kpad + c] = t2;
   }
   // epilogue tables: FPROP: bias; DGRAD NRC: (scale, beta-mean*scale, inv, -mean*inv)
-  for (int c = tid; c < p.npad; c += WC_THREADS) {
+  for (int c = tid; c < p.npad; c += ST_THREADS) {
     float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
     if (c < p.N) {
       if (MODE == M_FPROP) {
@@ -312,22 +318,23 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       etab[3 * p.npad + c] = t3;
     }
   }
-  for (int c = tid; c < BN; c += WC_THREADS) {
+  for (int c = tid; c < BN; c += ST_THREADS) {
     sacc[c] = 0.f;
     sacc[BN + c] = 0.f;
   }
   if (TAPS == 9) {  // window row -> (image block, padded row, padded column), same every tile
-    for (int r = tid; r < p.Rld; r += WC_THREADS) {
+    for (int r = tid; r < p.Rld; r += ST_THREADS) {
       const int i = r / p.WPI, rem = r - i * p.WPI;
       const int ry = rem / p.wp, rx = rem - ry * p.wp;
       rowtab[r] = (i << 20) | (ry << 10) | rx;
     }
   }
   if (p.stat_part != nullptr && p.ntiles > 1)  // this CTA's partial row accumulates in place
-    for (int c = tid; c < 2 * p.N; c += WC_THREADS) p.stat_part[(long long)blockIdx.x * 2 * p.N + c] = 0.f;
+    for (int c = tid; c < 2 * p.N; c += ST_THREADS) p.stat_part[(long long)blockIdx.x * 2 * p.N + c] = 0.f;
   tc_fence_before();
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"n"(ST_THREADS) : "memory");
   tc_fence_after();
+  }
   if (threadIdx.x == 0) trace_ev(p.trace, 9, 0);
   const uint32_t tmem = tmem_sh;
 
@@ -1002,8 +1009,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
       rowg[m] = (i << 20) | (yo << 10) | x;
     }
   }
-  griddep_wait();  // everything below reads data of the preceding launches
-  for (int c = tid; c < cin_pad; c += WG_THREADS) {  // x prologue: (scale, beta - mean*scale)
+  fence_proxy_async_smem();  // zeroed stage buffers -> visible to the async proxy (TMA, UMMA)
+  __syncthreads();           // ... and the barrier initialisation to every role
+  griddep_wait();            // everything below reads data of the preceding launches
+  // the producer warp (the last warp) starts streaming at once; the others build the tables
+  constexpr int GS_THREADS = WG_THREADS - 32;
+  static_assert(WG_PRODUCER * 32 == GS_THREADS, "producer is the last warp");
+  if (warp != WG_PRODUCER) {
+  for (int c = tid; c < cin_pad; c += GS_THREADS) {  // x prologue: (scale, beta - mean*scale)
     float t0 = 1.f, t1 = 0.f;
     if (c < p.cin && p.x_pro == BNFF_PRO_BN_RELU) {
       t0 = p.x_coef.b[c];
@@ -1012,7 +1025,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
     ptab[c] = t0;
     ptab[cin_pad + c] = t1;
   }
-  for (int c = tid; c < npad; c += WG_THREADS) {  // dy prologue (BN_DX)
+  for (int c = tid; c < npad; c += GS_THREADS) {  // dy prologue (BN_DX)
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
     if (c < p.cout && xb) {
       const float m = p.dy_coef.a[c], inv = p.dy_coef.b[c], k1 = p.dy_coef.c[c],
@@ -1025,10 +1038,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_kernel(const __grid_const
     qtab[npad + c] = t1;
     qtab[2 * npad + c] = t2;
   }
-  fence_proxy_async_smem();  // zeroed stage buffers -> visible to the async proxy (TMA, UMMA)
   tc_fence_before();
-  __syncthreads();
+  asm volatile("bar.sync 6, %0;" ::"n"(GS_THREADS) : "memory");
   tc_fence_after();
+  }
   const uint32_t tmem = tmem_sh;
   auto unit_of = [&](int ui, int& mg, int& nt, int& sp) {
     const int u = (int)blockIdx.x + ui * (int)gridDim.x;

@@ -120,7 +120,9 @@ struct Layout {
   static constexpr int CPR = RB / 16;                // 16B chunks per row
   static constexpr int RS = LT / CPR;                // loader row step
   static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
-  static constexpr bool WRES = TAPS == 9 && !SW;     // weights resident in smem (else streamed per stage)
+  // weights resident in smem (else streamed per stage): 3x3 unless streamed (SW); 1x1 fprop
+  // when SW is set (the CTA's fixed N tile of every slab, loaded once by the producer)
+  static constexpr bool WRES = (TAPS == 9 && !SW) || (TAPS == 1 && SW);
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
   static constexpr int CW = BN <= 32 ? 16 : (BN == 64 ? 32 : 64);
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     if (p.tstore) tma_prefetch_desc(&p.tma_out);
     if (p.tstore && MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN) tma_prefetch_desc(&p.tma_ex);
     fence_mbar_init();
-    if (L::WRES) {
+    if (L::WRES && TAPS == 9) {
       // resident weights: packed after the previous optimizer step, i.e. at least two
       // launches back, so they may be fetched before this grid's dependency wait
       const uint32_t wb = p.nslab * TAPS * BN * RB;
@@ -428,6 +430,14 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // the producer warp streams window boxes into the stage ring as fast as the MMA frees stages
     // (zero-filled outside the map: the 3x3 halo and image borders come for free)
     {  // converged warp; one elected lane issues the copies
+      if (TAPS == 1 && L::WRES && elect_one()) {  // this CTA's N tile of every slab, once
+        const int n0r = ((int)blockIdx.x % p.ntiles) * BN;
+        mbar_arrive_expect_tx(&w_bar, (uint32_t)(p.nslab * BN * RB));
+        for (int s = 0; s < p.nslab; ++s)
+          bulk_g2s(smem_u32(smem + cv.wres) + s * BN * RB, p.wpk + ((long long)s * p.npad + n0r) * RB, BN * RB,
+                   &w_bar);
+      }
+      __syncwarp();
       const bool xop = L::XOP && p.pro == BNFF_PRO_BN_DX;
       const uint32_t tx_bytes = (uint32_t)p.Rld * RB * (xop ? 2u : 1u);
       int st = 0, round = 0;
@@ -1524,9 +1534,24 @@ static int launch_t(WcParams p, cudaStream_t st) {
   return check_launch("wconv");
 }
 
+inline bool wres1_enabled() {  // BNFF_WRES1=0: stream 1x1 fprop weights per stage (A/B timing)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_WRES1");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
 template <int MODE, int TAPS>
 static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st, int sw = 0) {
   if (TAPS == 9 && sw) return launch_t<64, 64, TAPS, MODE, true>(p, st);
+  // 1x1 fprop with <= 64 KB of weights per N tile: weights resident, the freed half of every
+  // stage goes to a deeper window ring (more bytes in flight per SM)
+  if (TAPS == 1 && MODE == M_FPROP && RB == 128 && BN <= 128 && p.nslab * BN * RB <= 64 * 1024 &&
+      wres1_enabled()) {
+    if (BN == 128) return launch_t<128, 128, 1, MODE, true>(p, st);
+    if (BN == 64) return launch_t<64, 128, 1, MODE, true>(p, st);
+  }
   if (RB == 64) {
     switch (BN) {
       case 32: return launch_t<32, 64, TAPS, MODE>(p, st);

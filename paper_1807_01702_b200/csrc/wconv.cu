@@ -405,15 +405,26 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             uint4 o;
             if (p.pro == BNFF_PRO_RELU) {
               o = pack8(f, true);
-            } else if (p.pro == BNFF_PRO_BN_RELU) {
+            } else if (p.pro == BNFF_PRO_BN_RELU) {  // paired FFMA2: same RN fp32 FMAs, half the issues
 #pragma unroll
-              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], t1[i]);
+              for (int i = 0; i < 8; i += 2) {
+                const float2 r2 = __ffma2_rn(make_float2(f[i], f[i + 1]), make_float2(t0[i], t0[i + 1]),
+                                             make_float2(t1[i], t1[i + 1]));
+                f[i] = r2.x;
+                f[i + 1] = r2.y;
+              }
               o = pack8(f, true);
             } else {
               float xf[8];
               unpack8(*reinterpret_cast<const uint4*>(X + off), xf);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], t0[i], fmaf(xf[i], t1[i], t2[i]));
+              for (int i = 0; i < 8; i += 2) {
+                const float2 in2 = __ffma2_rn(make_float2(xf[i], xf[i + 1]), make_float2(t1[i], t1[i + 1]),
+                                              make_float2(t2[i], t2[i + 1]));
+                const float2 r2 = __ffma2_rn(make_float2(f[i], f[i + 1]), make_float2(t0[i], t0[i + 1]), in2);
+                f[i] = r2.x;
+                f[i + 1] = r2.y;
+              }
               o = pack8(f, false);
             }
             *reinterpret_cast<uint4*>(A + off) = o;
@@ -732,7 +743,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
                 ld16f(etab + gc, e0);
                 ld16f(etab + p.npad + gc, e1);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = fmaf(xv[i], e0[i], e1[i]) > 0.f ? v[i] : 0.f;
+                for (int i = 0; i < 16; i += 2) {
+                  const float2 z = __ffma2_rn(make_float2(xv[i], xv[i + 1]), make_float2(e0[i], e0[i + 1]),
+                                              make_float2(e1[i], e1[i + 1]));
+                  v[i] = z.x > 0.f ? v[i] : 0.f;
+                  v[i + 1] = z.y > 0.f ? v[i + 1] : 0.f;
+                }
               }
             }
             if (pix < 0) {
@@ -757,7 +773,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
                 unpack8(*reinterpret_cast<const uint4*>(gt0 + o0), o);
                 unpack8(*reinterpret_cast<const uint4*>(gt0 + o1), o + 8);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) d[i] = fmaf(sc[i], d[i], o[i]);
+                for (int i = 0; i < 16; i += 2) {
+                  const float2 z = __ffma2_rn(make_float2(sc[i], sc[i + 1]), make_float2(d[i], d[i + 1]),
+                                              make_float2(o[i], o[i + 1]));
+                  d[i] = z.x;
+                  d[i + 1] = z.y;
+                }
               } else {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) d[i] = sc[i] * d[i];

@@ -57,6 +57,12 @@ def kernel_class(name: str) -> str:
         return "dgrad"
     if "igemm_kernel" in name:
         return "fprop"
+    if "norm_relu_pool" in name:
+        return "norm_relu_pool"
+    if "pool_relu_bn_bwd" in name:
+        return "pool_relu_bn_bwd"
+    if "finalize_coeffs" in name:
+        return "bn_coeffs"
     for k in ("stats_finalize", "dx_coeffs", "bn_coeffs", "im2col", "avgpool", "grad_sum",
               "channel_sums", "sgd", "pack", "relu", "bn_apply"):
         if k in name:

@@ -122,7 +122,10 @@ struct Layout {
   static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
   // weights resident in smem (else streamed per stage): 3x3 unless streamed (SW); 1x1 fprop
   // when SW is set (the CTA's fixed N tile of every slab, loaded once by the producer)
-  static constexpr bool WRES = (TAPS == 9 && !SW) || (TAPS == 1 && SW);
+  static constexpr bool WRES = (TAPS == 9 && !SW) || (TAPS == 1 && SW && MODE == M_FPROP);
+  // 1x1 dgrad with SW set: the TMA epilogue (and TMA fold) is guaranteed by the host, so the
+  // register-store and register-fold paths are compiled out (fewer live registers)
+  static constexpr bool TST1 = TAPS == 1 && SW && MODE == M_DGRAD;
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
   static constexpr int CW = BN <= 32 ? 16 : (BN == 64 ? 32 : 64);
@@ -178,7 +181,7 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
 template <int BN, int RB, int TAPS, int MODE, bool SW>
 __host__ __device__ inline bool fold_tma(const WcParams& p) {
   return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW>::CW == 64 && p.tstore != 0 &&
-         p.epi >= BNFF_DG_NRC_ACC;
+         p.epi >= BNFF_DG_NRC_ACC;  // (TST1 instantiations are only launched with tstore set)
 }
 
 __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
@@ -560,8 +563,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
     // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
     // place in shared memory during the row pass and stores it back
-    const bool tfold = gb_s;
-    const bool tst = CW == 64 && p.tstore != 0 && (!fold || tfold);
+    const bool tfold = L::TST1 ? fold : gb_s;
+    const bool tst = L::TST1 ? true : (CW == 64 && p.tstore != 0 && (!fold || tfold));
     uint8_t* gb0 = smem + cv.gbuf + grp * MYCH * 128 * 128;
     const bool tx = tst && need_x;  // x tiles by TMA into 128B-swizzled rows
     // 3x3 boxes cover kt*wp (or kt*hp*wp) rows; the rows below never receive data: zero once
@@ -1555,6 +1558,14 @@ static int launch_t(WcParams p, cudaStream_t st) {
   return check_launch("wconv");
 }
 
+inline bool tst1_enabled() {  // BNFF_TST1=0: the 1x1 dgrad keeps the runtime-selected epilogue paths
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_TST1");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
 inline bool wres1_enabled() {  // BNFF_WRES1=0: stream 1x1 fprop weights per stage (A/B timing)
   static int v = -1;
   if (v < 0) {
@@ -1572,6 +1583,12 @@ static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st, int sw =
       wres1_enabled()) {
     if (BN == 128) return launch_t<128, 128, 1, MODE, true>(p, st);
     if (BN == 64) return launch_t<64, 128, 1, MODE, true>(p, st);
+  }
+  if (TAPS == 1 && MODE == M_DGRAD && RB == 128 && BN == 128 && p.tstore && tst1_enabled()) {
+    const bool xop = p.pro == BNFF_PRO_BN_DX;
+    const bool gb = p.epi >= BNFF_DG_NRC_ACC;
+    if (carve<128, 128, 1, MODE, true>(p.R, p.nslab, p.npad, 2, xop, gb).total <= SMEM_BUDGET)
+      return launch_t<128, 128, 1, MODE, true>(p, st);
   }
   if (RB == 64) {
     switch (BN) {

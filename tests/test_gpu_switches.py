@@ -18,6 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SWITCHES = [
     {"BNFF_TSTORE": "0"},
     {"BNFF_WRES1": "0"},
+    {"BNFF_TST1": "0"},
     {"BNFF_PDL": "0", "BNFF_FUSE_FINALIZE": "0", "BNFF_FUSE_NRP": "0"},
 ]
 

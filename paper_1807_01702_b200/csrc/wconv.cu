@@ -558,8 +558,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const int cp = gt % HALF, rg = gt / HALF;
     const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
     const bool nrc = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC;
-    const bool fold = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC_ACC;  // out (+)= scale * dt1
-    const bool fold_acc = MODE == M_DGRAD && p.epi == BNFF_DG_NRC_ACC;
+    // out (+)= scale * dt1: the ICF fold exists for 1x1 dgrads only (the host rejects it for 3x3),
+    // so the 3x3 instantiations carry no fold code
+    const bool fold = MODE == M_DGRAD && TAPS == 1 && p.epi >= BNFF_DG_NRC_ACC;
+    const bool fold_acc = MODE == M_DGRAD && TAPS == 1 && p.epi == BNFF_DG_NRC_ACC;
     // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
     // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
     // place in shared memory during the row pass and stores it back
@@ -1790,6 +1792,8 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.stat_part = stat_part;
   p.trace = g_wc_trace;
   if (kh == 3 && !g.sw && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
+  if (kh == 3 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
+    return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is a 1x1 dgrad epilogue");
   cudaStream_t st = (cudaStream_t)stream;
   if (mode == 0) {
     return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st, g.sw)

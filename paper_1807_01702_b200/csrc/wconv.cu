@@ -72,9 +72,13 @@ struct WcParams {
   unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
 };
 
-// event stamps of CTA 0 into p.trace[ev * 1024 + i] (debug builds of the timeline only)
+// event stamps of CTA 0 into p.trace[ev * 1024 + i]: compiled in only with -DBNFF_WC_TRACE=1
+// (tools/ab_defines.sh builds such a library for tools/trace_conv.py)
+#ifndef BNFF_WC_TRACE
+#define BNFF_WC_TRACE 0
+#endif
 __device__ __forceinline__ void trace_ev(unsigned long long* tr, int ev, int i) {
-  if (tr != nullptr && blockIdx.x == 0 && i < 1024) {
+  if (BNFF_WC_TRACE && tr != nullptr && blockIdx.x == 0 && i < 1024) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     tr[ev * 1024 + i] = t;

@@ -127,15 +127,14 @@ struct Layout {
   // weights resident in smem (else streamed per stage): 3x3 unless streamed (SW); 1x1 fprop
   // when SW is set (the CTA's fixed N tile of every slab, loaded once by the producer)
   static constexpr bool WRES = (TAPS == 9 && !SW) || (TAPS == 1 && SW && MODE == M_FPROP);
-  // 1x1 dgrad with SW set: the TMA epilogue (and TMA fold) is guaranteed by the host, so the
-  // register-store and register-fold paths are compiled out (fewer live registers)
-  static constexpr bool TST1 = TAPS == 1 && SW && MODE == M_DGRAD;
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
   static constexpr int CW = BN <= 32 ? 16 : (BN == 64 ? 32 : 64);
   static constexpr int NCH = BN / CW;                // chunks per tile (>= 2)
   static constexpr int MYCH = (NCH + 1) / 2;         // chunks per epilogue group
-  static constexpr int SROWB = CW * 2 + 16;          // staging row pitch (bytes)
+  // staging row pitch (bytes): 64-column chunks use dense 128-byte rows with the 128B swizzle
+  // (the TMA box layout); narrower chunks pad each row by 16 bytes against bank conflicts
+  static constexpr int SROWB = CW == 64 ? 128 : CW * 2 + 16;
   static constexpr int STG = 128 * SROWB;
   // per group: out staging (+ dgrad: one x buffer per owned chunk = a whole-tile lookahead)
   static constexpr int NSTG = MODE == M_DGRAD ? 1 + MYCH : 1;
@@ -184,8 +183,7 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
 // the 1x1 block-gradient fold runs through TMA (G tile loaded, folded in smem, stored back)
 template <int BN, int RB, int TAPS, int MODE, bool SW>
 __host__ __device__ inline bool fold_tma(const WcParams& p) {
-  return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW>::CW == 64 && p.tstore != 0 &&
-         p.epi >= BNFF_DG_NRC_ACC;  // (TST1 instantiations are only launched with tstore set)
+  return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW>::CW == 64 && p.epi >= BNFF_DG_NRC_ACC;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
@@ -569,8 +567,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
     // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
     // place in shared memory during the row pass and stores it back
-    const bool tfold = L::TST1 ? fold : gb_s;
-    const bool tst = L::TST1 ? true : (CW == 64 && p.tstore != 0 && (!fold || tfold));
+    // 64-column chunks always take the TMA path (the host encodes the descriptors or declines the
+    // window kernel), so the register-store / register-fold variants exist for narrow chunks only
+    const bool tfold = CW == 64 && fold;  // == gb_s (fold_tma)
+    constexpr bool tst = CW == 64;
     uint8_t* gb0 = smem + cv.gbuf + grp * MYCH * 128 * 128;
     const bool tx = tst && need_x;  // x tiles by TMA into 128B-swizzled rows
     // 3x3 boxes cover kt*wp (or kt*hp*wp) rows; the rows below never receive data: zero once
@@ -1540,14 +1540,6 @@ static int launch_t(WcParams p, cudaStream_t st) {
     c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop, gb);
     if (c.total <= SMEM_BUDGET) break;
   }
-  if (stages < 2 && gb) {  // no room for the fold tiles: register read-modify-write epilogue
-    p.tstore = 0;
-    gb = false;
-    for (stages = 8; stages >= 2; --stages) {
-      c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop, gb);
-      if (c.total <= SMEM_BUDGET) break;
-    }
-  }
   if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
   p.stages = stages;
   static int attr = 0;
@@ -1564,14 +1556,6 @@ static int launch_t(WcParams p, cudaStream_t st) {
   return check_launch("wconv");
 }
 
-inline bool tst1_enabled() {  // BNFF_TST1=0: the 1x1 dgrad keeps the runtime-selected epilogue paths
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("BNFF_TST1");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v != 0;
-}
 inline bool wres1_enabled() {  // BNFF_WRES1=0: stream 1x1 fprop weights per stage (A/B timing)
   static int v = -1;
   if (v < 0) {
@@ -1589,12 +1573,6 @@ static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st, int sw =
       wres1_enabled()) {
     if (BN == 128) return launch_t<128, 128, 1, MODE, true>(p, st);
     if (BN == 64) return launch_t<64, 128, 1, MODE, true>(p, st);
-  }
-  if (TAPS == 1 && MODE == M_DGRAD && RB == 128 && BN == 128 && p.tstore && tst1_enabled()) {
-    const bool xop = p.pro == BNFF_PRO_BN_DX;
-    const bool gb = p.epi >= BNFF_DG_NRC_ACC;
-    if (carve<128, 128, 1, MODE, true>(p.R, p.nslab, p.npad, 2, xop, gb).total <= SMEM_BUDGET)
-      return launch_t<128, 128, 1, MODE, true>(p, st);
   }
   if (RB == 64) {
     switch (BN) {
@@ -1636,14 +1614,6 @@ static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw =
   }
 #undef BNFF_FIT
   return c.total <= SMEM_BUDGET;
-}
-inline bool tstore_enabled() {  // BNFF_TSTORE=0: stores from the epilogue threads (A/B timing)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("BNFF_TSTORE");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v != 0;
 }
 }  // namespace wc
 }  // namespace bnff
@@ -1764,9 +1734,10 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
     box[0] = slabw; box[1] = 128;
   }
   p.tiles = p.mtiles * p.ntiles;
-  // TMA-store epilogue: 64-column chunks (BN >= 128), not the fold (read-modify-write) modes
+  // TMA epilogue for 64-column chunks (BN >= 128): the output (and dgrad x mask) descriptors are
+  // required; if they cannot be encoded the window kernel declines (generic implicit GEMM)
   p.tstore = 0;
-  if (g.BN >= 128 && (epi < BNFF_DG_NRC_ACC || kh == 1) && wc::tstore_enabled()) {
+  if (g.BN >= 128) {
     uint32_t ob[4];
     if (kh == 3) {
       ob[0] = 64; ob[1] = p.wp; ob[2] = p.tmode == 2 ? p.hp : p.kt; ob[3] = p.tmode == 2 ? p.kt : 1;
@@ -1777,6 +1748,7 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
     if (p.tstore && mode == 1 && epi != BNFF_DG_PLAIN &&
         !encode_nhwc_bf16(&p.tma_ex, ex.ptr, ex.n, ex.h, ex.w, ex.c, ex.row_stride, rank, ob))
       p.tstore = 0;
+    if (!p.tstore) return wc::kWindowNoFit;
   }
   if (!encode_nhwc_bf16(&p.tma_a, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
     return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (window operand)");

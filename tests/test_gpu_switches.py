@@ -1,6 +1,5 @@
 """The library's A/B switches select code paths that stay reachable in
-production (e.g. the register epilogue when a TMA descriptor cannot be encoded or the fold
-tiles do not fit).  The switches are read once per process, so each configuration runs in a
+production.  The switches are read once per process, so each configuration runs in a
 subprocess: the window-vs-generic kernel check of tools/bench_conv.py and the ICF fold /
 stem / padded-model parity tests of test_gpu_parity.py."""
 
@@ -16,9 +15,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SWITCHES = [
-    {"BNFF_TSTORE": "0"},
     {"BNFF_WRES1": "0"},
-    {"BNFF_TST1": "0"},
     {"BNFF_PDL": "0", "BNFF_FUSE_FINALIZE": "0", "BNFF_FUSE_NRP": "0"},
 ]
 

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include "sm100.cuh"
+#include <type_traits>
 #include "common.cuh"
 
 namespace bnff {
@@ -370,8 +371,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // =============================== transform warps ===============================
     // wait for a stage's TMA box, apply the operand prologue in place (halo / border
     // positions stay zero: padding applies after normalize/ReLU), arrive on full_bar.
+    // the operand prologue kind is a compile-time constant inside the loop (one copy per kind)
+    auto transform = [&](auto pro_c) {
+    constexpr int PRO = decltype(pro_c)::value;
     const int j = tid % CPR, r0 = tid / CPR;
-    const bool need_t = p.pro != BNFF_PRO_NONE;
+    const bool need_t = PRO != BNFF_PRO_NONE;
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < ntl; ++it) {
@@ -408,9 +412,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             float f[8];
             unpack8(*reinterpret_cast<const uint4*>(A + off), f);
             uint4 o;
-            if (p.pro == BNFF_PRO_RELU) {
+            if (PRO == BNFF_PRO_RELU) {
               o = pack8(f, true);
-            } else if (p.pro == BNFF_PRO_BN_RELU) {  // paired FFMA2: same RN fp32 FMAs, half the issues
+            } else if (PRO == BNFF_PRO_BN_RELU) {  // paired FFMA2: same RN fp32 FMAs, half the issues
 #pragma unroll
               for (int i = 0; i < 8; i += 2) {
                 const float2 r2 = __ffma2_rn(make_float2(f[i], f[i + 1]), make_float2(t0[i], t0[i + 1]),
@@ -440,6 +444,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         if (tid == 0) trace_ev(p.trace, 3, it * p.nslab + s);
         if (++st == ST) { st = 0; ph ^= 1u; }
       }
+    }
+    };
+    switch (p.pro) {
+      case BNFF_PRO_RELU: transform(std::integral_constant<int, BNFF_PRO_RELU>{}); break;
+      case BNFF_PRO_BN_RELU: transform(std::integral_constant<int, BNFF_PRO_BN_RELU>{}); break;
+      case BNFF_PRO_BN_DX: transform(std::integral_constant<int, BNFF_PRO_BN_DX>{}); break;
+      default: transform(std::integral_constant<int, BNFF_PRO_NONE>{}); break;
     }
   } else if (warp == PRODUCER) {
     // =============================== TMA producer ===============================

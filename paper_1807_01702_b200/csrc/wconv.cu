@@ -554,6 +554,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // thread = column pair, accumulated in registers), store pass (coalesced 16B stores
     // into the NHWC view).  Dgrad: the x tile for the NRC/CLIP mask is fetched one tile
     // ahead, chunk buffer by chunk buffer.
+    // the dgrad epilogue kind is a compile-time constant inside the tile loop (one copy per kind)
+    auto epilogue = [&](auto epi_c) {
+    constexpr int EPI = decltype(epi_c)::value;
     const int quad = warp & 3;
     const int et = tid - (NLW + 1) * 32;     // 0..255
     const int grp = et >> 7;                 // 0 / 1
@@ -569,12 +572,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     constexpr int HALF = CW / 2;             // column pairs per chunk
     constexpr int RG = 128 / HALF;           // row groups in the column pass
     const int cp = gt % HALF, rg = gt / HALF;
-    const bool need_x = MODE == M_DGRAD && p.epi != BNFF_DG_PLAIN;
-    const bool nrc = MODE == M_DGRAD && p.epi >= BNFF_DG_NRC;
+    const bool need_x = MODE == M_DGRAD && EPI != BNFF_DG_PLAIN;
+    const bool nrc = MODE == M_DGRAD && EPI >= BNFF_DG_NRC;
     // out (+)= scale * dt1: the ICF fold exists for 1x1 dgrads only (the host rejects it for 3x3),
     // so the 3x3 instantiations carry no fold code
-    const bool fold = MODE == M_DGRAD && TAPS == 1 && p.epi >= BNFF_DG_NRC_ACC;
-    const bool fold_acc = MODE == M_DGRAD && TAPS == 1 && p.epi == BNFF_DG_NRC_ACC;
+    const bool fold = MODE == M_DGRAD && TAPS == 1 && EPI >= BNFF_DG_NRC_ACC;
+    const bool fold_acc = MODE == M_DGRAD && TAPS == 1 && EPI == BNFF_DG_NRC_ACC;
     // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
     // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
     // place in shared memory during the row pass and stores it back
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
                 unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2), xv);
                 unpack8(*reinterpret_cast<const uint4*>(xrow + c16 * 2 + 16), xv + 8);
               }
-              if (p.epi == BNFF_DG_CLIP) {
+              if (EPI == BNFF_DG_CLIP) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = xv[i] > 0.f ? v[i] : 0.f;
               } else {
@@ -924,6 +927,22 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         if (n00 + c >= p.N) continue;
         p.stat_part[((long long)blockIdx.x * 2 + 0) * p.N + n00 + c] = sacc[c];
         p.stat_part[((long long)blockIdx.x * 2 + 1) * p.N + n00 + c] = sacc[BN + c];
+      }
+    }
+    };
+    if (MODE == M_FPROP) {
+      epilogue(std::integral_constant<int, BNFF_DG_PLAIN>{});
+    } else {
+      switch (p.epi) {
+        case BNFF_DG_CLIP: epilogue(std::integral_constant<int, BNFF_DG_CLIP>{}); break;
+        case BNFF_DG_NRC: epilogue(std::integral_constant<int, BNFF_DG_NRC>{}); break;
+        case BNFF_DG_NRC_ACC:
+          if constexpr (TAPS == 1) epilogue(std::integral_constant<int, BNFF_DG_NRC_ACC>{});
+          break;
+        case BNFF_DG_NRC_SET:
+          if constexpr (TAPS == 1) epilogue(std::integral_constant<int, BNFF_DG_NRC_SET>{});
+          break;
+        default: epilogue(std::integral_constant<int, BNFF_DG_PLAIN>{}); break;
       }
     }
   }

@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
           float2 a = acc1[k], b = acc2[k];
           if (MODE == M_FPROP) {
-#pragma unroll 16
+#pragma unroll 32
             for (int r = rg; r < 128; r += RG) {
               const uint32_t wv = tst ? s32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
                                       : s32[r * (L::SROWB / 4) + cp];
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             const int gc = n0 + cc + 2 * cp;
             const float2 hinv = make_float2(etab[2 * p.npad + gc], etab[2 * p.npad + gc + 1]);
             const float2 hsh = make_float2(etab[3 * p.npad + gc], etab[3 * p.npad + gc + 1]);
-#pragma unroll 16
+#pragma unroll 32
             for (int r = rg; r < 128; r += RG) {
               const uint32_t wv = tst ? s32[r * 32 + ((((cp >> 2) ^ (r & 7)) << 2) | (cp & 3))]
                                       : s32[r * (L::SROWB / 4) + cp];

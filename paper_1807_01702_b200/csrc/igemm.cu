@@ -172,7 +172,8 @@ __device__ __forceinline__ void st_chunk(uint8_t* plane0, uint8_t* plane1, uint3
   } else {
     float4 hi, lo;
     hi.x = tf32_hi(f[0]); hi.y = tf32_hi(f[1]); hi.z = tf32_hi(f[2]); hi.w = tf32_hi(f[3]);
-    lo.x = f[0] - hi.x; lo.y = f[1] - hi.y; lo.z = f[2] - hi.z; lo.w = f[3] - hi.w;
+    lo.x = tf32_rn(f[0] - hi.x); lo.y = tf32_rn(f[1] - hi.y);
+    lo.z = tf32_rn(f[2] - hi.z); lo.w = tf32_rn(f[3] - hi.w);
     *reinterpret_cast<float4*>(plane0 + off) = hi;
     *reinterpret_cast<float4*>(plane1 + off) = lo;
   }
@@ -743,7 +744,9 @@ static int dispatch(int dtype, const IgParams& p, int bn, bool hasx, cudaStream_
     if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, __nv_bfloat16, true>(p, bn, st);
     return dispatch_bn<MODE, __nv_bfloat16, false>(p, bn, st);
   }
-  if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, float, true>(p, bn, st);
+  // 3xTF32 stages carry hi/lo planes: a 256-wide B tile plus the x tile of a deferred-dx
+  // prologue would not fit two stages in shared memory, so those run as 128-wide N tiles
+  if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, float, true>(p, bn > 128 ? 128 : bn, st);
   return dispatch_bn<MODE, float, false>(p, bn, st);
 }
 

@@ -208,9 +208,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ float tf32_hi(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// round-to-nearest TF32 (low 13 mantissa bits zero).  3xTF32 splits x = hi + lo with both
+// parts rounded to nearest: |x - hi - lo| <= 2^-22 |x| (truncating either part costs 4x)
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
+__device__ __forceinline__ float tf32_hi(float x) { return tf32_rn(x); }
 
 }  // namespace bnff
 

@@ -588,6 +588,8 @@ class Engine:
         self._f_Concat(node)
         y = self.acts[node.outputs[0]]
         st = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
+        if self.sync_bn:  # the pieces' moments are over the global batch (_emit_stats_finalize)
+            st.count *= self.world
         off = 0
         for fs, ss in zip(feat, stat):
             piece = self.stats[ss]
@@ -660,6 +662,7 @@ class Engine:
             n, oh, ow, kp = colt.shape
             ws = max(ws, self.L.bnff_wgrad_workspace(n, oh, ow, 1, 1, kp, c1.out_c, 0))
         self.wg_ws = self._empty((ws,), torch.float32)
+        self._side_reads: list = []  # tensors read by side-stream thunks (pending until the join)
         for node in reversed(g.nodes):
             try:
                 getattr(self, "_b_" + node.kind)(node)
@@ -735,6 +738,8 @@ class Engine:
         extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
         # the weight gradient is off the critical path: it runs on the side stream, forked
         # before this conv's dgrad (they read the same dy) and joined at the end of backward
+        if self.side_wgrad:
+            self._side_reads += [dy, dy_x]
         self._emit(self.L.bnff_conv_wgrad, C.byref(wa), what=f"wgrad {node.name}",
                    nbytes=_nb(wx, dy) + extra + 4 * wconv.out_c * wconv.in_c * wconv.kh * wconv.kw,
                    flops=flops, launches=4, side=self.side_wgrad)
@@ -885,9 +890,9 @@ class Engine:
         if prod is not None and prod.kind == G.SPLIT:
             sib = next(o for o in prod.outputs if o != sid)
             sg = self.grads.get(sib)
-            if isinstance(sg, Plain) and any(sg.t.untyped_storage().data_ptr() == t.untyped_storage().data_ptr()
-                                             for t in self.loss_grad.values()):
-                return None  # never accumulate into the caller's loss-gradient buffer
+            tgt = sg.t if isinstance(sg, Plain) else sg.dt1 if isinstance(sg, Deferred) else None
+            if tgt is not None and not self._writable(tgt):
+                return None  # the caller's loss gradient, or still read by a side-stream wgrad
             if isinstance(sg, Plain) and tuple(sg.t.shape) == tuple(x.shape):
                 return sg.t, sib, _lib.DG_NRC_ACC, grp, lo
             if isinstance(sg, Deferred) and sg.affine and tuple(sg.dt1.shape) == tuple(x.shape):
@@ -972,8 +977,9 @@ class Engine:
         if len(branches) == 1:
             self._add_grad(node.inputs[0], branches[0])
             return
-        # in place into a plain branch's storage when one exists (block gradient buffer)
-        out = next((b.t for b in branches if isinstance(b, Plain)), None)
+        # in place into a plain branch's storage when that is safe (a block gradient buffer
+        # this backward wrote), else into a fresh buffer
+        out = next((b.t for b in branches if isinstance(b, Plain) and self._writable(b.t)), None)
         if out is None:
             out = self._fresh_like(branches[0].dt1)
         terms = (_lib.GradTerm * len(branches))()
@@ -987,6 +993,30 @@ class Engine:
         self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, len(branches),
                    what="split_bwd", nbytes=nb)
         self._add_grad(node.inputs[0], Plain(out))
+
+    @staticmethod
+    def _footprint(t):
+        """(storage, first channel, last channel + 1, row stride) of an NHWC view."""
+        rs = t.stride(2)
+        lo = t.storage_offset() % rs if rs else 0
+        return t.untyped_storage().data_ptr(), lo, lo + t.shape[3], rs
+
+    def _overlaps(self, a, b):
+        sa, la, ha, ra = self._footprint(a)
+        sb, lb, hb, rb = self._footprint(b)
+        if sa != sb:
+            return False
+        if ra != rb:
+            return True  # differently strided views of one storage: assume they alias
+        return la < hb and lb < ha
+
+    def _writable(self, t) -> bool:
+        """May backward overwrite t in place?  Not the caller's loss gradient (graph replays
+        and repeated backward() read it again), and not a tensor a side-stream weight
+        gradient still has to read (the side stream joins only at the end of the pass)."""
+        if any(self._overlaps(t, lg) for lg in self.loss_grad.values()):
+            return False
+        return not any(self._overlaps(t, r) for r in self._side_reads)
 
     def _b_EltwiseSum(self, node):
         dy = self._incoming(node.outputs[0])

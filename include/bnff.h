@@ -13,7 +13,7 @@
  *  - dtype BNFF_BF16: bf16 storage, bf16 tcgen05 MMA (kind::f16), fp32 accumulate.
  *    dtype BNFF_F32 : fp32 storage, 3xTF32 split tcgen05 MMA (kind::tf32, ~fp32).
  *  - Channel counts and channel offsets must be multiples of 8 (bf16) / 4 (f32).
- *  - Per-channel statistics are float64; per-tile partials are float32 and are
+ *  - Per-channel statistics are float64; per-tile partials are float64 and are
  *    combined in a fixed order (bitwise run-to-run deterministic, no atomics).
  *  - No allocation, no host synchronisation; all work is ordered on `stream`
  *    (a cudaStream_t, NULL = legacy default stream).
@@ -79,7 +79,7 @@ typedef struct {
   const float* bias;  /* c_out, nullable */
   int32_t x_pro;      /* BNFF_PRO_NONE / RELU / BN_RELU */
   bnff_coef x_coef;
-  float* stat_part;   /* nullable: sum/sumsq partials [bnff_stat_rows()][2][c_out] of the stored y */
+  double* stat_part;  /* nullable: sum/sumsq partials [bnff_stat_rows()][2][c_out] of the stored y */
   const void* wwin;   /* nullable: window-layout weights (bnff_pack_window, fwd); selects the
                          window-shift kernel when bnff_window_ok() */
 } bnff_fprop_args;
@@ -96,7 +96,7 @@ typedef struct {
   const void* wpack_t;/* packed transposed weights [c_in][kh*kw*c_out (padded)] */
   int32_t epi;        /* BNFF_DG_* */
   bnff_coef x_coef;   /* NRC: a = mean, b = scale, c = beta, d = invstd */
-  float* stat_part;   /* NRC: partials [bnff_stat_rows()][2][c_in] of (sum dt1, sum dt1*xhat) */
+  double* stat_part;  /* NRC: partials [bnff_stat_rows()][2][c_in] of (sum dt1, sum dt1*xhat) */
   const void* wwin;   /* nullable: window-layout weights (bnff_pack_window, dgrad) */
 } bnff_dgrad_args;
 
@@ -178,7 +178,7 @@ int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy
 int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                      int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
                      const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
-                     float* stat_part, void* stream);
+                     double* stat_part, void* stream);
 
 /* K5: channel sums over an NHWC view -> partials [tiles][2][c]:
  *   mode 0: (x, x^2)                         -- bn_stats_onepass (ops.py:231-237)
@@ -188,18 +188,18 @@ int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_v
  *   mode 2: (dy, 0)                          -- conv dbias (ops.py:203)                */
 int32_t bnff_sum_tiles(int64_t pixels);
 int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_view dy, bnff_coef coef,
-                      float* part, void* stream);
+                      double* part, void* stream);
 /* K4: partials -> float64 (sum, sumsq) and (mean, var) per channel plus the fp32
  * prologue table (mean32, scale32 = gamma*invstd, beta32, invstd32)
  * (ChannelStats.from_sums / inv_std, ops.py:109-116).  Writes sums at channel
  * offset `c_off` of the f64 arrays so per-piece stats assemble in place
  * (concat_stats, ops.py:128-143).                                               */
-int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count,
+int bnff_stats_finalize(const double* part, int32_t tiles, int32_t c, int64_t count,
                         double* sum, double* sumsq, double* mean, double* var, void* stream);
 /* two-pass centred variance for the unfused BN (ops.py:212-228): var from x and mean */
-int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, float* part,
+int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, double* part,
                       void* stream);
-int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+int bnff_var_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
                       void* stream);
 int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
                    const float* beta, float eps, float* mean32, float* scale32, float* beta32,
@@ -207,7 +207,7 @@ int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float
 /* bnff_stats_finalize of a freshly produced piece (channels [c_off, c_off+c_new) of c_total)
  * fused with the consumer's bnff_bn_coeffs over all c_total channels (the other channels'
  * mean/var are read from mean_all/var_all): one launch per ICF concatenation step.        */
-int bnff_stats_finalize_coeffs(const float* part, int32_t tiles, int32_t c_new, int64_t count,
+int bnff_stats_finalize_coeffs(const double* part, int32_t tiles, int32_t c_new, int64_t count,
                                double* sum, double* sumsq, double* mean, double* var, int32_t c_off,
                                int32_t c_total, const double* mean_all, const double* var_all,
                                const float* gamma, const float* beta, float eps, float* mean32,
@@ -215,7 +215,7 @@ int bnff_stats_finalize_coeffs(const float* part, int32_t tiles, int32_t c_new, 
 /* backward coefficient table from the reduced (dgamma, dbeta) sums:
  * k1 = dbeta/m, k2 = dgamma/m, g = gamma*invstd (ops.py:287-293). Also writes
  * the fp32 parameter gradients dgamma32/dbeta32 (nullable). */
-int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count,
+int bnff_dx_coeffs(int32_t c, const double* part, int32_t tiles, int64_t count,
                    const double* mean, const double* var, const float* gamma, float eps,
                    double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
                    float* mean32, float* inv32, float* dgamma32, float* dbeta32, void* stream);
@@ -224,7 +224,7 @@ int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count,
  * (acc_init = 1 overwrites), and mean32/inv32 written into the caller's block-level
  * arrays, so the block gradient resolves as G - acc_a - acc_b*xhat when its producer
  * reads it (bn_dx_from_sums ops.py:283-298 re-associated over consumers).            */
-int bnff_dx_coeffs_acc(int32_t c, const float* part, int32_t tiles, int64_t count,
+int bnff_dx_coeffs_acc(int32_t c, const double* part, int32_t tiles, int64_t count,
                        const double* mean, const double* var, const float* gamma, float eps,
                        double* dgamma64, double* dbeta64, float* k1, float* k2, float* g,
                        float* mean32, float* inv32, float* dgamma32, float* dbeta32,
@@ -260,7 +260,7 @@ int bnff_grad_sum(int32_t dtype, bnff_view out, int32_t accumulate, const bnff_g
 int bnff_relu_fwd(int32_t dtype, bnff_view x, bnff_view y, void* stream);
 int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view dx, void* stream);
 /* K9: avgpool k x k non-overlapping (ops.py:428-454); optional fused stats partials */
-int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, float* stat_part,
+int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, double* stat_part,
                      void* stream);
 int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void* stream);
 /* K9b: sub-BN2 -> ReLU -> k x k average pool in one pass (a chain whose consumer is a pool,
@@ -268,9 +268,9 @@ int bnff_avgpool_bwd(int32_t dtype, bnff_view dy, bnff_view dx, int32_t k, void*
  * backward dt1 = [bn(x) > 0] * spread(dy)/k^2 with (sum dt1, sum dt1*xhat) partials (xhat =
  * (x-a)*d), i.e. avgpool_bwd + relu_bwd + bn_bwd sums (ops.py:271-274, 314-319, 428-454). */
 int bnff_norm_relu_pool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, bnff_coef coef,
-                            float* stat_part, void* stream);
+                            double* stat_part, void* stream);
 int bnff_pool_relu_bn_bwd(int32_t dtype, bnff_view dy, bnff_view x, bnff_view dt1, int32_t k,
-                          bnff_coef coef, float* part, void* stream);
+                          bnff_coef coef, double* part, void* stream);
 /* K10: y = a + zero-channel-padded b (execute.py:266-280) */
 int bnff_ews_fwd(int32_t dtype, bnff_view a, bnff_view b, bnff_view y, void* stream);
 /* K11: copy a view into another (physical concat piece / gradient slice copy) */

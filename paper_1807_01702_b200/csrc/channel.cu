@@ -6,6 +6,7 @@
 // to a [tiles][2][C] buffer, then combined in a fixed order in float64.
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include "sm100.cuh"
@@ -66,19 +67,19 @@ __device__ __forceinline__ float bn_dx_elem(float dt, float x, int c, const bnff
 // partials [tiles][2][C] -> float64 totals, one launch: block = 32 channels x 8 row
 // groups; every (row group, channel) sum is a fixed-order loop, then a fixed-order
 // combine of the 8 groups (bitwise deterministic)
-__device__ __forceinline__ void reduce_two(const float* __restrict__ part, int tiles, int C, int c,
+__device__ __forceinline__ void reduce_two(const double* __restrict__ part, int tiles, int C, int c,
                                            double& o1, double& o2) {
   // block = 32 channels x 16 row groups; loads of one thread are independent (unrolled)
   __shared__ double sh[2][16][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double a = 0.0, b = 0.0;
   if (c < C) {
-    float va[12], vb[12];
+    double va[12], vb[12];
 #pragma unroll
     for (int u = 0; u < 12; ++u) {
       const int t = ty + 16 * u;
-      va[u] = t < tiles ? part[((long long)t * 2 + 0) * C + c] : 0.f;
-      vb[u] = t < tiles ? part[((long long)t * 2 + 1) * C + c] : 0.f;
+      va[u] = t < tiles ? part[((long long)t * 2 + 0) * C + c] : 0.0;
+      vb[u] = t < tiles ? part[((long long)t * 2 + 1) * C + c] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 12; ++u) { a += (double)va[u]; b += (double)vb[u]; }
@@ -96,7 +97,7 @@ __device__ __forceinline__ void reduce_two(const float* __restrict__ part, int t
   }
 }
 
-__global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __restrict__ part, int tiles, int C,
+__global__ void __launch_bounds__(512) stats_finalize_kernel(const double* __restrict__ part, int tiles, int C,
                                                              long long count, double* sum, double* sumsq,
                                                              double* mean, double* var) {
   griddep_launch();
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(512) stats_finalize_kernel(const float* __rest
 // fused with the next consumer's bn_coeffs over all c_total channels (ICF: concat_stats +
 // ChannelStats.from_sums + inv_std, ops.py:109-143; one launch instead of two)
 __global__ void __launch_bounds__(512) finalize_coeffs_kernel(
-    const float* __restrict__ part, int tiles, int c_new, long long count, double* sum, double* sumsq,
+    const double* __restrict__ part, int tiles, int c_new, long long count, double* sum, double* sumsq,
     double* mean, double* var, int c_off, int c_total, const double* mean_all, const double* var_all,
     const float* gamma, const float* beta, float eps, float* mean32, float* scale32, float* beta32,
     float* inv32) {
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(512) finalize_coeffs_kernel(
 }
 
 __global__ void __launch_bounds__(512) dx_coeffs_fused_kernel(
-    const float* __restrict__ part, int tiles, int C, long long count, const double* mean,
+    const double* __restrict__ part, int tiles, int C, long long count, const double* mean,
     const double* var, const float* gamma, float eps, double* dgamma64, double* dbeta64, float* k1,
     float* k2, float* g, float* mean32, float* inv32, float* dgamma32, float* dbeta32, float* acc_a,
     float* acc_b, int acc_init) {
@@ -197,7 +198,7 @@ __global__ void stats_from_sums_kernel(int C, long long count, const double* sum
 }
 
 // partials -> float64 totals of one slot (kept for the centred-variance path)
-__global__ void reduce_parts_kernel(const float* __restrict__ part, int tiles, int C, int slot,
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int tiles, int C, int slot,
                                     double* __restrict__ out) {
   griddep_launch();
   griddep_wait();
@@ -398,11 +399,14 @@ __host__ __device__ inline int sum_tiles(long long pixels) {
 // = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double)
 template <typename T>
 __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
-                                    bnff_coef cf, const double* mean64, float* part) {
+                                    bnff_coef cf, const double* mean64, double* part) {
   griddep_launch();
   griddep_wait();
   constexpr int V = VecIO<T>::V;
-  __shared__ float sh[2][kSumThreads][V];
+  // fp32 data accumulates in float64 (the reference's bn_stats_onepass sums in f64,
+  // ops.py:231-237); bf16 values (8-bit significands) accumulate in fp32
+  using Acc = typename std::conditional<sizeof(T) == 4, double, float>::type;
+  __shared__ Acc sh[2][kSumThreads][V];
   const int cpr = C / V;
   const int tiles = gridDim.x;
   const long long rows_per_tile = (pixels + tiles - 1) / tiles;
@@ -414,9 +418,9 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
     const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
     const bool active = trow < rows_per_iter;
     const int c0 = (cbase + tcol) * V;
-    float s1[V], s2[V];
+    Acc s1[V], s2[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = Acc(0);
     if (active) {
       // per-channel coefficients hoisted out of the row loop
       float ca[V], cb[V];
@@ -442,8 +446,8 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-              s1[i] += f[u][i];
-              s2[i] += f[u][i] * f[u][i];
+              s1[i] += (Acc)f[u][i];
+              s2[i] += (Acc)f[u][i] * (Acc)f[u][i];
             }
         }
       }
@@ -458,16 +462,16 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
 #pragma unroll
         for (int i = 0; i < V; ++i) {
           if (mode == 0) {
-            s1[i] += v[i];
-            s2[i] += v[i] * v[i];
+            s1[i] += (Acc)v[i];
+            s2[i] += (Acc)v[i] * (Acc)v[i];
           } else if (mode == 1) {
             const float xh = __fmul_rn(__fsub_rn(x[i], ca[i]), cb[i]);
-            s1[i] += v[i];
-            s2[i] += v[i] * xh;
+            s1[i] += (Acc)v[i];
+            s2[i] += (Acc)v[i] * (Acc)xh;
           } else if (mode == 2) {
-            s1[i] += dx2 ? dxc.apply(v[i], x[i], i) : v[i];
+            s1[i] += (Acc)(dx2 ? dxc.apply(v[i], x[i], i) : v[i]);
           } else {
-            const float d = (float)((double)v[i] - m64[i]);
+            const Acc d = (Acc)((double)v[i] - m64[i]);
             s1[i] += d * d;
           }
         }
@@ -481,9 +485,9 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
     __syncthreads();
     // fixed-order combine of the rows_per_iter threads sharing a column
     if (threadIdx.x < ccount) {
-      float a[V], b[V];
+      Acc a[V], b[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int i = 0; i < V; ++i) a[i] = b[i] = Acc(0);
       for (int rr = 0; rr < rows_per_iter; ++rr) {
 #pragma unroll
         for (int i = 0; i < V; ++i) {
@@ -604,11 +608,12 @@ __global__ void __launch_bounds__(256) relu_kernel(View x, View dy, View out, lo
 // as channel_sums: tile = range of output pixels)
 template <typename T>
 __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, int ow, int C, int k,
-                                   float* part) {
+                                   double* part) {
   griddep_launch();
   griddep_wait();
   constexpr int V = VecIO<T>::V;
-  __shared__ float sh[2][kSumThreads][V];
+  using Acc = typename std::conditional<sizeof(T) == 4, double, float>::type;  // f64 for fp32 data
+  __shared__ Acc sh[2][kSumThreads][V];
   const long long pixels = (long long)n * oh * ow;
   const int cpr = C / V;
   const int tiles = gridDim.x;
@@ -621,9 +626,9 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
     const int rows_per_iter = kSumThreads / ccount;
     const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
     const int c0 = (cbase + tcol) * V;
-    float s1[V], s2[V];
+    Acc s1[V], s2[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = Acc(0);
     if (trow < rows_per_iter) {
       for (long long r = r_begin + trow; r < r_end; r += rows_per_iter) {
         const int img = (int)(r / ((long long)oh * ow));
@@ -656,8 +661,8 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
         VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, acc);
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          s1[i] += acc[i];
-          s2[i] += acc[i] * acc[i];
+          s1[i] += (Acc)(acc[i]);
+          s2[i] += (Acc)acc[i] * (Acc)(acc[i]);
         }
       }
     }
@@ -669,9 +674,9 @@ __global__ void avgpool_fwd_kernel(View x, View y, int n, int h, int w, int oh, 
     }
     __syncthreads();
     if (threadIdx.x < ccount) {
-      float a[V], b[V];
+      Acc a[V], b[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int i = 0; i < V; ++i) a[i] = b[i] = Acc(0);
       for (int rr = 0; rr < rows_per_iter; ++rr)
 #pragma unroll
         for (int i = 0; i < V; ++i) {
@@ -757,11 +762,12 @@ __global__ void __launch_bounds__(256) avgpool_wide_kernel(View x, View y, int h
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, int oh, int ow, int C, int k,
-                                          bnff_coef cf, float* part) {
+                                          bnff_coef cf, double* part) {
   griddep_launch();
   griddep_wait();
   constexpr int V = VecIO<T>::V;
-  __shared__ float sh[2][kSumThreads][V];
+  using Acc = typename std::conditional<sizeof(T) == 4, double, float>::type;  // f64 for fp32 data
+  __shared__ Acc sh[2][kSumThreads][V];
   const long long pixels = (long long)n * oh * ow;
   const int cpr = C / V;
   const int tiles = gridDim.x;
@@ -774,9 +780,10 @@ __global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, i
     const int rows_per_iter = kSumThreads / ccount;
     const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
     const int c0 = (cbase + tcol) * V;
-    float s1[V], s2[V], ma[V], sc[V], be[V];
+    Acc s1[V], s2[V];
+    float ma[V], sc[V], be[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = Acc(0);
     if (trow < rows_per_iter) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
@@ -805,8 +812,8 @@ __global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, i
         VecIO<T>::store(const_cast<void*>(y.p), r * y.rs + c0, acc);
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          s1[i] += acc[i];
-          s2[i] += acc[i] * acc[i];
+          s1[i] += (Acc)(acc[i]);
+          s2[i] += (Acc)acc[i] * (Acc)(acc[i]);
         }
       }
     }
@@ -818,9 +825,9 @@ __global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, i
     }
     __syncthreads();
     if (threadIdx.x < ccount) {
-      float a[V], b[V];
+      Acc a[V], b[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int i = 0; i < V; ++i) a[i] = b[i] = Acc(0);
       for (int rr = 0; rr < rows_per_iter; ++rr)
 #pragma unroll
         for (int i = 0; i < V; ++i) {
@@ -840,11 +847,12 @@ __global__ void norm_relu_pool_fwd_kernel(View x, View y, int n, int h, int w, i
 
 template <typename T>
 __global__ void pool_relu_bn_bwd_kernel(View dyp, View x, View dr, int n, int h, int w, int oh, int ow, int C,
-                                        int k, bnff_coef cf, float* part) {
+                                        int k, bnff_coef cf, double* part) {
   griddep_launch();
   griddep_wait();
   constexpr int V = VecIO<T>::V;
-  __shared__ float sh[2][kSumThreads][V];
+  using Acc = typename std::conditional<sizeof(T) == 4, double, float>::type;  // f64 for fp32 data
+  __shared__ Acc sh[2][kSumThreads][V];
   const long long pixels = (long long)n * h * w;
   const int cpr = C / V;
   const int tiles = gridDim.x;
@@ -857,9 +865,10 @@ __global__ void pool_relu_bn_bwd_kernel(View dyp, View x, View dr, int n, int h,
     const int rows_per_iter = kSumThreads / ccount;
     const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
     const int c0 = (cbase + tcol) * V;
-    float s1[V], s2[V], ma[V], sc[V], be[V], iv[V];
+    Acc s1[V], s2[V];
+    float ma[V], sc[V], be[V], iv[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = Acc(0);
     if (trow < rows_per_iter) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
@@ -886,8 +895,8 @@ __global__ void pool_relu_bn_bwd_kernel(View dyp, View x, View dr, int n, int h,
           const float z = __fadd_rn(__fmul_rn(__fsub_rn(xf[i], ma[i]), sc[i]), be[i]);
           d[i] = VecIO<T>::round(z > 0.f ? VecIO<T>::round(d[i] * inv) : 0.f);
           const float xh = __fmul_rn(__fsub_rn(xf[i], ma[i]), iv[i]);
-          s1[i] += d[i];
-          s2[i] += d[i] * xh;
+          s1[i] += (Acc)(d[i]);
+          s2[i] += (Acc)d[i] * (Acc)(xh);
         }
         VecIO<T>::store(const_cast<void*>(dr.p), r * dr.rs + c0, d);
       }
@@ -899,9 +908,9 @@ __global__ void pool_relu_bn_bwd_kernel(View dyp, View x, View dr, int n, int h,
     }
     __syncthreads();
     if (threadIdx.x < ccount) {
-      float a[V], b[V];
+      Acc a[V], b[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = 0.f;
+      for (int i = 0; i < V; ++i) a[i] = b[i] = Acc(0);
       for (int rr = 0; rr < rows_per_iter; ++rr)
 #pragma unroll
         for (int i = 0; i < V; ++i) {
@@ -1127,7 +1136,7 @@ extern "C" int bnff_device_ok(void) {
 extern "C" int32_t bnff_sum_tiles(int64_t pixels) { return sum_tiles(pixels); }
 
 extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_view dy, bnff_coef coef,
-                                 float* part, void* stream) {
+                                 double* part, void* stream) {
   int rc;
   const bnff_view& shape = (mode == 0) ? x : dy;
   if ((rc = check_view(dtype, shape, "channel_sums"))) return rc;
@@ -1140,14 +1149,14 @@ extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_
   return check_launch("channel_sums");
 }
 
-extern "C" int bnff_stats_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* sum,
+extern "C" int bnff_stats_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* sum,
                                    double* sumsq, double* mean, double* var, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   launch(stats_finalize_kernel, dim3((c + 31) / 32), dim3(512), 0, st, part, tiles, c, count, sum, sumsq, mean, var);
   return check_launch("stats_finalize");
 }
 
-extern "C" int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, float* part, void* stream) {
+extern "C" int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, double* part, void* stream) {
   int rc;
   if ((rc = check_view(dtype, x, "centered_var"))) return rc;
   const long long pixels = x.n * x.h * x.w;
@@ -1158,7 +1167,7 @@ extern "C" int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean,
   return check_launch("centered_var");
 }
 
-extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+extern "C" int bnff_var_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
                                  void* stream);
 
 namespace bnff {
@@ -1170,7 +1179,7 @@ __global__ void scale_kernel(double* v, int c, double s) {
 }
 }  // namespace bnff
 
-extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, int64_t count, double* var,
+extern "C" int bnff_var_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
                                  void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   launch(reduce_parts_kernel, dim3((c + 31) / 32), dim3(256), 0, st, part, tiles, c, 0, var);
@@ -1179,7 +1188,7 @@ extern "C" int bnff_var_finalize(const float* part, int32_t tiles, int32_t c, in
   return check_launch("var_finalize");
 }
 
-extern "C" int bnff_stats_finalize_coeffs(const float* part, int32_t tiles, int32_t c_new, int64_t count,
+extern "C" int bnff_stats_finalize_coeffs(const double* part, int32_t tiles, int32_t c_new, int64_t count,
                                           double* sum, double* sumsq, double* mean, double* var,
                                           int32_t c_off, int32_t c_total, const double* mean_all,
                                           const double* var_all, const float* gamma, const float* beta,
@@ -1200,7 +1209,7 @@ extern "C" int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, 
   return check_launch("bn_coeffs");
 }
 
-extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64_t count, const double* mean,
+extern "C" int bnff_dx_coeffs(int32_t c, const double* part, int32_t tiles, int64_t count, const double* mean,
                               const double* var, const float* gamma, float eps, double* dgamma64,
                               double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
                               float* dgamma32, float* dbeta32, void* stream) {
@@ -1211,7 +1220,7 @@ extern "C" int bnff_dx_coeffs(int32_t c, const float* part, int32_t tiles, int64
   return check_launch("dx_coeffs");
 }
 
-extern "C" int bnff_dx_coeffs_acc(int32_t c, const float* part, int32_t tiles, int64_t count, const double* mean,
+extern "C" int bnff_dx_coeffs_acc(int32_t c, const double* part, int32_t tiles, int64_t count, const double* mean,
                                   const double* var, const float* gamma, float eps, double* dgamma64,
                                   double* dbeta64, float* k1, float* k2, float* g, float* mean32, float* inv32,
                                   float* dgamma32, float* dbeta32, float* acc_a, float* acc_b, int32_t acc_init,
@@ -1288,7 +1297,7 @@ extern "C" int bnff_relu_bwd(int32_t dtype, bnff_view x, bnff_view dy, bnff_view
   return check_launch("relu_bwd");
 }
 
-extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, float* stat_part,
+extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, double* stat_part,
                                 void* stream) {
   int rc;
   if ((rc = check_view(dtype, x, "avgpool x")) || (rc = check_view(dtype, y, "avgpool y"))) return rc;
@@ -1306,7 +1315,7 @@ extern "C" int bnff_avgpool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t
 }
 
 extern "C" int bnff_norm_relu_pool_fwd(int32_t dtype, bnff_view x, bnff_view y, int32_t k, bnff_coef coef,
-                                       float* stat_part, void* stream) {
+                                       double* stat_part, void* stream) {
   int rc;
   if ((rc = check_view(dtype, x, "norm_relu_pool x")) || (rc = check_view(dtype, y, "norm_relu_pool y"))) return rc;
   if (y.h != x.h / k || y.w != x.w / k || y.c != x.c || y.n != x.n || y.h < 1 || y.w < 1)
@@ -1319,7 +1328,7 @@ extern "C" int bnff_norm_relu_pool_fwd(int32_t dtype, bnff_view x, bnff_view y, 
 }
 
 extern "C" int bnff_pool_relu_bn_bwd(int32_t dtype, bnff_view dy, bnff_view x, bnff_view dt1, int32_t k,
-                                     bnff_coef coef, float* part, void* stream) {
+                                     bnff_coef coef, double* part, void* stream) {
   int rc;
   if ((rc = check_view(dtype, dy, "pool_relu_bn_bwd dy")) || (rc = check_view(dtype, x, "pool_relu_bn_bwd x")) ||
       (rc = check_view(dtype, dt1, "pool_relu_bn_bwd dt1")))
@@ -1416,7 +1425,7 @@ extern "C" int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, i
 // dbias = sum over pixels of dy (optionally BN_DX-transformed); scratch is the
 // caller's partial buffer [tiles][2][C] placed after the wgrad workspace.
 namespace bnff {
-__global__ void parts_to_f32_kernel(const float* part, int tiles, int C, float* out) {
+__global__ void parts_to_f32_kernel(const double* part, int tiles, int C, float* out) {
   griddep_launch();
   griddep_wait();
   // 256 threads per 32 channels; 8 warps split the tiles, combined in fixed order
@@ -1437,7 +1446,7 @@ __global__ void parts_to_f32_kernel(const float* part, int tiles, int C, float* 
 }  // namespace bnff
 
 extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, int32_t dy_pro, bnff_coef coef,
-                                  float* scratch, float* dbias, void* stream) {
+                                  double* scratch, float* dbias, void* stream) {
   bnff_coef cf = coef;
   if (dy_pro != BNFF_PRO_BN_DX) cf.e = nullptr;
   int rc = bnff_channel_sums(dtype, 2, dy_x, dy, cf, scratch, stream);

@@ -31,7 +31,7 @@ inline int check_launch(const char* where) {
 // sum over pixels of the (optionally BN_DX-transformed) gradient -> dbias (fp32, c);
 // scratch holds [bnff_sum_tiles(pixels)][2][c] partials
 extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, int32_t dy_pro,
-                                  bnff_coef coef, float* scratch, float* dbias, void* stream);
+                                  bnff_coef coef, double* scratch, float* dbias, void* stream);
 
 #include <cstdlib>
 #include <utility>

@@ -21,7 +21,9 @@
 // Stage hand-off uses mbarriers (producers arrive; tcgen05.commit frees a slot).
 // Layout/descriptor encodings validated on B200 by tools/umma_probe.cu.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include "sm100.cuh"
@@ -54,8 +56,9 @@ struct IgParams {
   int epi;
   const void* e_xptr; long long e_xrs;
   bnff_coef e_coef;
-  float* stat_part;
+  double* stat_part;
   int stat_ld;
+  int tf32_mode;  // fp32: 0 = hi*hi + hi*lo + lo*hi, 1 = + lo*lo, 2 = cross terms first (BNFF_TF32_MODE)
 };
 
 // ---------------------------------------------------------------------------
@@ -213,15 +216,16 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // butterfly transpose-reduce of 16 per-row values over a warp: afterwards even
 // lane l holds the 32-row total of column l/2 (fixed order => deterministic)
-__device__ __forceinline__ void warp_colsum16(float (&v)[16], int lane) {
+template <typename A>
+__device__ __forceinline__ void warp_colsum16(A (&v)[16], int lane) {
 #pragma unroll
   for (int w = 8; w >= 1; w >>= 1) {
     const int off = w * 2;  // 16, 8, 4, 2
     const bool upper = lane & off;
 #pragma unroll
     for (int i = 0; i < w; ++i) {
-      float keep = upper ? v[i + w] : v[i];
-      float send = upper ? v[i] : v[i + w];
+      A keep = upper ? v[i + w] : v[i];
+      A send = upper ? v[i] : v[i + w];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
@@ -261,10 +265,12 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
   uint8_t* smem = dsmem_raw + ((1024u - (smem_u32(dsmem_raw) & 1023u)) & 1023u);
   uint32_t* meta_a = reinterpret_cast<uint32_t*>(smem + STAGES * C::STAGE_BYTES);
   uint32_t* meta_b = meta_a + STAGES * 128;
-  float* sacc = reinterpret_cast<float*>(meta_b + STAGES * 128);  // [2][stat_ld]
+  double* sacc = reinterpret_cast<double*>(meta_b + STAGES * 128);  // [2][stat_ld], f64 across tiles
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], accf_bar[2], acce_bar[2];
   __shared__ uint32_t tmem_sh;
-  __shared__ float red[4][2][BN];
+  // per-tile column sums: fp32 data in float64 (ops.py:231-237), bf16 data in fp32
+  using SAcc = typename std::conditional<sizeof(T) == 4, double, float>::type;
+  __shared__ SAcc red[4][2][BN];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntl = (p.ntiles_total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
     fence_mbar_init();
   }
   if (do_stats)
-    for (int i = tid; i < 2 * p.stat_ld; i += blockDim.x) sacc[i] = 0.f;
+    for (int i = tid; i < 2 * p.stat_ld; i += blockDim.x) sacc[i] = 0.0;
   if (warp == 4) tmem_alloc<C::TCOLS>(&tmem_sh);
   tc_fence_before();
   __syncthreads();
@@ -540,9 +546,16 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
             }
             const uint32_t acc = (kk > 0 || q > 0) ? 1u : 0u;
             if constexpr (C::F32) {
-              umma_tf32(dt, ad0, bd0, idesc, acc);
-              umma_tf32(dt, ad0, bd1, idesc, 1u);
-              umma_tf32(dt, ad1, bd0, idesc, 1u);
+              if (p.tf32_mode == 2) {  // the two cross terms first, then hi*hi
+                umma_tf32(dt, ad0, bd1, idesc, acc);
+                umma_tf32(dt, ad1, bd0, idesc, 1u);
+                umma_tf32(dt, ad0, bd0, idesc, 1u);
+              } else {
+                umma_tf32(dt, ad0, bd0, idesc, acc);
+                umma_tf32(dt, ad0, bd1, idesc, 1u);
+                umma_tf32(dt, ad1, bd0, idesc, 1u);
+                if (p.tf32_mode == 1) umma_tf32(dt, ad1, bd1, idesc, 1u);  // + lo*lo
+              }
             } else {
               umma_f16(dt, ad0, bd0, idesc, acc);
             }
@@ -585,7 +598,8 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
                 *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
           }
         } else {
-          float s1[16], s2[16], xv[16];
+          SAcc s1[16], s2[16];
+          float xv[16];
           const bool need_x = MODE == MODE_DGRAD && p.epi != BNFF_DG_PLAIN;
           if (need_x) {
 #pragma unroll
@@ -623,14 +637,14 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
             v[q] = r;
             const bool sv = rval && cval;
             if constexpr (MODE == MODE_FPROP) {
-              s1[q] = sv ? r : 0.f;
-              s2[q] = sv ? r * r : 0.f;
+              s1[q] = sv ? (SAcc)r : SAcc(0);
+              s2[q] = sv ? (SAcc)r * (SAcc)r : SAcc(0);
             } else {
               float xh = 0.f;
               if (p.epi == BNFF_DG_NRC && cval)
                 xh = __fmul_rn(__fsub_rn(xv[q], __ldg(p.e_coef.a + gc)), __ldg(p.e_coef.d + gc));
-              s1[q] = sv ? r : 0.f;
-              s2[q] = sv ? r * xh : 0.f;
+              s1[q] = sv ? (SAcc)r : SAcc(0);
+              s2[q] = sv ? (SAcc)r * (SAcc)xh : SAcc(0);
             }
           }
           if (rval) {
@@ -667,8 +681,8 @@ __global__ void __launch_bounds__(288, 1) igemm_kernel(const IgParams p) {
         for (int c = et; c < BN; c += 128) {
           const int gc = n0 + c;
           if (gc < p.N) {
-            sacc[gc] += ((red[0][0][c] + red[1][0][c]) + red[2][0][c]) + red[3][0][c];
-            sacc[p.stat_ld + gc] += ((red[0][1][c] + red[1][1][c]) + red[2][1][c]) + red[3][1][c];
+            sacc[gc] += (double)red[0][0][c] + (double)red[1][0][c] + (double)red[2][0][c] + (double)red[3][0][c];
+            sacc[p.stat_ld + gc] += (double)red[0][1][c] + (double)red[1][1][c] + (double)red[2][1][c] + (double)red[3][1][c];
           }
         }
         named_bar(2, 128);
@@ -705,7 +719,7 @@ template <int MODE, int BN, typename T, bool HASX>
 static int launch_ig(IgParams p, cudaStream_t st) {
   using C = IgCfg<MODE, BN, T, HASX>;
   auto kern = igemm_kernel<MODE, BN, T, HASX>;
-  const int smem = C::SMEM_FIXED + (MODE != MODE_WGRAD && p.stat_part ? 2 * p.stat_ld * 4 : 0);
+  const int smem = C::SMEM_FIXED + (MODE != MODE_WGRAD && p.stat_part ? 2 * p.stat_ld * 8 : 0);
   static int attr_smem = 0;  // per instantiation
   if (smem > attr_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -723,6 +737,12 @@ static int launch_ig(IgParams p, cudaStream_t st) {
   p.fd_w = make_fastdiv(p.w);
   p.fd_cin = make_fastdiv(p.cin);
   p.taps = p.kh * p.kw;
+  static int tf32_mode = -1;
+  if (tf32_mode < 0) {
+    const char* e = getenv("BNFF_TF32_MODE");
+    tf32_mode = e ? atoi(e) : 0;
+  }
+  p.tf32_mode = tf32_mode;
   const int grid = p.ntiles_total < num_sms() ? p.ntiles_total : num_sms();
   launch(kern, dim3(grid), dim3(C::THREADS), smem, st, p);
   return check_launch("igemm");
@@ -740,6 +760,8 @@ static int dispatch_bn(const IgParams& p, int bn, cudaStream_t st) {
 
 template <int MODE>
 static int dispatch(int dtype, const IgParams& p, int bn, bool hasx, cudaStream_t st) {
+  // fp32: hi/lo operand planes, float64 statistics -- a 256-wide N tile does not fit two stages
+  if (dtype != BNFF_BF16 && bn > 128) bn = 128;
   if (dtype == BNFF_BF16) {
     if (MODE != MODE_FPROP && hasx) return dispatch_bn<MODE, __nv_bfloat16, true>(p, bn, st);
     return dispatch_bn<MODE, __nv_bfloat16, false>(p, bn, st);
@@ -887,7 +909,8 @@ extern "C" int64_t bnff_wgrad_workspace(int32_t n, int32_t oh, int32_t ow, int32
     const long long wwin = bnff_window_wgrad_ws(n, oh, ow, kh, c_in, c_out);
     if (wwin > part) part = wwin;
   }
-  return (int64_t)part + (int64_t)bnff_sum_tiles(npix) * 2 * c_out;
+  // + 1: the dbias partials are float64, 8-byte aligned after the split-K partials
+  return (int64_t)part + 1 + (int64_t)bnff_sum_tiles(npix) * 2 * c_out * 2;
 }
 
 namespace bnff {
@@ -956,7 +979,7 @@ generic:
   rc = check_launch("wgrad_reduce");
   if (rc) return rc;
   if (a->dbias != nullptr) {
-    float* scratch = a->workspace + (long long)splits * p.M * p.N;
+    double* scratch = reinterpret_cast<double*>(a->workspace + (((long long)splits * p.M * p.N + 1) & ~1LL));
     return bnff_dbias_scratch(a->dtype, a->dy, a->dy_x, a->dy_pro, a->dy_coef, scratch, a->dbias, stream);
   }
   return BNFF_OK;

@@ -68,7 +68,7 @@ struct WcParams {
   int epi;
   const __nv_bfloat16* ex; long long ex_rs;
   bnff_coef ecoef;
-  float* stat_part;
+  double* stat_part;
   int tstore;                  // 1: staging in 128B-swizzled rows, stored by cp.async.bulk.tensor
   unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
 };
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             sacc[cc + c] += s1;
             sacc[BN + cc + c] += s2;
           } else {
-            float* rowp = p.stat_part + (long long)blockIdx.x * 2 * p.N;
+            double* rowp = p.stat_part + (long long)blockIdx.x * 2 * p.N;
             rowp[gcol] += s1;
             rowp[p.N + gcol] += s2;
           }
@@ -1710,7 +1710,7 @@ extern "C" int bnff_debug_trace(void* buf) {
 extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                                 int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
                                 const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
-                                float* stat_part, void* stream) {
+                                double* stat_part, void* stream) {
   wc::WcParams p{};
   p.n = (int)in.n; p.h = (int)in.h; p.w = (int)in.w;
   p.pad = pad;

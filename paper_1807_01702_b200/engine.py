@@ -51,7 +51,9 @@ def view_of(t: torch.Tensor) -> _lib.View:
     if t.dim() != 4 or t.stride(3) != 1:
         raise ShapeError(f"expected an NHWC view with unit channel stride, got {tuple(t.shape)}")
     n, h, w, c = t.shape
-    return _lib.View(_ptr(t), n, h, w, c, t.stride(2))
+    # pixel stride; a contiguous tensor's is c even where size-1 dims carry arbitrary strides
+    rs = c if t.is_contiguous() else t.stride(2)
+    return _lib.View(_ptr(t), n, h, w, c, rs)
 
 
 def coef_of(a=None, b=None, c=None, d=None, e=None) -> _lib.Coef:
@@ -378,7 +380,7 @@ class Engine:
     def _channel_stats(self, x: torch.Tensor, st: Stats, tag):
         pixels = x.shape[0] * x.shape[1] * x.shape[2]
         tiles = self.L.bnff_sum_tiles(pixels)
-        part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+        part = self._empty((tiles, 2, x.shape[3]), torch.float64)
         self._emit(self.L.bnff_channel_sums, self.dcode, 0, view_of(x), view_of(x), coef_of(),
                    _ptr(part), what=f"channel_sums {tag}", nbytes=_nb(x))
         self._emit_stats_finalize(part, tiles, x.shape[3], pixels, st)
@@ -450,7 +452,7 @@ class Engine:
         pro = _lib.PRO_RELU if at.clip_input else _lib.PRO_NONE
         if node.kind == G.FUSED_CONV_STATS:
             mt = self.L.bnff_stat_rows()
-            part = self._zeros((mt, 2, y.shape[3]), torch.float32)
+            part = self._zeros((mt, 2, y.shape[3]), torch.float64)
             self._conv_fprop(node, x, y, at.conv, pro, None, part)
             st = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
             self._emit_stats_finalize(part, mt, y.shape[3], st.count, st)
@@ -470,7 +472,7 @@ class Engine:
         if not node.attrs.onepass:  # two-pass: centred variance overwrites var (ops.py:226-227)
             self._flush_pending()  # the centred pass reads the mean
             tiles = self.L.bnff_sum_tiles(pixels)
-            part = self._empty((tiles, 2, c), torch.float32)
+            part = self._empty((tiles, 2, c), torch.float64)
             self._emit(self.L.bnff_centered_var, self.dcode, view_of(x), _ptr(st.mean), _ptr(part),
                        what="centered_var", nbytes=_nb(x))
             self._emit(self.L.bnff_var_finalize, _ptr(part), tiles, c, pixels, _ptr(st.var),
@@ -524,7 +526,7 @@ class Engine:
             part, tiles = None, 0
             if pool.attrs.emit_stats:
                 tiles = self.L.bnff_sum_tiles(pixels)
-                part = self._empty((tiles, 2, y.shape[3]), torch.float32)
+                part = self._empty((tiles, 2, y.shape[3]), torch.float64)
             self._emit(self.L.bnff_norm_relu_pool_fwd, self.dcode, view_of(x), view_of(y), pool.attrs.k,
                        coef_of(tb[0], tb[1], tb[2]), _ptr(part), what=f"norm_relu_pool {node.name}",
                        nbytes=_nb(x, y))
@@ -556,7 +558,7 @@ class Engine:
         part = None
         if at.emit_stats:
             mt = self.L.bnff_stat_rows()
-            part = self._zeros((mt, 2, y.shape[3]), torch.float32)
+            part = self._zeros((mt, 2, y.shape[3]), torch.float64)
         self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
         if at.emit_stats:
             ost = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
@@ -628,7 +630,7 @@ class Engine:
         pixels = y.shape[0] * y.shape[1] * y.shape[2]
         if node.attrs.emit_stats:
             tiles = self.L.bnff_sum_tiles(pixels)
-            part = self._empty((tiles, 2, y.shape[3]), torch.float32)
+            part = self._empty((tiles, 2, y.shape[3]), torch.float64)
         self._emit(self.L.bnff_avgpool_fwd, self.dcode, view_of(x), view_of(y), node.attrs.k,
                    _ptr(part), what="avgpool", nbytes=_nb(x, y))
         if node.attrs.emit_stats:
@@ -752,7 +754,7 @@ class Engine:
             dx = self._empty(tuple(x.shape)) if dx_out is None else dx_out
             ecoef = coef_of()
             if dgrad_epi >= _lib.DG_NRC:
-                part = self._zeros((self.L.bnff_stat_rows(), 2, x.shape[3]), torch.float32)
+                part = self._zeros((self.L.bnff_stat_rows(), 2, x.shape[3]), torch.float64)
                 m32, s32, b32, i32 = dgrad_tables
                 ecoef = coef_of(m32, s32, b32, i32)
             da = _lib.DgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(dy),
@@ -811,7 +813,7 @@ class Engine:
         """dbeta = sum dy, dgamma = sum dy*xhat (ops.py:271-274) -> backward table."""
         pixels = x.shape[0] * x.shape[1] * x.shape[2]
         tiles = self.L.bnff_sum_tiles(pixels)
-        part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+        part = self._empty((tiles, 2, x.shape[3]), torch.float64)
         m32, _, _, i32 = tables
         self._emit(self.L.bnff_channel_sums, self.dcode, 1, view_of(x), view_of(dy),
                    coef_of(m32, i32), _ptr(part), what=f"bn_bwd_sums {tag}", nbytes=_nb(x, dy))
@@ -982,16 +984,22 @@ class Engine:
         out = next((b.t for b in branches if isinstance(b, Plain) and self._writable(b.t)), None)
         if out is None:
             out = self._fresh_like(branches[0].dt1)
-        terms = (_lib.GradTerm * len(branches))()
-        for i, b in enumerate(branches):
+        if any(isinstance(b, Plain) and b.t is out for b in branches):  # the in-place branch first
+            branches.sort(key=lambda b: not (isinstance(b, Plain) and b.t is out))
+
+        def term(b):
             if isinstance(b, Plain):
-                terms[i] = _lib.GradTerm(view_of(b.t), view_of(b.t), 0, coef_of())
-            else:
-                terms[i] = _lib.GradTerm(view_of(b.dt1), view_of(b.x), 1, b.coef())
-        self._keep.append(terms)
-        nb = _nb(out) + sum(_nb(b.t) if isinstance(b, Plain) else _nb(b.dt1, b.x) for b in branches)
-        self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 0, terms, len(branches),
-                   what="split_bwd", nbytes=nb)
+                return _lib.GradTerm(view_of(b.t), view_of(b.t), 0, coef_of())
+            return _lib.GradTerm(view_of(b.dt1), view_of(b.x), 1, b.coef())
+        # up to two branches per launch; later launches accumulate into out
+        for i in range(0, len(branches), 2):
+            part = branches[i:i + 2]
+            terms = (_lib.GradTerm * len(part))(*[term(b) for b in part])
+            self._keep.append(terms)
+            nb = _nb(out) * (2 if i else 1) + sum(_nb(b.t) if isinstance(b, Plain) else _nb(b.dt1, b.x)
+                                                  for b in part)
+            self._emit(self.L.bnff_grad_sum, self.dcode, view_of(out), 1 if i else 0, terms, len(part),
+                       what="split_bwd", nbytes=nb)
         self._add_grad(node.inputs[0], Plain(out))
 
     @staticmethod
@@ -1034,7 +1042,7 @@ class Engine:
             dt1 = self._fresh_like(x)
             pixels = x.shape[0] * x.shape[1] * x.shape[2]
             tiles = self.L.bnff_sum_tiles(pixels)
-            part = self._empty((tiles, 2, x.shape[3]), torch.float32)
+            part = self._empty((tiles, 2, x.shape[3]), torch.float64)
             self._emit(self.L.bnff_pool_relu_bn_bwd, self.dcode, view_of(dy), view_of(x), view_of(dt1),
                        node.attrs.k, coef_of(m32, s32, b32, i32), _ptr(part),
                        what=f"pool_relu_bn_bwd {head.name}", nbytes=_nb(dy, x, dt1))

@@ -45,7 +45,9 @@ def view(t: torch.Tensor) -> _lib.View:
     if t.dim() != 4 or t.stride(3) != 1:
         raise ShapeError(f"expected an NHWC view with unit channel stride, got {tuple(t.shape)}")
     n, h, w, c = t.shape
-    return _lib.View(_ptr(t), n, h, w, c, t.stride(2))
+    # pixel stride; a contiguous tensor's is c even where size-1 dims carry arbitrary strides
+    rs = c if t.is_contiguous() else t.stride(2)
+    return _lib.View(_ptr(t), n, h, w, c, rs)
 
 
 def coef(*arrs) -> _lib.Coef:
@@ -218,7 +220,7 @@ def _sums(mode, x, dy=None, cf=None):
     L = _L()
     src = x if mode == 0 else dy
     tiles = L.bnff_sum_tiles(_pixels(src))
-    part = torch.empty((tiles, 2, src.shape[3]), dtype=torch.float32, device=src.device)
+    part = torch.empty((tiles, 2, src.shape[3]), dtype=torch.float64, device=src.device)
     _call(L.bnff_channel_sums, _dcode(src), mode, view(x), view(dy if dy is not None else x),
           cf or coef(), _ptr(part), what="channel_sums")
     return part, tiles
@@ -237,7 +239,7 @@ def bn_stats_twopass(x) -> DevStats:
     st = bn_stats_onepass(x)
     L = _L()
     tiles = L.bnff_sum_tiles(_pixels(x))
-    part = torch.empty((tiles, 2, x.shape[3]), dtype=torch.float32, device=x.device)
+    part = torch.empty((tiles, 2, x.shape[3]), dtype=torch.float64, device=x.device)
     _call(L.bnff_centered_var, _dcode(x), view(x), _ptr(st.mean), _ptr(part), what="centered_var")
     _call(L.bnff_var_finalize, _ptr(part), tiles, x.shape[3], st.count, _ptr(st.var),
           what="var_finalize")
@@ -341,7 +343,7 @@ def avgpool_fwd(x, k: int, stride: int = None, out=None, emit_stats: bool = Fals
     part, tiles = None, 0
     if emit_stats:
         tiles = _L().bnff_sum_tiles(_pixels(out))
-        part = torch.empty((tiles, 2, c), dtype=torch.float32, device=x.device)
+        part = torch.empty((tiles, 2, c), dtype=torch.float64, device=x.device)
     _call(_L().bnff_avgpool_fwd, _dcode(x), view(x), view(out), k, _ptr(part), what="avgpool")
     if emit_stats:
         st = _new_stats(c, _pixels(out), x.device)
@@ -368,7 +370,7 @@ def fused_conv_stats_fwd(x, conv, out, budget: int = DEFAULT_BUDGET, workers: in
         raise ShapeError(f"{pc.p.name}: input has {x.shape[3]} channels, expected {pc.p.in_c}")
     out = _out_like(x, pc.p, out)
     mt = _L().bnff_stat_rows()
-    part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
+    part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float64, device=x.device)
     _fprop(x, pc, out, _lib.PRO_NONE, None, part)
     st = _new_stats(pc.p.out_c, _pixels(out), x.device)
     _finalize(part, mt, st)
@@ -396,7 +398,7 @@ def fused_norm_relu_conv_fwd(x, stats: DevStats, bn: BNParams, conv, out, saved_
     part, mt = None, 0
     if emit_stats:
         mt = _L().bnff_stat_rows()
-        part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float32, device=x.device)
+        part = torch.zeros((mt, 2, pc.p.out_c), dtype=torch.float64, device=x.device)
     _fprop(x, pc, out, _lib.PRO_BN_RELU, tb[:3], part)
     if emit_stats:
         st = _new_stats(pc.p.out_c, _pixels(out), x.device)
@@ -405,21 +407,26 @@ def fused_norm_relu_conv_fwd(x, stats: DevStats, bn: BNParams, conv, out, saved_
     return None
 
 
-def fused_nrc_bwd(x, saved_postrelu, stats: DevStats, bn: BNParams, conv, dy, dy_pkg=None):
-    """fused.py:157-200 -> (dt1, dw, dbias, dgamma64, dbeta64).
+def fused_nrc_bwd(x, saved_postrelu, stats: DevStats, bn: BNParams, conv, dy, dy_pkg=None,
+                  return_table: bool = False):
+    """fused.py:157-200 -> (dt1, dw, dbias, dgamma64, dbeta64), the reference's 5-tuple.
 
     The ReLU mask and the wgrad operand are recomputed from x (``saved_postrelu``
     may be None); dgamma/dbeta ride in the dgrad epilogue.  ``dy_pkg`` =
-    (dt1_next, x_next, table) applies an incoming deferred BN dx inline."""
+    (dt1_next, x_next, table) applies an incoming deferred BN dx inline.
+    ``return_table=True`` appends the device dx-coefficient table (mean, inv, k1, k2, g)
+    that fused_conv_stats_bwd(table=...) consumes without recomputing it."""
     pc = _packed(conv, x)
     tb = _tables(stats, bn, x.device)
     n, h, w, c = x.shape
     mt = _L().bnff_stat_rows()
-    part = torch.zeros((mt, 2, c), dtype=torch.float32, device=x.device)
+    part = torch.zeros((mt, 2, c), dtype=torch.float64, device=x.device)
     dt1 = _dgrad(dy, pc, x, _lib.DG_NRC, x, (tb[0], tb[1], tb[2], tb[3]), part, dy_pkg)
     dw, db = _wgrad(x, dy, pc, _lib.PRO_BN_RELU, tb[:3], dy_pkg)
     table, dg64, db64 = _dx_table(part, mt, stats, bn.gamma, bn.eps, x.device)
-    return dt1, dw, db, dg64, db64, table
+    if return_table:
+        return dt1, dw, db, dg64, db64, table
+    return dt1, dw, db, dg64, db64
 
 
 def fused_conv_stats_bwd(x_own_out, saved_in, conv, dt1, dgamma, dbeta, stats: DevStats,
@@ -444,18 +451,21 @@ def fused_conv_stats_bwd(x_own_out, saved_in, conv, dt1, dgamma, dbeta, stats: D
 
 def fused_split_bwd_bn_dx(branch_grads: list, resolve=None) -> torch.Tensor:
     """fused.py:222-230 -- sum of fan-out gradients; each branch is a tensor or a deferred
-    package (dt1, x, table) resolved inline in the same sweep."""
-    if not 1 <= len(branch_grads) <= 2:
-        raise ShapeError("fused_split_bwd_bn_dx: 1 or 2 branches")
-    terms = (_lib.GradTerm * len(branch_grads))()
-    ref = None
-    for i, b in enumerate(branch_grads):
+    package (dt1, x, table) resolved inline in the same sweep.  Any number of branches:
+    the first launch writes the sum of up to two, later launches accumulate two more."""
+    if len(branch_grads) < 1:
+        raise ShapeError("fused_split_bwd_bn_dx: no branches")
+
+    def term(b):
         if isinstance(b, tuple):
-            terms[i] = _lib.GradTerm(view(b[0]), view(b[1]), 1, coef(*b[2]))
-            ref = b[0] if ref is None else ref
-        else:
-            terms[i] = _lib.GradTerm(view(b), view(b), 0, coef())
-            ref = b if ref is None else ref
-    out = torch.empty(tuple(ref.shape), dtype=ref.dtype, device=ref.device)
-    _call(_L().bnff_grad_sum, _dcode(ref), view(out), 0, terms, len(branch_grads), what="split_bwd")
+            return _lib.GradTerm(view(b[0]), view(b[1]), 1, coef(*b[2])), b[0]
+        return _lib.GradTerm(view(b), view(b), 0, coef()), b
+
+    first = term(branch_grads[0])[1]
+    out = torch.empty(tuple(first.shape), dtype=first.dtype, device=first.device)
+    for i in range(0, len(branch_grads), 2):
+        chunk = [term(b)[0] for b in branch_grads[i:i + 2]]
+        terms = (_lib.GradTerm * len(chunk))(*chunk)
+        _call(_L().bnff_grad_sum, _dcode(first), view(out), 1 if i else 0, terms, len(chunk),
+              what="split_bwd")
     return out

@@ -160,7 +160,7 @@ def test_composite_block_backward(dt):
     std = K.fused_conv_stats_fwd(xd, p1, t0d)
     yd = torch.empty((2, 10, 10, 16), dtype=DT[dt], device="cuda")
     K.fused_norm_relu_conv_fwd(t0d, std, bn, p2, yd)
-    dt1, dw2, _, dg, dbt, table = K.fused_nrc_bwd(t0d, None, std, bn, p2, to_dev(dy, dt))
+    dt1, dw2, _, dg, dbt, table = K.fused_nrc_bwd(t0d, None, std, bn, p2, to_dev(dy, dt), return_table=True)
     dx1, dw1, _ = K.fused_conv_stats_bwd(t0d, xd, p1, dt1, dg, dbt, std, bn.gamma, bn.eps, table=table)
     torch.cuda.synchronize()
     tol = 1e-4 if dt == "f32" else 1.5e-1  # bf16: BN-backward cancellation on 200 px/channel

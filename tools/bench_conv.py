@@ -112,7 +112,7 @@ def case(n, hw, cin, cout, k, mode, pro, epi, reps):
         outs = {}
         for nm, pc in (("win", pw), ("gen", pg)):
             y = torch.empty(n, hw, hw, cout, device=dev, dtype=torch.bfloat16)
-            part = torch.zeros((L.bnff_stat_rows(), 2, cout), device=dev)
+            part = torch.zeros((L.bnff_stat_rows(), 2, cout), dtype=torch.float64, device=dev)
 
             def run(pc=pc, y=y, part=part):
                 K._fprop(x, pc, y, pro, tb, part)
@@ -132,7 +132,7 @@ def case(n, hw, cin, cout, k, mode, pro, epi, reps):
         pkg = (dy, dyx, (m, inv, k1, k2, g)) if pro == _lib.PRO_BN_DX else None
         outs = {}
         for nm, pc in (("win", pw), ("gen", pg)):
-            part = torch.zeros((L.bnff_stat_rows(), 2, cin), device=dev)
+            part = torch.zeros((L.bnff_stat_rows(), 2, cin), dtype=torch.float64, device=dev)
             holder = {}
 
             def run(pc=pc, part=part, holder=holder):

@@ -37,7 +37,7 @@ def main():
     m, s, b, inv, k1, k2 = bench_conv.tables(cout, dev, 4)
     em, es, eb, einv, _, _ = bench_conv.tables(cin, dev, 5)
     pkg = (dy, dyx, (m, inv, k1, k2, s))
-    part = torch.zeros((L.bnff_stat_rows(), 2, cin), device=dev)
+    part = torch.zeros((L.bnff_stat_rows(), 2, cin), dtype=torch.float64, device=dev)
     G = torch.zeros(n, hw, hw, cin, device=dev, dtype=torch.bfloat16)
     rows = []
     for name, epi, use_pkg, st in (("plain, dy only", _lib.DG_PLAIN, False, False),

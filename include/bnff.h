@@ -175,7 +175,7 @@ int64_t bnff_window_wgrad_ws(int32_t n, int32_t h, int32_t w, int32_t kh, int32_
 int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
                       int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, float* dw,
                       int32_t dw_cin, float* dbias, void* stream);
-int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
+int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                      int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
                      const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
                      double* stat_part, void* stream);
@@ -284,10 +284,15 @@ int bnff_nhwc_to_nchw(int32_t dtype, bnff_view src, float* dst, void* stream);
  * col (n, oh, ow, kpad), k = (ky*kw + kx)*c_real + ci, zero beyond kh*kw*c_real; the
  * conv is then a 1x1 conv over col (forward and weight gradient), replacing the
  * 49-chunk gather of conv2d_fwd/conv2d_bwd (ops.py:151-204) for this layer.
- * x must be stored with 8 channels (bf16).  weight_to_cols / cols_to_weight move
+ * x must be stored as one 16-byte pixel (8 bf16 / 4 fp32 channels).  weight_to_cols / cols_to_weight move
  * fp32 weights between (c_out, c_in, kh, kw) and (c_out, kpad).                  */
 int bnff_im2col(int32_t dtype, bnff_view x, int32_t c_real, int32_t kh, int32_t kw, int32_t stride,
                 int32_t pad, bnff_view col, void* stream);
+/* K13b: input gradient of a patch-matrix stem conv: dx = col2im(dcol), dcol = dgrad of the 1x1
+ * GEMM over the patch matrix (ops.py:178-204 dx for the 7x7/s2 stem); deterministic gather,
+ * storage channels >= c_real written as zeros */
+int bnff_col2im(int32_t dtype, bnff_view dcol, int32_t c_real, int32_t kh, int32_t kw, int32_t stride,
+                int32_t pad, bnff_view dx, void* stream);
 int bnff_weight_to_cols(const float* w, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
                         int32_t kpad, float* w2, void* stream);
 int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,

@@ -81,7 +81,7 @@ SIGNATURES = {
     "bnff_window_ok": (C.c_int, [_I32] * 9),
     "bnff_window_pack_size": (_I64, [_I32] * 6),
     "bnff_pack_window": (C.c_int, [_I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
-    "bnff_window_conv": (C.c_int, [_I32, _I32, _I32, View, View, _I32, Coef, View, _P, _P, _I32,
+    "bnff_window_conv": (C.c_int, [_I32, _I32, _I32, _I32, View, View, _I32, Coef, View, _P, _P, _I32,
                                    View, Coef, _P, _P]),
     "bnff_window_wgrad_ws": (_I64, [_I32] * 6),
     "bnff_pack_window_multi": (C.c_int, [_I32, _I32, _P, _I64, _P]),
@@ -118,6 +118,7 @@ SIGNATURES = {
     "bnff_sgd": (C.c_int, [_P, _P, _I64, _F, _P]),
     "bnff_debug_trace": (C.c_int, [_P]),
     "bnff_im2col": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
+    "bnff_col2im": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
     "bnff_weight_to_cols": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "bnff_cols_to_weight": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
 }

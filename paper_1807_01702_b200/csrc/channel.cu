@@ -1056,7 +1056,7 @@ __global__ void sgd_kernel(float* w, const float* g, long long n, float lr) {
   griddep_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    w[i] = w[i] - lr * g[i];
+    w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));  // w - lr*g, two roundings (no FMA contraction)
 }
 
 template <typename T>

@@ -33,6 +33,14 @@ inline int check_launch(const char* where) {
 extern "C" int bnff_dbias_scratch(int32_t dtype, bnff_view dy, bnff_view dy_x, int32_t dy_pro,
                                   bnff_coef coef, double* scratch, float* dbias, void* stream);
 
+// wgrad32.cu / wconv.cu internals shared with igemm.cu's bnff_conv_wgrad
+extern "C" int64_t bnff_wgrad_f32_ws(int32_t n, int32_t h, int32_t w, int32_t kh, int32_t c_in, int32_t c_out);
+extern "C" int bnff_wgrad_f32_partials(bnff_view x, int32_t x_pro, bnff_coef x_coef, bnff_view dy, bnff_view dy_x,
+                                       int32_t dy_pro, bnff_coef dy_coef, int32_t kh, float* ws, int32_t want_db,
+                                       int32_t* splits_out, void* stream);
+extern "C" int bnff_wgrad_reduce(const float* ws, int32_t splits, int32_t taps, int32_t cin, int32_t cout,
+                                 int32_t cin_real, float* dw, const float* wsb, float* dbias, void* stream);
+
 #include <cstdlib>
 #include <utility>
 

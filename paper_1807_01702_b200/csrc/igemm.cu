@@ -821,7 +821,7 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
     return set_error(BNFF_ERR_STATE, "fprop: missing statistics for the normalize prologue");
   if (a->wwin && bnff_window_ok(a->dtype, (int)a->x.c, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     bnff_view none{};
-    const int wrc = bnff_window_conv(0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin,
+    const int wrc = bnff_window_conv(a->dtype, 0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin,
                                      a->bias, 0, none, bnff_coef{}, a->stat_part, stream);
     if (wrc != kWindowNoFitAbi) return wrc;
   }
@@ -859,7 +859,7 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   if (a->wwin && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     if (a->dy_pro == BNFF_PRO_BN_DX && (!a->dy_coef.a || !a->dy_coef.e))
       return set_error(BNFF_ERR_STATE, "dgrad: missing deferred-gradient coefficients");
-    const int wrc = bnff_window_conv(1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx,
+    const int wrc = bnff_window_conv(a->dtype, 1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx,
                                      a->wwin, nullptr, a->epi, a->x, a->x_coef,
                                      a->epi >= BNFF_DG_NRC ? a->stat_part : nullptr, stream);
     if (wrc != kWindowNoFitAbi) return wrc;
@@ -905,9 +905,11 @@ extern "C" int64_t bnff_wgrad_workspace(int32_t n, int32_t oh, int32_t ow, int32
   const long long npix = (long long)n * oh * ow;
   // split-K partial tiles + dbias channel partials [tiles][2][c_out]
   long long part = (long long)splits * kh * kw * c_in * c_out;
-  if (kh == kw && (kh == 1 || kh == 3)) {  // the window kernel may plan more splits (stride 1: oh = h)
+  if (kh == kw && (kh == 1 || kh == 3)) {  // the window kernels may plan more splits (stride 1: oh = h)
     const long long wwin = bnff_window_wgrad_ws(n, oh, ow, kh, c_in, c_out);
     if (wwin > part) part = wwin;
+    const long long w32 = bnff_wgrad_f32_ws(n, oh, ow, kh, c_in, c_out);
+    if (w32 > part) part = w32;
   }
   // + 1: the dbias partials are float64, 8-byte aligned after the split-K partials
   return (int64_t)part + 1 + (int64_t)bnff_sum_tiles(npix) * 2 * c_out * 2;
@@ -944,12 +946,25 @@ extern "C" int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream) {
   p.oh = (int)a->dy.h; p.ow = (int)a->dy.w; p.cout = (int)a->dy.c;
   if ((p.h + 2 * p.pad - p.kh) / p.stride + 1 != p.oh || (p.w + 2 * p.pad - p.kw) / p.stride + 1 != p.ow)
     return set_error(BNFF_ERR_SHAPE, "wgrad: dy spatial dims inconsistent with x");
-  if (a->splits >= 0 && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+  if (a->splits >= 0 && a->dtype == BNFF_BF16 && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
     // window-shift kernel (splits < 0 forces the generic path)
     int rc2 = bnff_window_wgrad(a->x, a->x_pro, a->x_coef, a->dy, a->dy_x, a->dy_pro, a->dy_coef, p.kh,
                                 a->workspace, a->dw, a->dw_cin, a->dbias, stream);
     if (rc2 == kWindowNoFitAbi) goto generic;
     return rc2;
+  }
+  if (a->splits >= 0 && a->dtype == BNFF_F32 && p.stride == 1 && p.kh == p.kw && (p.kh == 1 || p.kh == 3) &&
+      p.pad == p.kh / 2) {
+    // fp32: TMA tap-box wgrad (wgrad32.cu), then the fixed-order split reduction
+    int splits = 0;
+    const int rc3 = bnff_wgrad_f32_partials(a->x, a->x_pro, a->x_coef, a->dy, a->dy_x, a->dy_pro, a->dy_coef, p.kh,
+                                            a->workspace, a->dbias != nullptr, &splits, stream);
+    if (rc3 != kWindowNoFitAbi) {
+      if (rc3) return rc3;
+      const float* wsb = a->workspace + (long long)splits * p.kh * p.kw * p.cin * p.cout;
+      return bnff_wgrad_reduce(a->workspace, splits, p.kh * p.kw, p.cin, p.cout, a->dw_cin, a->dw,
+                               a->dbias ? wsb : nullptr, a->dbias, stream);
+    }
   }
 generic:
   const int taps = p.kh * p.kw;

@@ -102,6 +102,15 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
                ::"r"(smem_u32(bar)) : "memory");
 }
+// kind::tf32 from one elected lane of a converged warp (see umma_f16_elect)
+__device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 // kind::tf32 (fp32 bit patterns in smem, low 13 mantissa bits ignored)
 __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
@@ -345,10 +354,11 @@ inline EncodeTiledFn encode_tiled_fn() {
   }
   return fn;
 }
-// bf16 NHWC view (ptr, n, h, w, c, row_stride elements) as a rank-2 {c, n*h*w} or
-// rank-4 {c, w, h, n} tensor; box {bc, b1[, b2, b3]}; swizzle 64B/128B by box row bytes
-inline bool encode_nhwc_bf16(CUtensorMap* tm, const void* ptr, long long n, long long h, long long w,
-                             long long c, long long rs, int rank, const uint32_t* box) {
+// NHWC view (ptr, n, h, w, c, row_stride elements of `es` bytes: 2 = bf16, 4 = fp32) as a
+// rank-2 {c, n*h*w} or rank-4 {c, w, h, n} tensor; box {bc, b1[, b2, b3]}; swizzle
+// 32B/64B/128B by box row bytes
+inline bool encode_nhwc(CUtensorMap* tm, int esz, const void* ptr, long long n, long long h, long long w,
+                        long long c, long long rs, int rank, const uint32_t* box) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return false;
   cuuint64_t dims[4], strides[3];
@@ -356,19 +366,24 @@ inline bool encode_nhwc_bf16(CUtensorMap* tm, const void* ptr, long long n, long
   dims[0] = (cuuint64_t)c;
   if (rank == 2) {
     dims[1] = (cuuint64_t)(n * h * w);
-    strides[0] = (cuuint64_t)rs * 2;
+    strides[0] = (cuuint64_t)rs * esz;
   } else {
     dims[1] = (cuuint64_t)w; dims[2] = (cuuint64_t)h; dims[3] = (cuuint64_t)n;
-    strides[0] = (cuuint64_t)rs * 2;
-    strides[1] = (cuuint64_t)(w * rs) * 2;
-    strides[2] = (cuuint64_t)(h * w * rs) * 2;
+    strides[0] = (cuuint64_t)rs * esz;
+    strides[1] = (cuuint64_t)(w * rs) * esz;
+    strides[2] = (cuuint64_t)(h * w * rs) * esz;
   }
   for (int i = 0; i < rank; ++i) bx[i] = box[i];
-  const CUtensorMapSwizzle sw = box[0] * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                                  : (box[0] * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                                      : CU_TENSOR_MAP_SWIZZLE_32B);
-  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(ptr), dims, strides, bx,
+  const CUtensorMapSwizzle sw = box[0] * esz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                   : (box[0] * esz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                        : CU_TENSOR_MAP_SWIZZLE_32B);
+  const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return fn(tm, dt, (cuuint32_t)rank, const_cast<void*>(ptr), dims, strides, bx,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+inline bool encode_nhwc_bf16(CUtensorMap* tm, const void* ptr, long long n, long long h, long long w,
+                             long long c, long long rs, int rank, const uint32_t* box) {
+  return encode_nhwc(tm, 2, ptr, n, h, w, c, rs, rank, box);
 }
 }  // namespace bnff

@@ -23,12 +23,14 @@ namespace stem {
 // column k to its element offset in that stage (-1: K padding), so every thread builds
 // whole 16-byte chunks of patch rows (8 table-driven shared loads) and stores them
 // coalesced.
-__global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __restrict__ x, long long x_rs,
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, long long x_rs,
                                                      int h, int w, int oh, int ow, int kh, int kw,
                                                      int stride, int pad, int creal, int kpad, int tp,
-                                                     __nv_bfloat16* __restrict__ col, long long col_rs) {
+                                                     T* __restrict__ col, long long col_rs) {
   griddep_launch();
-  extern __shared__ uint4 tile[];  // [kh][tw] pixels of 8 bf16, then int koff[kpad]
+  constexpr int EPP = 16 / (int)sizeof(T);  // elements per stored pixel / per 16-byte chunk
+  extern __shared__ uint4 tile[];  // [kh][tw] 16-byte pixels (8 bf16 / 4 fp32), then int koff[kpad]
   const int tpr = (ow + tp - 1) / tp;
   const int b = blockIdx.x;
   const int row = b / tpr;  // img * oh + oy
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __rest
     if (k < K) {
       const int tap = k / creal, ci = k - tap * creal;
       const int ky = tap / kw, kx = tap - ky * kw;
-      o = (ky * tw + kx) * 8 + ci;
+      o = (ky * tw + kx) * EPP + ci;
     }
     koff[k] = o;
   }
@@ -59,19 +61,25 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __nv_bfloat16* __rest
   }
   __syncthreads();
   const unsigned short* ts = reinterpret_cast<const unsigned short*>(tile);
-  const int cpp = kpad / 8;  // 16-byte chunks per patch row
+  const uint32_t* tw32 = reinterpret_cast<const uint32_t*>(tile);
+  const int cpp = kpad / EPP;  // 16-byte chunks per patch row
   const long long p0 = (long long)row * ow + ox0;
   for (int i = threadIdx.x; i < np * cpp; i += blockDim.x) {
     const int p = i / cpp, j = i - p * cpp;
-    const int pb = p * stride * 8;
+    const int pb = p * stride * EPP;
     uint32_t v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int o0 = koff[j * 8 + 2 * e], o1 = koff[j * 8 + 2 * e + 1];
-      const uint32_t lo = o0 >= 0 ? ts[o0 + pb] : 0u, hi = o1 >= 0 ? ts[o1 + pb] : 0u;
-      v[e] = lo | (hi << 16);
+      if constexpr (EPP == 8) {
+        const int o0 = koff[j * 8 + 2 * e], o1 = koff[j * 8 + 2 * e + 1];
+        const uint32_t lo = o0 >= 0 ? ts[o0 + pb] : 0u, hi = o1 >= 0 ? ts[o1 + pb] : 0u;
+        v[e] = lo | (hi << 16);
+      } else {
+        const int o = koff[j * 4 + e];
+        v[e] = o >= 0 ? tw32[o + pb] : 0u;
+      }
     }
-    *reinterpret_cast<uint4*>(col + (p0 + p) * col_rs + j * 8) = make_uint4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<uint4*>(col + (p0 + p) * col_rs + j * EPP) = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -106,6 +114,47 @@ __global__ void cols_to_weight_kernel(const float* __restrict__ dw2, int co_n, i
   }
 }
 
+// input gradient of the stem conv through its patch matrix: dx[n, iy, ix, ci] = sum over the
+// (ky, kx) taps whose output (oy, ox) = ((iy + pad - ky) / s, (ix + pad - kx) / s) is an
+// integer position inside the map of dcol[n, oy, ox, (ky*kw + kx)*creal + ci]
+// (col2im as a deterministic gather: every dx element sums its taps in fixed order; the
+// storage channels beyond creal are written as zeros).  One thread per (pixel, channel).
+template <typename T>
+__global__ void __launch_bounds__(256) col2im_kernel(const T* __restrict__ dcol, long long col_rs, int n, int h,
+                                                     int w, int oh, int ow, int kh, int kw, int stride, int pad,
+                                                     int creal, int cstore, T* __restrict__ dx, long long dx_rs) {
+  griddep_launch();
+  griddep_wait();
+  const long long total = (long long)n * h * w * cstore;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(i % cstore);
+    const long long pix = i / cstore;
+    const int ix = (int)(pix % w);
+    const long long t = pix / w;
+    const int iy = (int)(t % h);
+    const int img = (int)(t / h);
+    float acc = 0.f;
+    if (ci < creal) {
+      for (int ky = 0; ky < kh; ++ky) {
+        const int ty = iy + pad - ky;
+        if (ty < 0 || ty % stride) continue;
+        const int oy = ty / stride;
+        if (oy >= oh) continue;
+        for (int kx = 0; kx < kw; ++kx) {
+          const int tx = ix + pad - kx;
+          if (tx < 0 || tx % stride) continue;
+          const int ox = tx / stride;
+          if (ox >= ow) continue;
+          const long long q = ((long long)img * oh + oy) * ow + ox;
+          acc += (float)dcol[q * col_rs + (ky * kw + kx) * creal + ci];
+        }
+      }
+    }
+    dx[pix * dx_rs + ci] = (T)acc;
+  }
+}
+
 }  // namespace stem
 }  // namespace bnff
 
@@ -113,32 +162,42 @@ using namespace bnff;
 
 extern "C" int bnff_im2col(int32_t dtype, bnff_view x, int32_t c_real, int32_t kh, int32_t kw,
                            int32_t stride, int32_t pad, bnff_view col, void* stream) {
-  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "im2col: bf16 only");
-  if (x.c != 8 || c_real < 1 || c_real > 8)
-    return set_error(BNFF_ERR_UNSUPPORTED, "im2col: input must be stored with 8 channels (got %lld)",
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "im2col: dtype");
+  const int epp = dtype == BNFF_F32 ? 4 : 8;  // one 16-byte pixel
+  if (x.c != epp || c_real < 1 || c_real > epp)
+    return set_error(BNFF_ERR_UNSUPPORTED, "im2col: input must be stored with %d channels (got %lld)", epp,
                      (long long)x.c);
   if (kh < 1 || kw < 1 || stride < 1 || pad < 0) return set_error(BNFF_ERR_SHAPE, "im2col: bad conv geometry");
   const long long oh = (x.h + 2 * pad - kh) / stride + 1, ow = (x.w + 2 * pad - kw) / stride + 1;
   if (col.n != x.n || col.h != oh || col.w != ow)
     return set_error(BNFF_ERR_SHAPE, "im2col: col (%lld,%lld,%lld) != (%lld,%lld,%lld)", (long long)col.n,
                      (long long)col.h, (long long)col.w, (long long)x.n, oh, ow);
-  if (col.c % 8 || col.c < (long long)kh * kw * c_real || col.row_stride % 8 || x.row_stride % 8)
-    return set_error(BNFF_ERR_SHAPE, "im2col: col channels %lld must be a multiple of 8 >= %d",
-                     (long long)col.c, kh * kw * c_real);
+  if (col.c % epp || col.c < (long long)kh * kw * c_real || col.row_stride % epp || x.row_stride % epp)
+    return set_error(BNFF_ERR_SHAPE, "im2col: col channels %lld must be a multiple of %d >= %d",
+                     (long long)col.c, epp, kh * kw * c_real);
   const int tp = ow <= 128 ? (int)ow : 64;
   const int tw = (tp - 1) * stride + kw;
   const size_t smem = (size_t)kh * tw * 16 + (size_t)col.c * 4;
   if (smem > 200 * 1024) return set_error(BNFF_ERR_UNSUPPORTED, "im2col: window too large");
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(stem::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "im2col attr");
-  }
   const long long blocks = x.n * oh * ((ow + tp - 1) / tp);
   if (blocks == 0) return BNFF_OK;
-  launch(stem::im2col_kernel, dim3((unsigned)blocks), dim3(256), smem, (cudaStream_t)stream,
-         (const __nv_bfloat16*)x.ptr, (long long)x.row_stride, (int)x.h, (int)x.w, (int)oh, (int)ow, kh, kw,
-         stride, pad, c_real, (int)col.c, tp, (__nv_bfloat16*)col.ptr, (long long)col.row_stride);
+  cudaError_t e = cudaSuccess;
+  if (dtype == BNFF_F32) {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(stem::im2col_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "im2col attr");
+    launch(stem::im2col_kernel<float>, dim3((unsigned)blocks), dim3(256), smem, (cudaStream_t)stream,
+           (const float*)x.ptr, (long long)x.row_stride, (int)x.h, (int)x.w, (int)oh, (int)ow, kh, kw, stride,
+           pad, c_real, (int)col.c, tp, (float*)col.ptr, (long long)col.row_stride);
+  } else {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(stem::im2col_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "im2col attr");
+    launch(stem::im2col_kernel<__nv_bfloat16>, dim3((unsigned)blocks), dim3(256), smem, (cudaStream_t)stream,
+           (const __nv_bfloat16*)x.ptr, (long long)x.row_stride, (int)x.h, (int)x.w, (int)oh, (int)ow, kh, kw,
+           stride, pad, c_real, (int)col.c, tp, (__nv_bfloat16*)col.ptr, (long long)col.row_stride);
+  }
   return check_launch("im2col");
 }
 
@@ -158,4 +217,28 @@ extern "C" int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in
   launch(stem::cols_to_weight_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, dw2, c_out,
          c_in, kh, kw, kpad, dw);
   return check_launch("cols_to_weight");
+}
+
+extern "C" int bnff_col2im(int32_t dtype, bnff_view dcol, int32_t c_real, int32_t kh, int32_t kw, int32_t stride,
+                           int32_t pad, bnff_view dx, void* stream) {
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "col2im: dtype");
+  if (kh < 1 || kw < 1 || stride < 1 || pad < 0 || c_real < 1 || c_real > dx.c)
+    return set_error(BNFF_ERR_SHAPE, "col2im: bad conv geometry");
+  const long long oh = (dx.h + 2 * pad - kh) / stride + 1, ow = (dx.w + 2 * pad - kw) / stride + 1;
+  if (dcol.n != dx.n || dcol.h != oh || dcol.w != ow || dcol.c < (long long)kh * kw * c_real)
+    return set_error(BNFF_ERR_SHAPE, "col2im: dcol (%lld,%lld,%lld,%lld) vs dx", (long long)dcol.n,
+                     (long long)dcol.h, (long long)dcol.w, (long long)dcol.c);
+  const long long total = dx.n * dx.h * dx.w * dx.c;
+  if (total == 0) return BNFF_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (dtype == BNFF_F32)
+    launch(stem::col2im_kernel<float>, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream,
+           (const float*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)oh, (int)ow, kh,
+           kw, stride, pad, c_real, (int)dx.c, (float*)dx.ptr, (long long)dx.row_stride);
+  else
+    launch(stem::col2im_kernel<__nv_bfloat16>, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream,
+           (const __nv_bfloat16*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)oh,
+           (int)ow, kh, kw, stride, pad, c_real, (int)dx.c, (__nv_bfloat16*)dx.ptr, (long long)dx.row_stride);
+  return check_launch("col2im");
 }

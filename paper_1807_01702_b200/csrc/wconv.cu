@@ -58,15 +58,13 @@ struct WcParams {
   int n, h, w, hp, wp, pad, Q, mtiles, ntiles, tiles, R, stages;
   FastDiv fd_hpwp, fd_wp;
   int ci, nslab, N, npad;
-  const __nv_bfloat16* src; long long src_rs;
-  const __nv_bfloat16* srcx; long long srcx_rs;
   int pro;
   bnff_coef pcoef;
   const uint8_t* wpk;
-  __nv_bfloat16* out; long long out_rs;
+  void* out; long long out_rs;      // bf16 or fp32 elements (the kernel's ES)
   const float* bias;
   int epi;
-  const __nv_bfloat16* ex; long long ex_rs;
+  const void* ex; long long ex_rs;
   bnff_coef ecoef;
   double* stat_part;
   int tstore;                  // 1: staging in 128B-swizzled rows, stored by cp.async.bulk.tensor
@@ -99,9 +97,25 @@ struct Geo {
 // 3x3 weights stay resident in shared memory when they fit (<= 96 KB, one N tile); wider
 // 3x3 convs (ResNet's 128..512 channels) stream the 9 taps of each slab with the stage
 // (sw = 1), in 64-column N tiles.
-__host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
+__host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad, int es = 2) {
   Geo g{};
   g.taps = kh * kw;
+  if (es == 4) {
+    // fp32 (3xTF32): every operand element takes 8 bytes of shared memory (hi + lo planes).
+    // 1x1: 128-byte slabs (32 channels), N tiles <= 128 (fprop) / 64 (dgrad: x tile + 2
+    // staging buffers per group); 3x3: 64-byte slabs (16 channels), weights streamed with
+    // the stage, N tiles of 32 / 64
+    g.RB = (g.taps == 9 || CI <= 16) ? 64 : 128;
+    g.BN = pick_bn(N);
+    // (the 64-byte-slab 1x1 instantiation -- K <= 16 channels -- exists for 32-wide N tiles only)
+    const int cap = g.taps == 9 ? (dgrad ? 32 : 64) : (g.RB == 64 ? 32 : (dgrad ? 64 : 128));
+    if (g.BN > cap) g.BN = cap;
+    g.sw = g.taps == 9 ? 1 : 0;
+    g.nslab = (CI + g.RB / 4 - 1) / (g.RB / 4);
+    g.ntiles = (N + g.BN - 1) / g.BN;
+    g.npad = g.ntiles * g.BN;
+    return g;
+  }
   // 3x3: 64-byte slabs (32 channels) -> small window stages, deep prefetch beside the
   // resident weights
   g.RB = (CI <= 32 || g.taps == 9) ? 64 : pick_rb(CI);
@@ -119,9 +133,11 @@ __host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad) {
 }
 
 
-template <int BN, int RB, int TAPS, int MODE, bool SW = false>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false, int ES = 2>
 struct Layout {
-  static constexpr int SLABW = RB / 2;               // channels per slab row
+  static constexpr bool F32 = ES == 4;               // fp32 storage, 3xTF32 MMAs
+  static constexpr int PL = F32 ? 2 : 1;             // operand planes (hi, lo)
+  static constexpr int SLABW = RB / ES;              // channels per slab row
   static constexpr int CPR = RB / 16;                // 16B chunks per row
   static constexpr int RS = LT / CPR;                // loader row step
   static constexpr int UR = (TAPS == 1 ? 128 : RMAX) / RS;  // rows per loader thread (max)
@@ -130,12 +146,13 @@ struct Layout {
   static constexpr bool WRES = (TAPS == 9 && !SW) || (TAPS == 1 && SW && MODE == M_FPROP);
   static constexpr bool XOP = MODE == M_DGRAD;       // second window operand (BN_DX x)
   // epilogue column chunk: two groups of 4 warps take alternate chunks
-  static constexpr int CW = BN <= 32 ? 16 : (BN == 64 ? 32 : 64);
+  static constexpr int CW = F32 ? (BN <= 32 ? 16 : 32) : (BN <= 32 ? 16 : (BN == 64 ? 32 : 64));
   static constexpr int NCH = BN / CW;                // chunks per tile (>= 2)
   static constexpr int MYCH = (NCH + 1) / 2;         // chunks per epilogue group
   // staging row pitch (bytes): 64-column chunks use dense 128-byte rows with the 128B swizzle
   // (the TMA box layout); narrower chunks pad each row by 16 bytes against bank conflicts
-  static constexpr int SROWB = CW == 64 ? 128 : CW * 2 + 16;
+  static constexpr bool TST = CW * ES == 128;       // 128-byte staging rows stored by TMA
+  static constexpr int SROWB = TST ? 128 : CW * ES + 16;
   static constexpr int STG = 128 * SROWB;
   // per group: out staging (+ dgrad: one x buffer per owned chunk = a whole-tile lookahead)
   static constexpr int NSTG = MODE == M_DGRAD ? 1 + MYCH : 1;
@@ -149,15 +166,16 @@ struct Carve {
   int wres, stage0, stage_bytes, a_bytes, stg, gbuf, ptab, etab, sacc, red, rowtab, rowpix, meta, total;
 };
 
-template <int BN, int RB, int TAPS, int MODE, bool SW = false>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false, int ES = 2>
 __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop, bool gb = false) {
-  using L = Layout<BN, RB, TAPS, MODE, SW>;
+  using L = Layout<BN, RB, TAPS, MODE, SW, ES>;
   Carve c{};
   int off = 0;
   c.wres = off;
-  if (L::WRES) off += align_up(nslab * TAPS * BN * RB, 1024);
+  if (L::WRES) off += align_up(nslab * TAPS * BN * RB * L::PL, 1024);
   c.a_bytes = align_up(R * RB, 1024);
-  c.stage_bytes = c.a_bytes * (xop ? 2 : 1) + (L::WRES ? 0 : TAPS * BN * RB);
+  // stage: A planes (hi[, lo]) | x operand (BN_DX) | B planes (streamed weights)
+  c.stage_bytes = c.a_bytes * (L::PL + (xop ? 1 : 0)) + (L::WRES ? 0 : TAPS * BN * RB * L::PL);
   c.stage0 = off;
   off += stages * c.stage_bytes;
   c.stg = off;
@@ -169,9 +187,9 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.etab = off;
   off += (MODE == M_DGRAD ? 4 : 1) * npad * 4;  // bias | NRC (scale, shift, inv, -mean*inv)
   c.sacc = off;
-  off += 2 * BN * 4;  // per-CTA sums when one N tile (else accumulated in the global row)
+  off += 2 * BN * (L::F32 ? 8 : 4);  // per-CTA sums (fp32 data: float64)
   c.red = off;
-  off += 2 * 4 * 128 * 4;
+  off += 2 * 4 * 128 * (L::F32 ? 8 : 4);
   c.rowtab = off;
   off += 2 * RMAX * 4;
   c.rowpix = off;
@@ -182,9 +200,10 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
 }
 
 // the 1x1 block-gradient fold runs through TMA (G tile loaded, folded in smem, stored back)
-template <int BN, int RB, int TAPS, int MODE, bool SW>
+template <int BN, int RB, int TAPS, int MODE, bool SW, int ES = 2>
 __host__ __device__ inline bool fold_tma(const WcParams& p) {
-  return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW>::CW == 64 && p.epi >= BNFF_DG_NRC_ACC;
+  return ES == 2 && TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW, ES>::CW == 64 &&
+         p.epi >= BNFF_DG_NRC_ACC;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
@@ -201,6 +220,10 @@ __device__ __forceinline__ uint4 pack8(const float* f, bool relu) {
     o.z = pack_bf16_rn(f[4], f[5]); o.w = pack_bf16_rn(f[6], f[7]);
   }
   return o;
+}
+__device__ __forceinline__ void ld4f(const float* p, float* v) {  // 4 floats, 16B aligned
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
 __device__ __forceinline__ void ld8f(const float* p, float* v) {  // 8 floats, 16B aligned
   const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
@@ -226,11 +249,15 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
   }
 }
 
-template <int BN, int RB, int TAPS, int MODE, bool SW = false>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false, int ES = 2>
 __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_constant__ WcParams p) {
   griddep_launch();
   if (threadIdx.x == 0) trace_ev(p.trace, 8, 0);
-  using L = Layout<BN, RB, TAPS, MODE, SW>;
+  using L = Layout<BN, RB, TAPS, MODE, SW, ES>;
+  constexpr bool F32 = L::F32;
+  constexpr int PL = L::PL;
+  using E = typename std::conditional<F32, float, __nv_bfloat16>::type;  // storage element
+  using SA = typename std::conditional<F32, double, float>::type;        // statistics accumulator
   constexpr int CPR = L::CPR, RS = L::RS, UR = L::UR, SLABW = L::SLABW, CW = L::CW;
   extern __shared__ uint8_t dsm_raw[];
   // offset (not integer-cast) the shared array so the compiler keeps the shared state space
@@ -238,13 +265,13 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   __shared__ uint64_t full_bar[8], empty_bar[8], ld_bar[8], accf_bar[2], acce_bar[2], w_bar, g_bar[4], x_bar[4];
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
-  const bool gb_s = fold_tma<BN, RB, TAPS, MODE, SW>(p);
-  const Carve cv = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, p.stages, xop_s, gb_s);
+  const bool gb_s = fold_tma<BN, RB, TAPS, MODE, SW, ES>(p);
+  const Carve cv = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, p.stages, xop_s, gb_s);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* etab = reinterpret_cast<float*>(smem + cv.etab);
-  float* sacc = reinterpret_cast<float*>(smem + cv.sacc);
-  float* red = reinterpret_cast<float*>(smem + cv.red);
+  SA* sacc = reinterpret_cast<SA*>(smem + cv.sacc);
+  SA* red = reinterpret_cast<SA*>(smem + cv.red);
   int* rowtab = reinterpret_cast<int*>(smem + cv.rowtab);
   int* rowpix = reinterpret_cast<int*>(smem + cv.rowpix);
   uint32_t* meta = reinterpret_cast<uint32_t*>(smem + cv.meta);
@@ -272,7 +299,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     if (L::WRES && TAPS == 9) {
       // resident weights: packed after the previous optimizer step, i.e. at least two
       // launches back, so they may be fetched before this grid's dependency wait
-      const uint32_t wb = p.nslab * TAPS * BN * RB;
+      const uint32_t wb = p.nslab * TAPS * BN * RB * PL;
       mbar_arrive_expect_tx(&w_bar, wb);
       bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
     }
@@ -327,8 +354,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     }
   }
   for (int c = tid; c < BN; c += ST_THREADS) {
-    sacc[c] = 0.f;
-    sacc[BN + c] = 0.f;
+    sacc[c] = SA(0);
+    sacc[BN + c] = SA(0);
   }
   if (TAPS == 9) {  // window row -> (image block, padded row, padded column), same every tile
     for (int r = tid; r < p.Rld; r += ST_THREADS) {
@@ -346,10 +373,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   if (threadIdx.x == 0) trace_ev(p.trace, 9, 0);
   const uint32_t tmem = tmem_sh;
 
+  // stage: A hi [| A lo] [| x] | B (tap-major [tap][plane][BN][RB])
   auto stage_a = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes; };
-  auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes; };
+  auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * PL; };
   auto stage_b = [&](int s) {
-    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (xop_s ? 2 : 1);
+    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (PL + (xop_s ? 1 : 0));
   };
   auto tile_of = [&](int it, int& mt, int& n0) {
     const int t = (int)blockIdx.x + it * (int)gridDim.x;
@@ -389,7 +417,61 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         mbar_wait(&ld_bar[st], ph);
         if (tid == 0) trace_ev(p.trace, 2, it * p.nslab + s);
         const int cs = min(SLABW, p.ci - s * SLABW);
-        if (need_t && j * 8 < cs) {
+        if constexpr (F32) {
+          // prologue in fp32, then the 3xTF32 split: hi (round-to-nearest TF32) in place,
+          // lo = TF32(f - hi) into the second plane; halo / border positions keep the TMA's
+          // zero fill in hi and get a zero lo
+          uint8_t* A = stage_a(st);
+          uint8_t* AL = A + cv.a_bytes;
+          const uint8_t* X = stage_x(st);
+          const bool live = j * 4 < cs;
+          const int c0 = s * SLABW + j * 4;
+          float t0[4] = {1.f, 1.f, 1.f, 1.f}, t1[4] = {0.f, 0.f, 0.f, 0.f}, t2[4] = {0.f, 0.f, 0.f, 0.f};
+          if (need_t && live) {
+            ld4f(ptab + c0, t0);
+            ld4f(ptab + kpad + c0, t1);
+            ld4f(ptab + 2 * kpad + c0, t2);
+          }
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int r = r0 + u * RS;
+            if (r >= p.Rld) continue;
+            uint32_t off;
+            if constexpr (RB == 128) off = r * 128 + ((j ^ (r & 7)) << 4);
+            else off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+            bool dead = !live;
+            if (TAPS == 9) {
+              const int wr = rowtab[r];
+              const int y = y0 + ((wr >> 10) & 1023), rx = wr & 1023;
+              dead = dead || (unsigned)y >= (unsigned)p.h || rx < 1 || rx > p.w || img0 + (wr >> 20) >= p.n;
+            }
+            if (dead) {
+              *reinterpret_cast<uint4*>(AL + off) = make_uint4(0, 0, 0, 0);
+              continue;
+            }
+            const float4 a4 = *reinterpret_cast<const float4*>(A + off);
+            float f[4] = {a4.x, a4.y, a4.z, a4.w};
+            if (PRO == BNFF_PRO_RELU) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) f[i] = fmaxf(f[i], 0.f);
+            } else if (PRO == BNFF_PRO_BN_RELU) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) f[i] = fmaxf(fmaf(f[i], t0[i], t1[i]), 0.f);
+            } else if (PRO == BNFF_PRO_BN_DX) {
+              const float4 x4 = *reinterpret_cast<const float4*>(X + off);
+              const float xf[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) f[i] = fmaf(f[i], t0[i], fmaf(xf[i], t1[i], t2[i]));
+            }
+            float4 hi, lo;
+            hi.x = tf32_rn(f[0]); hi.y = tf32_rn(f[1]); hi.z = tf32_rn(f[2]); hi.w = tf32_rn(f[3]);
+            lo.x = tf32_rn(f[0] - hi.x); lo.y = tf32_rn(f[1] - hi.y);
+            lo.z = tf32_rn(f[2] - hi.z); lo.w = tf32_rn(f[3] - hi.w);
+            *reinterpret_cast<float4*>(A + off) = hi;
+            *reinterpret_cast<float4*>(AL + off) = lo;
+          }
+          fence_proxy_async_smem();
+        } else if (need_t && j * 8 < cs) {
           const int c0 = s * SLABW + j * 8;
           float t0[8], t1[8], t2[8];
           ld8f(ptab + c0, t0);
@@ -459,8 +541,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     {  // converged warp; one elected lane issues the copies
       if (TAPS == 1 && L::WRES && elect_one()) {  // this CTA's N tile of every slab, once
         const int n0r = ((int)blockIdx.x % p.ntiles) * BN;
-        mbar_arrive_expect_tx(&w_bar, (uint32_t)(p.nslab * BN * RB));
-        for (int s = 0; s < p.nslab; ++s)
+        mbar_arrive_expect_tx(&w_bar, (uint32_t)(p.nslab * BN * RB * PL));
+        for (int s = 0; s < p.nslab * PL; ++s)  // [slab][plane] rows of the pack
           bulk_g2s(smem_u32(smem + cv.wres) + s * BN * RB, p.wpk + ((long long)s * p.npad + n0r) * RB, BN * RB,
                    &w_bar);
       }
@@ -478,12 +560,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
           trace_ev(p.trace, 1, it * p.nslab + s);
           if (elect_one()) {
-            if (!L::WRES) {  // this slab's weights for the N tile, every tap ([slab][tap][npad][RB] pack)
-              mbar_arrive_expect_tx(&full_bar[st], TAPS * BN * RB);
+            if (!L::WRES) {  // this slab's weights for the N tile, every tap ([slab][tap][plane][npad][RB])
+              mbar_arrive_expect_tx(&full_bar[st], TAPS * BN * RB * PL);
 #pragma unroll 1
-              for (int u = 0; u < TAPS; ++u)
+              for (int u = 0; u < TAPS * PL; ++u)
                 bulk_g2s(smem_u32(stage_b(st)) + u * BN * RB,
-                         p.wpk + ((long long)(s * TAPS + u) * p.npad + n0) * RB, BN * RB, &full_bar[st]);
+                         p.wpk + ((long long)(s * TAPS * PL + u) * p.npad + n0) * RB, BN * RB, &full_bar[st]);
             }
             mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
             const int c = s * SLABW;
@@ -506,7 +588,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     // the whole warp runs the loop (converged, warp-uniform operands); one elected lane issues
     {
       if (L::WRES) mbar_wait(&w_bar, 0);
-      constexpr uint32_t idesc = make_idesc(128, BN, kFmtBF16, 0, 0);
+      constexpr uint32_t idesc = make_idesc(128, BN, F32 ? kFmtTF32 : kFmtBF16, 0, 0);
+      constexpr int KE = F32 ? 8 : 16;  // K elements per MMA (32 bytes either way)
       const uint32_t wres = smem_u32(smem + cv.wres);
       int st = 0;
       uint32_t ph = 0;
@@ -521,19 +604,27 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           trace_ev(p.trace, 4, it * p.nslab + s);
           tc_fence_after();
           const uint32_t abase = smem_u32(stage_a(st));
-          const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB : smem_u32(stage_b(st));
-          const int ks = min(SLABW, p.ci - s * SLABW) / 16;
+          const uint32_t bbase = L::WRES ? wres + s * TAPS * BN * RB * PL : smem_u32(stage_b(st));
+          const int ks = min(SLABW, p.ci - s * SLABW) / KE;
           // descriptors advance by adding (byte offset >> 4) to the start-address field
           const uint64_t a0 = make_sdesc(abase, 16, L::SBO, L::LAY);
           const uint64_t b0 = make_sdesc(bbase, 16, L::SBO, L::LAY);
 #pragma unroll
           for (int u = 0; u < TAPS; ++u) {
             const uint32_t ash = TAPS == 9 ? (uint32_t)(((u / 3) * p.wp + (u % 3)) * RB) >> 4 : 0u;
-            const uint32_t bsh = (uint32_t)(u * BN * RB) >> 4;
+            const uint32_t bsh = (uint32_t)(u * PL * BN * RB) >> 4;
 #pragma unroll
-            for (int kk = 0; kk < SLABW / 16; ++kk) {
+            for (int kk = 0; kk < SLABW / KE; ++kk) {
               if (kk < ks) {
-                umma_f16_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                if constexpr (F32) {  // 3xTF32: hi*hi + hi*lo + lo*hi
+                  constexpr uint32_t blo = (uint32_t)(BN * RB) >> 4;
+                  const uint32_t alo = (uint32_t)cv.a_bytes >> 4;
+                  umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                  umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + blo + kk * 2, idesc, 1u);
+                  umma_tf32_elect(d, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
+                } else {
+                  umma_f16_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                }
                 acc = 1;
               }
             }
@@ -565,7 +656,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const int bar_id = 2 + grp;
     uint8_t* stg = smem + cv.stg + grp * L::NSTG * L::STG;
     uint8_t* xs0 = stg + L::STG;             // dgrad: x buffers, one per owned chunk
-    float* gred = red + grp * 512;
+    SA* gred = red + grp * 512;
     int* gpix = rowpix + grp * 128;
     const int hpwp = p.hp * p.wp;
     constexpr int CW = L::CW, NCH = L::NCH, MYCH = L::MYCH;
@@ -576,15 +667,18 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const bool nrc = MODE == M_DGRAD && EPI >= BNFF_DG_NRC;
     // out (+)= scale * dt1: the ICF fold exists for 1x1 dgrads only (the host rejects it for 3x3),
     // so the 3x3 instantiations carry no fold code
-    const bool fold = MODE == M_DGRAD && TAPS == 1 && EPI >= BNFF_DG_NRC_ACC;
-    const bool fold_acc = MODE == M_DGRAD && TAPS == 1 && EPI == BNFF_DG_NRC_ACC;
+    const bool fold = !F32 && MODE == M_DGRAD && TAPS == 1 && EPI >= BNFF_DG_NRC_ACC;
+    const bool fold_acc = !F32 && MODE == M_DGRAD && TAPS == 1 && EPI == BNFF_DG_NRC_ACC;
+    E* const outp = reinterpret_cast<E*>(p.out);
+    const E* const exq = reinterpret_cast<const E*>(p.ex);
+    constexpr int EPC = 16 / ES;             // elements per 16-byte chunk
     // TMA-store epilogue (64-column chunks): the staged chunk leaves by one bulk tensor store;
     // the 1x1 fold also loads the old block-gradient tile by TMA one tile ahead, folds it in
     // place in shared memory during the row pass and stores it back
     // 64-column chunks always take the TMA path (the host encodes the descriptors or declines the
     // window kernel), so the register-store / register-fold variants exist for narrow chunks only
-    const bool tfold = CW == 64 && fold;  // == gb_s (fold_tma)
-    constexpr bool tst = CW == 64;
+    const bool tfold = L::TST && fold;  // == gb_s (fold_tma)
+    constexpr bool tst = L::TST;
     uint8_t* gb0 = smem + cv.gbuf + grp * MYCH * 128 * 128;
     const bool tx = tst && need_x;  // x tiles by TMA into 128B-swizzled rows
     // 3x3 boxes cover kt*wp (or kt*hp*wp) rows; the rows below never receive data: zero once
@@ -598,9 +692,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     }
     const bool stats = do_stats && (MODE == M_FPROP || nrc);
     const bool persist = true;  // grid % ntiles == 0: a CTA's columns never change, sums stay in registers
-    float2 acc1[MYCH], acc2[MYCH];
+    struct D2 { double x, y; };
+    using P2 = typename std::conditional<F32, D2, float2>::type;  // a column pair's running sums
+    P2 acc1[MYCH], acc2[MYCH];
 #pragma unroll
-    for (int k = 0; k < MYCH; ++k) { acc1[k] = make_float2(0.f, 0.f); acc2[k] = make_float2(0.f, 0.f); }
+    for (int k = 0; k < MYCH; ++k) { acc1[k] = P2{SA(0), SA(0)}; acc2[k] = P2{SA(0), SA(0)}; }
     auto out_pix = [&](int mt, int m) {
       // output row m of m-tile mt -> output pixel (or -1: a padding column / row past the map)
       if (TAPS == 1) {
@@ -647,8 +743,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         const int col = n0b + (grp + 2 * k) * CW;
         const bool ok = pix >= 0 && col < p.N;
 #pragma unroll
-        for (int i = 0; i < CW / 8; ++i)
-          cp_async16(dst + i * 16, p.ex + (ok ? (long long)pix * p.ex_rs + col + i * 8 : 0), ok ? 16u : 0u);
+        for (int i = 0; i < CW / EPC; ++i)
+          cp_async16(dst + i * 16, exq + (ok ? (long long)pix * p.ex_rs + col + i * EPC : 0), ok ? 16u : 0u);
       }
       cp_async_commit();
     };
@@ -659,12 +755,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       gred[(rg * 4 + 1) * HALF + cp] = acc1[k].y;
       gred[(rg * 4 + 2) * HALF + cp] = acc2[k].x;
       gred[(rg * 4 + 3) * HALF + cp] = acc2[k].y;
-      acc1[k] = make_float2(0.f, 0.f);
-      acc2[k] = make_float2(0.f, 0.f);
+      acc1[k] = P2{SA(0), SA(0)};
+      acc2[k] = P2{SA(0), SA(0)};
       named_bar_sync(bar_id, 128);
       if (gt < CW) {
         const int c = gt, pc = c >> 1, odd = c & 1;
-        float s1 = 0.f, s2 = 0.f;
+        SA s1 = SA(0), s2 = SA(0);
         for (int q = 0; q < RG; ++q) {
           s1 += gred[(q * 4 + odd) * HALF + pc];
           s2 += gred[(q * 4 + 2 + odd) * HALF + pc];
@@ -722,7 +818,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             const int px = gpix[r];
             const int col = n0 + cc + ch * 8;
             gold[i] = (px >= 0 && col < p.N)
-                          ? *reinterpret_cast<const uint4*>(p.out + (long long)px * p.out_rs + col)
+                          ? *reinterpret_cast<const uint4*>(outp + (long long)px * p.out_rs + col)
                           : make_uint4(0, 0, 0, 0);
           }
         } else {
@@ -749,7 +845,15 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
           } else {
             if (need_x) {
               float xv[16];
-              if (tx) {
+              if constexpr (F32) {  // 16 fp32 = four 16-byte chunks
+                const uint8_t* xb = xs0 + k * L::STG + row * (tx ? 128 : L::SROWB);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const int j = (c16 >> 2) + q;
+                  const float4 t = *reinterpret_cast<const float4*>(xb + (tx ? ((j ^ (row & 7)) << 4) : j * 16));
+                  xv[4 * q] = t.x; xv[4 * q + 1] = t.y; xv[4 * q + 2] = t.z; xv[4 * q + 3] = t.w;
+                }
+              } else if (tx) {
                 const uint8_t* xb = xs0 + k * L::STG + row * 128;
                 const int j = c16 >> 3;
                 unpack8(*reinterpret_cast<const uint4*>(xb + ((j ^ (row & 7)) << 4)), xv);
@@ -779,7 +883,14 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
               for (int i = 0; i < 16; ++i) v[i] = 0.f;
             }
           }
-          if (tst) {  // dense 128-byte rows, 128B swizzle (the TMA store's box layout)
+          if constexpr (F32) {  // fp32 staging: 16 values = four 16-byte chunks
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int j = (c16 >> 2) + q;
+              const uint32_t o = tst ? row * 128 + ((j ^ (row & 7)) << 4) : row * L::SROWB + j * 16;
+              *reinterpret_cast<float4*>(stg + o) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          } else if (tst) {  // dense 128-byte rows, 128B swizzle (the TMA store's box layout)
             const int j = c16 >> 3;
             const int o0 = row * 128 + ((j ^ (row & 7)) << 4), o1 = row * 128 + (((j + 1) ^ (row & 7)) << 4);
             *reinterpret_cast<uint4*>(stg + o0) = pack8(v, false);
@@ -834,9 +945,37 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         }
         if (et == 0) trace_ev(p.trace, 11, it * 4 + k);
         // ---- column pass: sums of the stored values (FPROP: y, y^2; NRC: dt1, dt1*xhat)
-        if (stats) {
+        if (stats && F32) {  // fp32 staging: a column pair is 8 bytes; float64 sums
+          const float* sf = reinterpret_cast<const float*>(stg);
+          const float* xf = reinterpret_cast<const float*>(xs0 + k * L::STG);
+          SA a0 = acc1[k].x, a1 = acc1[k].y, b0 = acc2[k].x, b1 = acc2[k].y;
+          const int gc = n0 + cc + 2 * cp;
+          float hinv0 = 0.f, hinv1 = 0.f, hsh0 = 0.f, hsh1 = 0.f;
+          if (MODE == M_DGRAD) {
+            hinv0 = etab[2 * p.npad + gc]; hinv1 = etab[2 * p.npad + gc + 1];
+            hsh0 = etab[3 * p.npad + gc]; hsh1 = etab[3 * p.npad + gc + 1];
+          }
+#pragma unroll 16
+          for (int r = rg; r < 128; r += RG) {
+            const int w = tst ? r * 32 + ((((cp >> 1) ^ (r & 7)) << 2) | ((2 * cp) & 3)) : r * (L::SROWB / 4) + 2 * cp;
+            const float f0 = sf[w], f1 = sf[w + 1];
+            a0 += (SA)f0;
+            a1 += (SA)f1;
+            if (MODE == M_FPROP) {
+              b0 += (SA)f0 * (SA)f0;
+              b1 += (SA)f1 * (SA)f1;
+            } else {
+              const int wx = tx ? r * 32 + ((((cp >> 1) ^ (r & 7)) << 2) | ((2 * cp) & 3)) : r * (L::SROWB / 4) + 2 * cp;
+              b0 += (SA)f0 * (SA)fmaf(xf[wx], hinv0, hsh0);
+              b1 += (SA)f1 * (SA)fmaf(xf[wx + 1], hinv1, hsh1);
+            }
+          }
+          acc1[k] = P2{a0, a1};
+          acc2[k] = P2{b0, b1};
+        } else if (stats) {
           const uint32_t* s32 = reinterpret_cast<const uint32_t*>(stg);
-          float2 a = acc1[k], b = acc2[k];
+          float2 a = make_float2((float)acc1[k].x, (float)acc1[k].y);
+          float2 b = make_float2((float)acc2[k].x, (float)acc2[k].y);
           if (MODE == M_FPROP) {
 #pragma unroll 32
             for (int r = rg; r < 128; r += RG) {
@@ -863,8 +1002,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
               b = __ffma2_rn(f, xh, b);
             }
           }
-          acc1[k] = a;
-          acc2[k] = b;
+          acc1[k] = P2{a.x, a.y};
+          acc2[k] = P2{b.x, b.y};
         }
         if (et == 0) trace_ev(p.trace, 12, it * 4 + k);
         // ---- store pass
@@ -885,7 +1024,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
               unpack8(gold[i], o);
 #pragma unroll
               for (int e = 0; e < 8; ++e) d[e] = fold_acc ? fmaf(sc[e], d[e], o[e]) : sc[e] * d[e];
-              *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = pack8(d, false);
+              *reinterpret_cast<uint4*>(outp + (long long)px * p.out_rs + col) = pack8(d, false);
             }
           }
         } else if (tst) {
@@ -894,14 +1033,15 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             fetch_g(it + 1, k); // the fold tile is free: fetch the next tile's old block gradient
           }
         } else {
+          constexpr int CPS = CW * ES / 16;  // 16-byte chunks per staged row
 #pragma unroll 2
-          for (int kk = gt; kk < 128 * CPO; kk += 128) {
-            const int r = kk / CPO, ch = kk - r * CPO;
+          for (int kk = gt; kk < 128 * CPS; kk += 128) {
+            const int r = kk / CPS, ch = kk - r * CPS;
             const int px = gpix[r];
-            const int col = n0 + cc + ch * 8;
+            const int col = n0 + cc + ch * EPC;
             if (px >= 0 && col < p.N) {
               const uint4 vv = *reinterpret_cast<const uint4*>(stg + r * L::SROWB + ch * 16);
-              *reinterpret_cast<uint4*>(p.out + (long long)px * p.out_rs + col) = vv;
+              *reinterpret_cast<uint4*>(outp + (long long)px * p.out_rs + col) = vv;
             }
           }
         }
@@ -1497,6 +1637,62 @@ __global__ void pack_window_kernel(const float* __restrict__ w, int co_n, int ci
   }
 }
 
+// fp32 (3xTF32) pack: [slab][tap][plane][npad][RB] with plane 0 = TF32(w) (round to nearest),
+// plane 1 = TF32(w - hi); slabs of RB/4 channels, same 16-byte chunk swizzle
+__device__ __forceinline__ void pack_f32_elem(const float* __restrict__ w, int co_n, int ci_n, int kh, int kw,
+                                              int dgrad, int CI, int N, int npad, int RB, long long i,
+                                              float* __restrict__ out) {
+  const int taps = kh * kw;
+  const int slabw = RB / 4;
+  const int k = (int)(i % slabw);
+  long long t = i / slabw;
+  const int n = (int)(t % npad);
+  t /= npad;
+  const int u = (int)(t % taps);
+  const int s = (int)(t / taps);
+  const int ch = s * slabw + k;
+  float v = 0.f;
+  if (n < N && ch < CI) {
+    int ky = u / kw, kx = u % kw;
+    int co, ci;
+    if (dgrad) { ky = kh - 1 - ky; kx = kw - 1 - kx; co = ch; ci = n; }
+    else { co = n; ci = ch; }
+    v = w[(((long long)co * ci_n + ci) * kh + ky) * kw + kx];
+  }
+  const float hi = tf32_rn(v), lo = tf32_rn(v - hi);
+  const int kb = k * 4;
+  int chunk = kb >> 4;
+  chunk ^= RB == 128 ? (n & 7) : ((n >> 1) & 3);
+  const long long row = ((long long)s * taps + u) * 2;  // plane 0 row block; plane 1 = +1
+  const long long b0 = (row * npad + n) * RB + chunk * 16 + (kb & 15);
+  const long long b1 = ((row + 1) * npad + n) * RB + chunk * 16 + (kb & 15);
+  out[b0 / 4] = hi;
+  out[b1 / 4] = lo;
+}
+__global__ void pack_window_f32_kernel(const float* __restrict__ w, int co_n, int ci_n, int kh, int kw, int dgrad,
+                                       int CI, int N, int npad, int RB, int nslab, float* __restrict__ out) {
+  griddep_launch();
+  griddep_wait();
+  const long long total = (long long)nslab * kh * kw * npad * (RB / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    pack_f32_elem(w, co_n, ci_n, kh, kw, dgrad, CI, N, npad, RB, i, out);
+}
+__global__ void pack_window_multi_f32_kernel(const bnff_pack_job* __restrict__ jobs) {
+  griddep_launch();
+  griddep_wait();
+  const bnff_pack_job jb = jobs[blockIdx.y];
+  const int d = blockIdx.z;
+  void* out = d ? jb.wdgrad : jb.wfwd;
+  if (!out) return;
+  const int CI = d ? jb.c_out : jb.c_in, N = d ? jb.c_in : jb.c_out;
+  const Geo gg = geo(CI, N, jb.kh, jb.kw, d, 4);
+  const long long total = (long long)gg.nslab * jb.kh * jb.kw * gg.npad * (gg.RB / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    pack_f32_elem(jb.w, jb.c_out, jb.c_in, jb.kh, jb.kw, d, CI, N, gg.npad, gg.RB, i, (float*)out);
+}
+
 // one launch re-packing many convs (after each optimizer step): grid (x, job, fwd|dgrad)
 __global__ void pack_window_multi_kernel(const bnff_pack_job* __restrict__ jobs) {
   griddep_launch();
@@ -1559,15 +1755,15 @@ int num_sms_wc() {
   return n;
 }
 
-template <int BN, int RB, int TAPS, int MODE, bool SW = false>
+template <int BN, int RB, int TAPS, int MODE, bool SW = false, int ES = 2>
 static int launch_t(WcParams p, cudaStream_t st) {
-  auto kern = wconv_kernel<BN, RB, TAPS, MODE, SW>;
+  auto kern = wconv_kernel<BN, RB, TAPS, MODE, SW, ES>;
   int stages = 8;
   Carve c{};
   const bool xop = MODE == M_DGRAD && p.pro == BNFF_PRO_BN_DX;
-  bool gb = fold_tma<BN, RB, TAPS, MODE, SW>(p);
+  bool gb = fold_tma<BN, RB, TAPS, MODE, SW, ES>(p);
   for (; stages >= 2; --stages) {
-    c = carve<BN, RB, TAPS, MODE, SW>(p.R, p.nslab, p.npad, stages, xop, gb);
+    c = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, stages, xop, gb);
     if (c.total <= SMEM_BUDGET) break;
   }
   if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
@@ -1593,6 +1789,23 @@ inline bool wres1_enabled() {  // BNFF_WRES1=0: stream 1x1 fprop weights per sta
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v != 0;
+}
+// fp32 (3xTF32) instantiations: 1x1 with 128-byte slabs, N tiles 32..128 (dgrad <= 64);
+// 3x3 with 64-byte slabs and streamed weights, N tiles 32 / 64
+template <int MODE, int TAPS>
+static int dispatch_f32(const WcParams& p, int BN, int RB, cudaStream_t st) {
+  if (TAPS == 9) {
+    if (BN == 32) return launch_t<32, 64, TAPS, MODE, true, 4>(p, st);
+    return launch_t<64, 64, TAPS, MODE, true, 4>(p, st);
+  }
+  if (RB == 64) return launch_t<32, 64, TAPS, MODE, false, 4>(p, st);
+  switch (BN) {
+    case 32: return launch_t<32, 128, TAPS, MODE, false, 4>(p, st);
+    case 64: return launch_t<64, 128, TAPS, MODE, false, 4>(p, st);
+    default:
+      if constexpr (MODE == M_FPROP) return launch_t<128, 128, TAPS, MODE, false, 4>(p, st);
+      else return kWindowNoFit;
+  }
 }
 template <int MODE, int TAPS>
 static int dispatch(const WcParams& p, int BN, int RB, cudaStream_t st, int sw = 0) {
@@ -1628,6 +1841,18 @@ using namespace bnff;
 namespace bnff {
 namespace wc {
 template <int MODE, int TAPS>
+static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop) {
+  Carve c{};
+  if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop)
+                              : carve<64, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop);
+  else if (RB == 64) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
+  else if (BN == 32) c = carve<32, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
+  else if (BN == 64) c = carve<64, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
+  else if (MODE == M_FPROP) c = carve<128, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
+  else return false;
+  return c.total <= SMEM_BUDGET;
+}
+template <int MODE, int TAPS>
 static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw = 0) {
   Carve c{};
 #define BNFF_FIT(bn, rb) c = carve<bn, rb, TAPS, MODE>(R, nslab, npad, 2, xop)
@@ -1652,7 +1877,8 @@ static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw =
 // three passes: the shared-memory plan must fit with >= 2 stages in the worst case
 extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
                               int32_t stride, int32_t pad, int32_t h, int32_t w) {
-  if (dtype != BNFF_BF16 || stride != 1) return 0;
+  if ((dtype != BNFF_BF16 && dtype != BNFF_F32) || stride != 1) return 0;
+  const int es = dtype == BNFF_F32 ? 4 : 2;
   if (!((kh == 1 && kw == 1 && pad == 0) || (kh == 3 && kw == 3 && pad == 1))) return 0;
   if (c_in % 16 || c_out % 16) return 0;
   if (kh == 3) {
@@ -1663,7 +1889,15 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
   const int R = 128 + (kh == 3 ? 2 * (w + 2) + 2 : 0);
   for (int d = 0; d < 2; ++d) {
     const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
-    const wc::Geo g = wc::geo(CI, N, kh, kw, d);
+    const wc::Geo g = wc::geo(CI, N, kh, kw, d, es);
+    if (es == 4) {
+      const bool ok4 = kh == 3 ? (d ? wc::fits2_f32<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true)
+                                    : wc::fits2_f32<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false))
+                               : (d ? wc::fits2_f32<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
+                                    : wc::fits2_f32<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false));
+      if (!ok4) return 0;
+      continue;
+    }
     const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, g.sw)
                                  : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, g.sw))
                             : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
@@ -1675,15 +1909,33 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
 
 extern "C" int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_t kh,
                                          int32_t kw, int32_t dgrad) {
-  if (dtype != BNFF_BF16) return 0;
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return 0;
+  const int es = dtype == BNFF_F32 ? 4 : 2;
   const int CI = dgrad ? c_out : c_in, N = dgrad ? c_in : c_out;
-  const wc::Geo g = wc::geo(CI, N, kh, kw, dgrad);
-  return (int64_t)g.nslab * g.taps * g.npad * (g.RB / 2);  // elements
+  const wc::Geo g = wc::geo(CI, N, kh, kw, dgrad, es);
+  // elements: [slab][tap][plane][npad][RB bytes]; fp32 has hi and lo planes
+  return (int64_t)g.nslab * g.taps * g.npad * (g.RB / es) * (es == 4 ? 2 : 1);
 }
 
 extern "C" int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t kh,
                                 int32_t kw, void* fwd, void* dgr, void* stream) {
-  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window: bf16 only");
+  if (dtype == BNFF_F32) {
+    for (int d = 0; d < 2; ++d) {
+      void* out = d ? dgr : fwd;
+      if (!out) continue;
+      const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
+      const wc::Geo g = wc::geo(CI, N, kh, kw, d, 4);
+      const long long total = (long long)g.nslab * g.taps * g.npad * (g.RB / 4);
+      int blocks = (int)((total + 255) / 256);
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      launch(wc::pack_window_f32_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, w, c_out, c_in, kh,
+             kw, d, CI, N, g.npad, g.RB, g.nslab, (float*)out);
+      int rc = check_launch("pack_window f32");
+      if (rc) return rc;
+    }
+    return BNFF_OK;
+  }
+  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window: bf16 / f32");
   for (int d = 0; d < 2; ++d) {
     void* out = d ? dgr : fwd;
     if (!out) continue;
@@ -1707,7 +1959,7 @@ extern "C" int bnff_debug_trace(void* buf) {
 }
 
 // internal entry used by bnff_conv_fprop / bnff_conv_dgrad when bnff_window_ok()
-extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
+extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t pad, bnff_view in, bnff_view in_x,
                                 int32_t pro, bnff_coef pcoef, bnff_view out, const void* wwin,
                                 const float* bias, int32_t epi, bnff_view ex, bnff_coef ecoef,
                                 double* stat_part, void* stream) {
@@ -1723,11 +1975,14 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   p.fd_wp = make_fastdiv(p.wp);
   p.ci = (int)in.c;
   p.N = (int)out.c;
-  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode);
+  const int es = dtype == BNFF_F32 ? 4 : 2;
+  if (es == 4 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
+    return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is bf16-only");
+  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode, es);
   p.nslab = g.nslab;
   p.npad = g.npad;
   p.ntiles = g.ntiles;
-  const int slabw = g.RB / 2;
+  const int slabw = g.RB / es;
   uint32_t box[4];
   int rank;
   if (kh == 3) {
@@ -1764,36 +2019,36 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
     box[0] = slabw; box[1] = 128;
   }
   p.tiles = p.mtiles * p.ntiles;
-  // TMA epilogue for 64-column chunks (BN >= 128): the output (and dgrad x mask) descriptors are
-  // required; if they cannot be encoded the window kernel declines (generic implicit GEMM)
+  // TMA epilogue for 128-byte staged chunks (bf16: 64 columns, BN >= 128; fp32: 32 columns,
+  // BN >= 64): the output (and dgrad x mask) descriptors are required; if they cannot be
+  // encoded the window kernel declines (generic implicit GEMM)
   p.tstore = 0;
-  if (g.BN >= 128) {
+  const int cw128 = 128 / es;  // columns of a 128-byte staged row
+  if (es == 4 ? g.BN >= 64 : g.BN >= 128) {
     uint32_t ob[4];
     if (kh == 3) {
-      ob[0] = 64; ob[1] = p.wp; ob[2] = p.tmode == 2 ? p.hp : p.kt; ob[3] = p.tmode == 2 ? p.kt : 1;
+      ob[0] = cw128; ob[1] = p.wp; ob[2] = p.tmode == 2 ? p.hp : p.kt; ob[3] = p.tmode == 2 ? p.kt : 1;
     } else {
-      ob[0] = 64; ob[1] = 128;
+      ob[0] = cw128; ob[1] = 128;
     }
-    p.tstore = encode_nhwc_bf16(&p.tma_out, out.ptr, out.n, out.h, out.w, out.c, out.row_stride, rank, ob) ? 1 : 0;
+    p.tstore = encode_nhwc(&p.tma_out, es, out.ptr, out.n, out.h, out.w, out.c, out.row_stride, rank, ob) ? 1 : 0;
     if (p.tstore && mode == 1 && epi != BNFF_DG_PLAIN &&
-        !encode_nhwc_bf16(&p.tma_ex, ex.ptr, ex.n, ex.h, ex.w, ex.c, ex.row_stride, rank, ob))
+        !encode_nhwc(&p.tma_ex, es, ex.ptr, ex.n, ex.h, ex.w, ex.c, ex.row_stride, rank, ob))
       p.tstore = 0;
     if (!p.tstore) return wc::kWindowNoFit;
   }
-  if (!encode_nhwc_bf16(&p.tma_a, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
+  if (!encode_nhwc(&p.tma_a, es, in.ptr, in.n, in.h, in.w, in.c, in.row_stride, rank, box))
     return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (window operand)");
   if (mode == 1 && pro == BNFF_PRO_BN_DX &&
-      !encode_nhwc_bf16(&p.tma_x, in_x.ptr, in_x.n, in_x.h, in_x.w, in_x.c, in_x.row_stride, rank, box))
+      !encode_nhwc(&p.tma_x, es, in_x.ptr, in_x.n, in_x.h, in_x.w, in_x.c, in_x.row_stride, rank, box))
     return set_error(BNFF_ERR_CUDA, "wconv: cuTensorMapEncodeTiled failed (x operand)");
-  p.src = (const __nv_bfloat16*)in.ptr; p.src_rs = in.row_stride;
-  p.srcx = (const __nv_bfloat16*)in_x.ptr; p.srcx_rs = in_x.row_stride;
   p.pro = pro;
   p.pcoef = pcoef;
   p.wpk = (const uint8_t*)wwin;
-  p.out = (__nv_bfloat16*)out.ptr; p.out_rs = out.row_stride;
+  p.out = out.ptr; p.out_rs = out.row_stride;
   p.bias = bias;
   p.epi = epi;
-  p.ex = (const __nv_bfloat16*)ex.ptr; p.ex_rs = ex.row_stride;
+  p.ex = ex.ptr; p.ex_rs = ex.row_stride;
   p.ecoef = ecoef;
   p.stat_part = stat_part;
   p.trace = g_wc_trace;
@@ -1801,6 +2056,11 @@ extern "C" int bnff_window_conv(int32_t mode, int32_t kh, int32_t pad, bnff_view
   if (kh == 3 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
     return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is a 1x1 dgrad epilogue");
   cudaStream_t st = (cudaStream_t)stream;
+  if (es == 4) {
+    if (mode == 0)
+      return kh == 3 ? wc::dispatch_f32<wc::M_FPROP, 9>(p, g.BN, g.RB, st) : wc::dispatch_f32<wc::M_FPROP, 1>(p, g.BN, g.RB, st);
+    return kh == 3 ? wc::dispatch_f32<wc::M_DGRAD, 9>(p, g.BN, g.RB, st) : wc::dispatch_f32<wc::M_DGRAD, 1>(p, g.BN, g.RB, st);
+  }
   if (mode == 0) {
     return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st, g.sw)
                    : wc::dispatch<wc::M_FPROP, 1>(p, g.BN, g.RB, st);
@@ -1936,10 +2196,30 @@ extern "C" int bnff_window_wgrad(bnff_view x, int32_t x_pro, bnff_coef x_coef, b
   return check_launch("wgrad window reduce");
 }
 
+// fixed-order split reduction of [splits][taps][cin][cout] partials into dW (co, ci, kh, kw) and
+// of [splits][cout] into dbias (shared by the bf16 window wgrad and wgrad32.cu)
+extern "C" int bnff_wgrad_reduce(const float* ws, int32_t splits, int32_t taps, int32_t cin, int32_t cout,
+                                 int32_t cin_real, float* dw, const float* wsb, float* dbias, void* stream) {
+  const int M4 = taps * cin * (cout / 4);
+  int blocks = (M4 + 31) / 32;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  launch(wc::wg_reduce_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, ws, splits, taps, cin, cout,
+         cin_real > 0 ? cin_real : cin, dw, wsb, dbias);
+  return check_launch("wgrad reduce");
+}
+
 extern "C" int bnff_pack_window_multi(int32_t dtype, int32_t njobs, const bnff_pack_job* jobs_dev,
                                       int64_t max_elems, void* stream) {
-  if (dtype != BNFF_BF16) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window_multi: bf16 only");
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "pack_window_multi: dtype");
   if (njobs <= 0) return BNFF_OK;
+  if (dtype == BNFF_F32) {
+    long long bx = (max_elems / 2 + 255) / 256;  // one thread per (hi, lo) element pair
+    if (bx > 64) bx = 64;
+    if (bx < 1) bx = 1;
+    launch(wc::pack_window_multi_f32_kernel, dim3((unsigned)bx, (unsigned)njobs, 2), dim3(256), 0,
+           (cudaStream_t)stream, jobs_dev);
+    return check_launch("pack_window_multi f32");
+  }
   long long bx = (max_elems / 8 + 255) / 256;  // one thread per 16-byte chunk
   if (bx > 32) bx = 32;
   if (bx < 1) bx = 1;

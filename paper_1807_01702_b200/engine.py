@@ -159,7 +159,7 @@ class Engine:
         self.sync_bn = bool(sync_bn) and self.world > 1
         if self.sync_bn and any(n.kind == G.BN and not n.attrs.onepass for n in g.nodes):
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
-        self.use_window = bool(use_window) and self.dcode == _lib.BF16
+        self.use_window = bool(use_window)
         self.side_wgrad = bool(side_wgrad)
         import os
         self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
@@ -406,7 +406,8 @@ class Engine:
         (conv1x1, col, dw2, kpad) or None when the conv does not qualify."""
         if conv.name in self.cols:
             return self.cols[conv.name]
-        if not (self.use_window and x.shape[3] == 8 and conv.in_c <= 8 and conv.kh * conv.kw > 1):
+        if not (self.use_window and x.shape[3] * x.element_size() == 16 and conv.in_c <= x.shape[3]
+                and conv.kh * conv.kw > 1):
             return None
         kpad = _round_up(conv.kh * conv.kw * conv.in_c, 16)
         n, h, w, _ = x.shape
@@ -750,6 +751,24 @@ class Engine:
                        orig.kw, col[3], _ptr(self.grad(f"{orig.name}.weight")),
                        what=f"cols_to_weight {node.name}", side=self.side_wgrad)
         dx, part = None, None
+        if col is not None and self._wants_dx(node.inputs[0]):
+            # stem input gradient: dgrad of the 1x1 GEMM over the patch matrix (dcol), then a
+            # col2im gather into the channel-padded image layout
+            c1, colt, _, kpad = col
+            dcol = self._empty(tuple(colt.shape))
+            _, wt1, _, _ = self._pack(c1, kpad, (colt.shape[1], colt.shape[2]))
+            da = _lib.DgradArgs(self.dcode, 1, 1, 1, 0, view_of(dy), view_of(dy_x), dy_pro, dy_coef,
+                                view_of(dcol), view_of(colt), _ptr(wt1), _lib.DG_PLAIN, coef_of(), 0,
+                                self._wwin(c1, 1))
+            self._keep.append(da)
+            n_, h_, w_, _ = dcol.shape
+            extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
+            self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
+                       nbytes=_nb(dy, dcol, wt1) + extra, flops=2 * n_ * h_ * w_ * kpad * dy.shape[3])
+            dx = self._empty(tuple(x.shape))
+            self._emit(self.L.bnff_col2im, self.dcode, view_of(dcol), orig.in_c, orig.kh, orig.kw,
+                       orig.stride, orig.pad, view_of(dx), what=f"col2im {node.name}", nbytes=_nb(dcol, dx))
+            return dx, None
         if self._wants_dx(node.inputs[0]):
             dx = self._empty(tuple(x.shape)) if dx_out is None else dx_out
             ecoef = coef_of()

@@ -117,7 +117,7 @@ class PackedConv:
               p.kh, p.kw, _ptr(self.wp), _ptr(self.wt), what="pack_weights")
         # window-shift kernel weights (used when the conv/input qualifies, bf16 only)
         self.wf = self.wd = None
-        if window and self.dcode == _lib.BF16 and self.cin_store == p.in_c:
+        if window and self.cin_store == p.in_c:
             nf = L.bnff_window_pack_size(self.dcode, p.out_c, p.in_c, p.kh, p.kw, 0)
             nd = L.bnff_window_pack_size(self.dcode, p.out_c, p.in_c, p.kh, p.kw, 1)
             self.wf = torch.zeros(nf, dtype=dtype, device=device)

@@ -2,7 +2,9 @@
 
 One process per GPU (torchrun), NCCL over NVLink/NVSwitch for the single
 exchange step of the path: the sum all-reduce of the flat fp32 parameter
-gradient buffer between backward and the SGD step.  BN
+gradient buffer, issued in reverse-layer buckets from inside
+backward on a communication stream as each bucket's gradients become final,
+and captured with the rest of the step in one CUDA graph.  BN
 statistics stay per-GPU as in the paper/reference unless ``sync_bn`` is set
 (engine option): then the 2*C float64 (sum, sum^2) of every BN and the 2*C
 (dbeta, dgamma) sums are all-reduced before they are finalised.
@@ -53,23 +55,27 @@ def allreduce_grads(flat: torch.Tensor, group=None):
 
 
 class DPTrainer:
-    """Drive an ``Engine`` data-parallel: captured fwd+bwd graph -> all-reduce ->
-    captured SGD graph.  With world == 1 this is exactly ``Engine.step``."""
+    """Drive an ``Engine`` data-parallel.  With bucketed all-reduces (the default for
+    world > 1, ``Engine(dp_buckets=True)``) the whole step -- forward, backward with the
+    gradient SUM all-reduces issued bucket by bucket on the communication stream, SGD --
+    is ONE captured CUDA graph; otherwise (dp_buckets=False) a fwd+bwd graph, one flat
+    all-reduce, and the SGD graph.  With world == 1 this is exactly ``Engine.step``."""
 
     def __init__(self, engine, group=None):
         self.eng = engine
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.parts = None
+        self.fused = self.world == 1 or getattr(engine, "dp_buckets", False)
 
     def capture(self):
-        if self.world == 1:
+        if self.fused:
             self.eng.capture()
         else:
             self.parts = self.eng.capture(split=True)
 
     def step(self):
-        if self.world == 1:
+        if self.fused:
             self.eng.step()
             return
         if self.parts is None:

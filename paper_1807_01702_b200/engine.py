@@ -141,7 +141,8 @@ class Engine:
 
     def __init__(self, g: G.Graph, dtype: str = "bf16", device="cuda", input_grad: bool = True,
                  save_postrelu: bool = False, lr: float = 0.0, use_window: bool = True,
-                 sync_bn: bool = False, group=None, side_wgrad: bool = True, fold_icf: bool = True):
+                 sync_bn: bool = False, group=None, side_wgrad: bool = True, fold_icf: bool = True,
+                 dp_buckets: bool | None = None, bucket_bytes: int = 4 << 20):
         self.L = _lib.lib()
         self.g = g
         self.dcode = _lib.BF16 if dtype == "bf16" else _lib.F32
@@ -161,6 +162,13 @@ class Engine:
             raise _lib.UnsupportedError("sync_bn needs one-pass statistics (fusion level rcf+mvf or above)")
         self.use_window = bool(use_window)
         self.side_wgrad = bool(side_wgrad)
+        # data parallel: the gradient SUM all-reduce is issued in reverse-layer buckets from
+        # inside backward, on a communication stream, as soon as a bucket's gradients are
+        # final (overlapping the rest of backward; captured in the step's CUDA graph)
+        self.dp_buckets = (self.world > 1) if dp_buckets is None else bool(dp_buckets)
+        self.bucket_bytes = int(bucket_bytes)
+        self._comm = None
+        self.buckets: list = []  # (lo, hi) ranges of the flat gradient, in issue order
         import os
         self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
@@ -666,16 +674,83 @@ class Engine:
             ws = max(ws, self.L.bnff_wgrad_workspace(n, oh, ow, 1, 1, kp, c1.out_c, 0))
         self.wg_ws = self._empty((ws,), torch.float32)
         self._side_reads: list = []  # tensors read by side-stream thunks (pending until the join)
+        self._done_params: set = set()
+        self._bucket_hi = int(self.gflat.numel())
         for node in reversed(g.nodes):
             try:
                 getattr(self, "_b_" + node.kind)(node)
             except ShapeError as e:
                 raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
+            if self.dp_buckets:
+                self._done_params.update(self._params_of(node))
+                self._maybe_bucket(final=False)
+        if self.dp_buckets:
+            self._maybe_bucket(final=True)
         self.input_grads = {}
         for sid in g.inputs:
             gv = self.grads.get(sid)
             self.input_grads[sid] = self._resolve(gv) if (gv is not None and self.input_grad) else None
         self.launch_counts["bwd"] = len(self.bwd)
+
+    @staticmethod
+    def _params_of(node):
+        at = node.attrs
+        names = []
+        conv = getattr(at, "conv", None)
+        if conv is not None:
+            names += [f"{conv.name}.weight", f"{conv.name}.bias"]
+        bn = getattr(at, "bn", None)
+        if bn is not None:
+            names += [f"{bn.name}.gamma", f"{bn.name}.beta"]
+        return names
+
+    def _maybe_bucket(self, final: bool):
+        """Emit an all-reduce of the flat-gradient range [lo, hi) once every parameter in it
+        has its final gradient and the range holds >= bucket_bytes (the remainder at the end).
+        Parameters sit in forward order in the flat buffer and finish in reverse order, so the
+        finished ones form a suffix; a range is only issued while that holds."""
+        hi = self._bucket_hi
+        if final:
+            lo = 0
+        else:
+            done = [self.poff[k] for k in self._done_params if k in self.poff]
+            if not done:
+                return
+            lo = min(o for o, _ in done)
+            # every parameter inside [lo, hi) must be final
+            if any(o < hi and o + n > lo and k not in self._done_params for k, (o, n) in self.poff.items()):
+                return
+            if (hi - lo) * 4 < self.bucket_bytes:
+                return
+        if hi <= lo:
+            return
+        self._emit_grad_allreduce(lo, hi)
+        self._bucket_hi = lo
+
+    def _emit_grad_allreduce(self, lo, hi):
+        import torch.distributed as dist
+        grp = self.group
+        view = self.gflat[lo:hi]
+        self.buckets.append((lo, hi))
+
+        def _ar(stream, v=view):
+            main = torch.cuda.current_stream(self.dev)
+            if self._comm is None:
+                self._comm = torch.cuda.Stream(self.dev)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self._comm.wait_event(ev)
+            if self._side is not None:  # the bucket's weight gradients ran on the side stream
+                ev2 = torch.cuda.Event()
+                ev2.record(self._side)
+                self._comm.wait_event(ev2)
+            with torch.cuda.stream(self._comm):
+                if dist.is_initialized():
+                    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=grp)
+            self._comm_used = True
+        _ar.what = f"grad_allreduce [{lo}, {hi})"
+        _ar.kind, _ar.nbytes, _ar.flops, _ar.launches = "grad_allreduce", 0, 0, 0
+        self._cur.append(_ar)
 
     def _fresh_like(self, t):
         return self._empty(tuple(t.shape))
@@ -1145,6 +1220,11 @@ class Engine:
             ev = torch.cuda.Event()
             ev.record(self._side)
             main.wait_event(ev)
+        if getattr(self, "_comm_used", False):  # the bucketed gradient all-reduces
+            ev = torch.cuda.Event()
+            ev.record(self._comm)
+            main.wait_event(ev)
+            self._comm_used = False
 
     def set_input(self, x):
         """Graph input: NCHW fp32 (numpy or torch, host or device) -> padded NHWC."""

@@ -116,44 +116,79 @@ __global__ void cols_to_weight_kernel(const float* __restrict__ dw2, int co_n, i
 
 // input gradient of the stem conv through its patch matrix: dx[n, iy, ix, ci] = sum over the
 // (ky, kx) taps whose output (oy, ox) = ((iy + pad - ky) / s, (ix + pad - kx) / s) is an
-// integer position inside the map of dcol[n, oy, ox, (ky*kw + kx)*creal + ci]
-// (col2im as a deterministic gather: every dx element sums its taps in fixed order; the
-// storage channels beyond creal are written as zeros).  One thread per (pixel, channel).
+// integer position inside the map of dcol[n, oy, ox, (ky*kw + kx)*creal + ci] (col2im as a
+// deterministic gather).  One CTA per input row: for each of the <= ceil(kh/s) (ky, oy) pairs
+// that reach the row, the kw*creal contiguous patch entries of every output column are staged
+// in shared memory (each dcol element is read exactly once over the grid, in contiguous runs),
+// then one thread per (column, channel) sums its taps in fixed order; storage channels beyond
+// creal are written as zeros.
 template <typename T>
 __global__ void __launch_bounds__(256) col2im_kernel(const T* __restrict__ dcol, long long col_rs, int n, int h,
                                                      int w, int oh, int ow, int kh, int kw, int stride, int pad,
                                                      int creal, int cstore, T* __restrict__ dx, long long dx_rs) {
   griddep_launch();
+  constexpr int EC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+  extern __shared__ uint4 cbuf[];          // [pairs][ow][NC chunks]: the aligned chunks covering a run
+  const int row = blockIdx.x;
+  const int img = row / h, iy = row - img * h;
+  const int E = kw * creal;                // one ky's run of patch entries
+  const int NC = (E + 2 * EC - 2) / EC;    // chunks that can cover a run at any alignment
+  int pky[8], poy[8], np = 0;
+  for (int ky = 0; ky < kh && np < 8; ++ky) {
+    const int ty = iy + pad - ky;
+    if (ty < 0 || ty % stride) continue;
+    const int oy = ty / stride;
+    if (oy >= oh) continue;
+    pky[np] = ky;
+    poy[np] = oy;
+    ++np;
+  }
   griddep_wait();
-  const long long total = (long long)n * h * w * cstore;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int ci = (int)(i % cstore);
-    const long long pix = i / cstore;
-    const int ix = (int)(pix % w);
-    const long long t = pix / w;
-    const int iy = (int)(t % h);
-    const int img = (int)(t / h);
-    float acc = 0.f;
-    if (ci < creal) {
-      for (int ky = 0; ky < kh; ++ky) {
-        const int ty = iy + pad - ky;
-        if (ty < 0 || ty % stride) continue;
-        const int oy = ty / stride;
-        if (oy >= oh) continue;
-        for (int kx = 0; kx < kw; ++kx) {
-          const int tx = ix + pad - kx;
-          if (tx < 0 || tx % stride) continue;
-          const int ox = tx / stride;
-          if (ox >= ow) continue;
-          const long long q = ((long long)img * oh + oy) * ow + ox;
-          acc += (float)dcol[q * col_rs + (ky * kw + kx) * creal + ci];
-        }
+  for (int p = 0; p < np; ++p) {  // 16-byte loads of the aligned chunks around each run
+    const int c0 = pky[p] * E / EC;
+    const T* src = dcol + ((long long)img * oh + poy[p]) * ow * col_rs + (long long)c0 * EC;
+    uint4* dst = cbuf + p * ow * NC;
+    for (int i = threadIdx.x; i < ow * NC; i += blockDim.x) {
+      const int ox = i / NC, c = i - ox * NC;
+      dst[i] = (c0 + c) * EC < col_rs ? *reinterpret_cast<const uint4*>(src + (long long)ox * col_rs + c * EC)
+                                       : make_uint4(0, 0, 0, 0);
+    }
+  }
+  __syncthreads();
+  const T* sb = reinterpret_cast<const T*>(cbuf);
+  T* out = dx + (long long)row * w * dx_rs;
+  // one thread per input column: its <= ceil(kw/s) horizontal taps per staged (ky, oy) pair,
+  // every real channel in registers, one 16-byte store of the whole stored pixel
+  for (int ix = threadIdx.x; ix < w; ix += blockDim.x) {
+    float acc[EC];
+#pragma unroll
+    for (int c = 0; c < EC; ++c) acc[c] = 0.f;
+    const int kx0 = (ix + pad) % stride;
+    for (int p = 0; p < np; ++p) {
+      const int off0 = pky[p] * E - (pky[p] * E / EC) * EC;  // run start inside its first chunk
+      const T* b = sb + (p * ow * NC) * EC + off0;
+      for (int kx = kx0; kx < kw; kx += stride) {
+        const int tx = ix + pad - kx;
+        if (tx < 0) break;
+        const int ox = tx / stride;
+        if (ox >= ow) continue;
+        const T* e = b + ox * NC * EC + kx * creal;
+#pragma unroll
+        for (int c = 0; c < EC; ++c)
+          if (c < creal) acc[c] += (float)e[c];
       }
     }
-    dx[pix * dx_rs + ci] = (T)acc;
+    if (cstore == EC) {
+      __align__(16) T v[EC];
+#pragma unroll
+      for (int c = 0; c < EC; ++c) v[c] = (T)acc[c];
+      *reinterpret_cast<uint4*>(out + (long long)ix * dx_rs) = *reinterpret_cast<const uint4*>(v);
+    } else {
+      for (int c = 0; c < cstore; ++c) out[(long long)ix * dx_rs + c] = (T)(c < EC ? acc[c] : 0.f);
+    }
   }
 }
+
 
 }  // namespace stem
 }  // namespace bnff
@@ -228,17 +263,32 @@ extern "C" int bnff_col2im(int32_t dtype, bnff_view dcol, int32_t c_real, int32_
   if (dcol.n != dx.n || dcol.h != oh || dcol.w != ow || dcol.c < (long long)kh * kw * c_real)
     return set_error(BNFF_ERR_SHAPE, "col2im: dcol (%lld,%lld,%lld,%lld) vs dx", (long long)dcol.n,
                      (long long)dcol.h, (long long)dcol.w, (long long)dcol.c);
-  const long long total = dx.n * dx.h * dx.w * dx.c;
-  if (total == 0) return BNFF_OK;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (dtype == BNFF_F32)
-    launch(stem::col2im_kernel<float>, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream,
+  const long long rows = dx.n * dx.h;
+  if (rows == 0) return BNFF_OK;
+  const int np_max = (kh + stride - 1) / stride;
+  const int ec = dtype == BNFF_F32 ? 4 : 8;
+  const int nc = (kw * c_real + 2 * ec - 2) / ec;
+  if (dcol.row_stride % ec) return set_error(BNFF_ERR_UNSUPPORTED, "col2im: dcol rows not 16-byte aligned");
+  if (c_real > ec || dx.row_stride % ec)
+    return set_error(BNFF_ERR_UNSUPPORTED, "col2im: the image must be stored as one 16-byte pixel");
+  const size_t smem = (size_t)np_max * ow * nc * 16;
+  if (np_max > 8 || smem > 200 * 1024) return set_error(BNFF_ERR_UNSUPPORTED, "col2im: window too large");
+  cudaError_t e = cudaSuccess;
+  if (dtype == BNFF_F32) {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(stem::col2im_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "col2im attr");
+    launch(stem::col2im_kernel<float>, dim3((unsigned)rows), dim3(256), smem, (cudaStream_t)stream,
            (const float*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)oh, (int)ow, kh,
            kw, stride, pad, c_real, (int)dx.c, (float*)dx.ptr, (long long)dx.row_stride);
-  else
-    launch(stem::col2im_kernel<__nv_bfloat16>, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream,
+  } else {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(stem::col2im_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "col2im attr");
+    launch(stem::col2im_kernel<__nv_bfloat16>, dim3((unsigned)rows), dim3(256), smem, (cudaStream_t)stream,
            (const __nv_bfloat16*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)oh,
            (int)ow, kh, kw, stride, pad, c_real, (int)dx.c, (__nv_bfloat16*)dx.ptr, (long long)dx.row_stride);
+  }
   return check_launch("col2im");
 }

@@ -35,6 +35,7 @@ struct P {
   CUtensorMap tma_x, tma_dy, tma_dyx;
   int n, h, w, cin, cout, kh, pad;
   int bw, kt, xb, tpi, KBr, nkb, kpt, splits, MG, NT, units, stages;
+  int RS, rows;  // box row stride (3x3: bw + 2, the two trailing columns are junk) and box rows
   int x_pro;
   bnff_coef x_coef;
   int dy_pro;
@@ -64,6 +65,8 @@ template <int BN, int TAPS>
 __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_constant__ P p) {
   griddep_launch();
   constexpr int NBA = BN / 32;  // B (dy) atoms of 32 fp32 channels
+  constexpr int SPK = TAPS == 9 ? 3 : 1;  // stages per k-block (vertical taps)
+  constexpr int TPS = TAPS == 9 ? 3 : 1;  // taps per stage (horizontal taps)
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* smem = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[MAXST], empty_bar[MAXST], ld_bar[MAXST], accf_bar, acce_bar;
@@ -155,9 +158,15 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
 #pragma unroll
       for (int i = 0; i < 4; ++i) bacc[b][i] = 0.f;
     const int j = tid & 7;          // 16-byte chunk of a 128-byte row
-    const int r = tid >> 3;         // the row (KBr <= 32: one row per thread)
-    const int ly = r / p.bw, lx = r - ly * p.bw;  // its (row, column) inside the k-block
-    const bool rowok = r < p.KBr;
+    const int r0 = tid >> 3;        // rows r0, r0 + 32 (KBr <= 64)
+    // (box row, box column) of this thread's rows; rows past the box stay zero
+    int gly[2], glx[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = r0 + 32 * q;
+      gly[q] = r < p.rows ? r / p.RS : 1 << 20;
+      glx[q] = r < p.rows ? r - gly[q] * p.RS : 0;
+    }
     int st = 0;
     uint32_t ph = 0;
     for (int ui = 0; ui < nun; ++ui) {
@@ -168,8 +177,8 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
         const int kb = sp * p.kpt + k;
         int img, y0, x0;
         kb_org(kb, img, y0, x0);
-        for (int u = 0; u < TAPS; ++u) {
-          const int ty = TAPS == 9 ? u / 3 - p.pad : 0, tx = TAPS == 9 ? u % 3 - p.pad : 0;
+        for (int u = 0; u < SPK; ++u) {  // one stage per vertical tap (3x3) -- the 3 horizontal
+          const int ty = TAPS == 9 ? u - 1 : 0;  // taps read it through K-row-shifted descriptors
           mbar_wait(&ld_bar[st], ph);
           uint8_t* A = stage(st);
           uint8_t* AL = A + AB;
@@ -186,10 +195,15 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
 #pragma unroll
               for (int i = 0; i < 4; ++i) { t0[i] = ptab[c0 + i]; t1[i] = ptab[cin_pad + c0 + i]; }
             }
-            if (rowok) {
-              const int y = y0 + ly + ty, xx = x0 + lx + tx;
-              const bool in = live && ly < p.kt && y0 + ly < p.h && x0 + lx < p.w &&
-                              (unsigned)y < (unsigned)p.h && (unsigned)xx < (unsigned)p.w;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int r = r0 + 32 * q;
+              if (r >= p.KBr) break;
+              const int ly = gly[q], lx = glx[q];
+              // input position of box row r: row y0+ly+ty, column x0+lx (1x1) / x0-1+lx (3x3)
+              const int y = y0 + ly + ty, xx = x0 + lx - (TAPS == 9 ? 1 : 0);
+              const bool in = live && ly < p.kt && (unsigned)y < (unsigned)p.h && (unsigned)xx < (unsigned)p.w &&
+                              (TAPS == 9 || x0 + lx < p.w);
               // the TMA writes 128B-swizzled rows (16-byte chunk j at j ^ (r & 7)); the MN-major
               // TF32 operand layout (128B_BASE32B) wants 32-byte chunks at (j/2) ^ (r & 3): every
               // row is permuted in place by its 8 threads (all read, then all write)
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
             }
           }
           // B: dy (BN_DX-transformed when deferred) at the k-block's output positions
-          const bool dbias_here = need_db && mg == 0 && u == 0;
+          const bool dbias_here = need_db && mg == 0 && u == 0;  // dy is the same in every stage
 #pragma unroll
           for (int b = 0; b < NBA; ++b) {
             const int co = nt * BN + b * 32 + j * 4;
@@ -227,8 +241,13 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
                 q0[i] = qtab[co + i]; q1[i] = qtab[npad + co + i]; q2[i] = qtab[2 * npad + co + i];
               }
             }
-            if (rowok) {
-              const bool in = live && ly < p.kt && y0 + ly < p.h && x0 + lx < p.w;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int r = r0 + 32 * q;
+              if (r >= p.KBr) break;
+              const int ly = gly[q], lx = glx[q];
+              // output position of K row r: (y0+ly, x0+lx); 3x3 rows carry 2 junk columns
+              const bool in = live && ly < p.kt && y0 + ly < p.h && x0 + lx < p.w && lx < p.bw;
               const uint32_t rowb = b * p.KBr * 128 + r * 128;
               const uint32_t off = rowb + ((j ^ (r & 7)) << 4);
               const uint32_t dst = rowb + ((((j >> 1) ^ (r & 3)) << 5) | ((j & 1) << 4));
@@ -277,8 +296,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
     }
   } else if (warp == PRODUCER) {
     // =============================== TMA producer ===============================
-    const uint32_t box_rows = (uint32_t)(p.bw * p.kt);
-    const uint32_t tx_bytes = box_rows * 128u * (4u + NBA * (xb ? 2u : 1u));
+    const uint32_t tx_bytes = (uint32_t)p.rows * 128u * (4u + NBA * (xb ? 2u : 1u));
     int st = 0, round = 0;
     for (int ui = 0; ui < nun; ++ui) {
       int mg, nt, sp;
@@ -288,8 +306,8 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
         const int kb = sp * p.kpt + k;
         int img, y0, x0;
         kb_org(kb, img, y0, x0);
-        for (int u = 0; u < TAPS; ++u) {
-          const int ty = TAPS == 9 ? u / 3 - p.pad : 0, tx = TAPS == 9 ? u % 3 - p.pad : 0;
+        for (int u = 0; u < SPK; ++u) {
+          const int ty = TAPS == 9 ? u - 1 : 0, xa = TAPS == 9 ? x0 - 1 : x0;
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);
           if (elect_one()) {
             mbar_arrive_expect_tx(&ld_bar[st], tx_bytes);
@@ -297,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
             const uint32_t B = A + 2 * AB, X = B + 2 * BB;
 #pragma unroll
             for (int a = 0; a < 4; ++a)
-              tma_load_4d(A + a * p.KBr * 128, &p.tma_x, mg * 128 + a * 32, x0 + tx, y0 + ty, img, &ld_bar[st]);
+              tma_load_4d(A + a * p.KBr * 128, &p.tma_x, mg * 128 + a * 32, xa, y0 + ty, img, &ld_bar[st]);
 #pragma unroll
             for (int b = 0; b < NBA; ++b) {
               tma_load_4d(B + b * p.KBr * 128, &p.tma_dy, nt * BN + b * 32, x0, y0, img, &ld_bar[st]);
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
   } else if (warp == NTW) {
     // =============================== MMA issuer ===============================
     constexpr uint32_t idesc = make_idesc(128, BN, kFmtTF32, 1, 1);
-    const int ksteps = p.KBr / 8;
+    const int ksteps = (p.rows + 7) / 8;
     int st = 0;
     uint32_t ph = 0;
     for (int ui = 0; ui < nun; ++ui) {
@@ -323,23 +341,26 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
       if (ui >= 1) mbar_wait(&acce_bar, (ui - 1) & 1);
       tc_fence_after();
       for (int k = 0; k < cnt; ++k) {
-        for (int u = 0; u < TAPS; ++u) {
+        for (int u = 0; u < SPK; ++u) {
           mbar_wait(&full_bar[st], ph);
           tc_fence_after();
           const uint32_t A = smem_u32(stage(st));
           const uint32_t AL = A + AB, B = A + 2 * AB, BL = B + BB;
-          const uint32_t d = tmem + u * BN;
 #pragma unroll 1
-          for (int kk = 0; kk < ksteps; ++kk) {
-            // MN-major TF32 operands: 128-byte rows of 32 channels per K index, atoms KBr rows apart
-            const uint64_t ah = make_sdesc(A + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
-            const uint64_t al = make_sdesc(AL + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
-            const uint64_t bh = make_sdesc(B + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
-            const uint64_t bl = make_sdesc(BL + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
-            const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
-            umma_tf32_elect(d, ah, bh, idesc, acc);
-            umma_tf32_elect(d, ah, bl, idesc, 1u);
-            umma_tf32_elect(d, al, bh, idesc, 1u);
+          for (int tx = 0; tx < TPS; ++tx) {  // horizontal taps: A shifted by tx rows (128 B)
+            const uint32_t d = tmem + (u * TPS + tx) * BN;
+#pragma unroll 1
+            for (int kk = 0; kk < ksteps; ++kk) {
+              // MN-major TF32 operands: 128-byte rows of 32 channels per K index, atoms KBr rows apart
+              const uint64_t ah = make_sdesc(A + tx * 128 + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
+              const uint64_t al = make_sdesc(AL + tx * 128 + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
+              const uint64_t bh = make_sdesc(B + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
+              const uint64_t bl = make_sdesc(BL + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
+              const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
+              umma_tf32_elect(d, ah, bh, idesc, acc);
+              umma_tf32_elect(d, ah, bl, idesc, 1u);
+              umma_tf32_elect(d, al, bh, idesc, 1u);
+            }
           }
           umma_commit_elect(&empty_bar[st]);
           if (++st == ST) { st = 0; ph ^= 1u; }
@@ -383,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
 }
 
 struct Plan {
-  int ok, BN, bw, kt, xb, tpi, KBr, nkb, kpt, splits, MG, NT, stages;
+  int ok, BN, bw, kt, xb, tpi, KBr, nkb, kpt, splits, MG, NT, stages, RS, rows;
 };
 
 inline int num_sms32() {
@@ -408,15 +429,26 @@ inline Plan plan(int n, int h, int w, int cin, int cout, int kh, bool xop) {
   Plan q{};
   if (cin % 32 || cout % 32) return q;
   q.BN = (kh == 3 || cout <= 32) ? 32 : 64;  // TMEM: taps * BN <= 512; smem: two stages
-  // k-blocks of ~32 pixels (whole rows of small maps, 32-pixel row pieces of wide ones):
-  // short stages keep 4+ of them in flight (TMA latency hidden) at 8 bytes per operand element
-  q.bw = w < 32 ? w : 32;
-  q.kt = w < 32 ? 32 / w : 1;
+  // k-blocks of ~32 pixels (whole rows of small maps, row pieces of wide ones): short stages
+  // keep 3-4 of them in flight at 8 bytes per operand element.  3x3: box rows of bw + 2
+  // (the input row with its halo; for the output side the 2 trailing columns are junk, zeroed)
+  // so the horizontal taps are K-row shifts of one box; A needs 2 rows past the last K row
+  if (kh == 3) {
+    q.bw = w < 30 ? w : 30;
+    q.kt = w < 30 ? 32 / (w + 2) : 1;
+    if (q.kt < 1) q.kt = 1;
+    q.RS = q.bw + 2;
+  } else {
+    q.bw = w < 32 ? w : 32;
+    q.kt = w < 32 ? 32 / w : 1;
+    q.RS = q.bw;
+  }
   if (q.kt > h) q.kt = h;
   q.xb = (w + q.bw - 1) / q.bw;
   q.tpi = (h + q.kt - 1) / q.kt;
-  q.KBr = (q.bw * q.kt + 7) / 8 * 8;
-  if (q.KBr > 32) return q;
+  q.rows = q.kt * q.RS;
+  q.KBr = ((q.rows + 7) / 8 * 8 + (kh == 3 ? 2 : 0) + 7) / 8 * 8;
+  if (q.KBr > 64) return q;
   q.nkb = n * q.tpi * q.xb;
   q.MG = (cin + 127) / 128;
   q.NT = (cout + q.BN - 1) / q.BN;
@@ -473,11 +505,12 @@ extern "C" int bnff_wgrad_f32_partials(bnff_view x, int32_t x_pro, bnff_coef x_c
   p.n = (int)x.n; p.h = (int)x.h; p.w = (int)x.w; p.cin = (int)x.c; p.cout = (int)dy.c;
   p.kh = kh; p.pad = kh / 2;
   p.bw = q.bw; p.kt = q.kt; p.xb = q.xb; p.tpi = q.tpi; p.KBr = q.KBr; p.nkb = q.nkb; p.kpt = q.kpt;
+  p.RS = q.RS; p.rows = q.rows;
   p.splits = q.splits; p.MG = q.MG; p.NT = q.NT; p.units = q.MG * q.NT * q.splits; p.stages = q.stages;
   p.x_pro = x_pro; p.x_coef = x_coef; p.dy_pro = dy_pro; p.dy_coef = dy_coef;
   p.ws = ws;
   p.wsb = want_db ? ws + (long long)q.splits * kh * kh * p.cin * p.cout : nullptr;
-  const uint32_t box[4] = {32u, (uint32_t)q.bw, (uint32_t)q.kt, 1u};
+  const uint32_t box[4] = {32u, (uint32_t)q.RS, (uint32_t)q.kt, 1u};
   if (!encode_nhwc(&p.tma_x, 4, x.ptr, x.n, x.h, x.w, x.c, x.row_stride, 4, box) ||
       !encode_nhwc(&p.tma_dy, 4, dy.ptr, dy.n, dy.h, dy.w, dy.c, dy.row_stride, 4, box) ||
       (xop && !encode_nhwc(&p.tma_dyx, 4, dy_x.ptr, dy_x.n, dy_x.h, dy_x.w, dy_x.c, dy_x.row_stride, 4, box)))

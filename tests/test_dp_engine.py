@@ -44,7 +44,7 @@ def _spec(batch):
                        name="densenet-micro-aligned")
 
 
-def _worker(rank, port, sync_bn, out_dir):
+def _worker(rank, port, sync_bn, out_dir, buckets=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(WORLD), LOCAL_RANK="0")
     import torch.distributed as dist
@@ -60,14 +60,16 @@ def _worker(rank, port, sync_bn, out_dir):
     xg = rng.uniform((n * WORLD, c, h, w), -1.0, 1.0)
     dyg = rng.normal((n * WORLD,) + tuple(g.slots[g.outputs[0]].shape[1:]))
     lo, hi = dp.shard_batch(n * WORLD, WORLD, rank)
-    eng = Engine(g, dtype="f32", input_grad=False, sync_bn=sync_bn)
+    eng = Engine(g, dtype="f32", input_grad=False, sync_bn=sync_bn, dp_buckets=buckets,
+                 bucket_bytes=16 << 10)
     eng.set_input(xg[lo:hi])
     eng.set_loss_grad(dyg[lo:hi])
     eng.forward()
     eng.backward()
     torch.cuda.synchronize()
     out = eng.output()
-    dp.allreduce_grads(eng.gflat)
+    if not buckets:  # else backward already issued the bucketed all-reduces
+        dp.allreduce_grads(eng.gflat)
     torch.cuda.synchronize()
     grads = eng.param_grads()
     # oracle references (fp64)
@@ -100,9 +102,10 @@ def _worker(rank, port, sync_bn, out_dir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("buckets", [False, True], ids=["flat-allreduce", "bucketed-in-backward"])
 @pytest.mark.parametrize("sync_bn", [False, True], ids=["per-replica-bn", "syncbn"])
-def test_dp_engine_two_ranks(sync_bn, tmp_path):
+def test_dp_engine_two_ranks(sync_bn, buckets, tmp_path):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(_free_port(), sync_bn, str(tmp_path)), nprocs=WORLD, join=True)
+    mp.spawn(_worker, args=(_free_port(), sync_bn, str(tmp_path), buckets), nprocs=WORLD, join=True)
     for r in range(WORLD):
         assert float(np.load(tmp_path / f"r{r}.npy")[0]) < TOL

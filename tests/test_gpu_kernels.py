@@ -19,7 +19,7 @@ from paper_1807_01702_b200.errors import StateError  # noqa: E402
 from paper_1807_01702_b200.params import BNParams, ConvParams  # noqa: E402
 
 DT = {"f32": torch.float32, "bf16": torch.bfloat16}
-TOL = {"f32": 1e-4, "bf16": 3e-2}
+TOL = {"f32": 1e-4, "bf16": 5e-3}
 
 
 def to_dev(a, dt):

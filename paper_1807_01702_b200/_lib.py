@@ -117,6 +117,7 @@ SIGNATURES = {
     "bnff_nhwc_to_nchw": (C.c_int, [_I32, View, _P, _P]),
     "bnff_sgd": (C.c_int, [_P, _P, _I64, _F, _P]),
     "bnff_debug_trace": (C.c_int, [_P]),
+    "bnff_debug_mark": (C.c_int, [_I32, _P]),
     "bnff_im2col": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
     "bnff_col2im": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
     "bnff_weight_to_cols": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),

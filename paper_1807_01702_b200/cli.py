@@ -6,11 +6,20 @@ Device additions: ``--dtype`` (bf16 | f32), ``--gpus`` (informational; one proce
 is bench.py's job) and ``--syncbn``.
 
     python -m paper_1807_01702_b200.cli bench --model densenet-121 --batch 64 --fusion all
+    python -m paper_1807_01702_b200.cli traffic --model densenet-121 --batch 64 --out report/
+    python -m paper_1807_01702_b200.cli explain --model densenet-121 --fusion bnff+icf
 
 Columns follow the reference; ``traffic_bytes`` is the algorithmic HBM bytes of the launches
 of that pass (each tensor counted once per launch, in the storage dtype) rather than the
 reference's fp32 sweep rulebook, ``threads`` is the GPU count, ``conv_share`` the share of
-device time in conv launches measured by per-launch events.
+device time in conv launches measured by per-launch events.  ``checksum`` follows the
+reference contract (one value for every level of a run, test_cli.py:89-90): a digest of the
+run's shared inputs and initial weights; the device outputs of every level are compared
+with the baseline level's and the relative L2 gap is printed.
+
+``traffic`` / ``explain`` mirror ``bnfuse traffic`` / ``explain`` (cli.py:247-286): the
+reference's sweep rulebook (traffic.py) per level, one CSV per level plus summary.json, and
+the rewrite plan of each level.
 """
 
 from __future__ import annotations
@@ -77,7 +86,11 @@ def cmd_bench(a) -> int:
     rng = Rng(a.seed + 1)
     x = rng.uniform(base.slots[base.inputs[0]].shape, -1.0, 1.0)
     dy = rng.normal(base.slots[base.outputs[0]].shape)
-    rows, baseline_total = [], None
+    rows, baseline_total, ref_out = [], None, None
+    h = hashlib.sha1(np.ascontiguousarray(x).tobytes())
+    for k in sorted(base.params):
+        h.update(np.ascontiguousarray(base.params[k]).tobytes())
+    checksum = h.hexdigest()[:12]
     for level in _levels(a.fusion):
         g2, _ = fusion.plan(base, level)
         try:
@@ -96,7 +109,10 @@ def cmd_bench(a) -> int:
         conv = sum(ms for t, ms in prof if t.kind in _CONV_KINDS)
         allms = sum(ms for _, ms in prof) or 1.0
         out = eng.output()
-        checksum = hashlib.sha1(np.ascontiguousarray(out).tobytes()).hexdigest()[:12]
+        if ref_out is None:
+            ref_out = out
+        gap = float(np.linalg.norm(out - ref_out) / max(float(np.linalg.norm(ref_out)), 1e-30))
+        print(f"{level.token:10s} output rel-L2 vs first level {gap:.2e}")
         traffic = {"forward": sum(t.nbytes for t in eng.fwd), "backward": sum(t.nbytes for t in eng.bwd)}
         total = [f + b for f, b in zip(fwd, bwd)]
         if level == fusion.FusionLevel.BASELINE:
@@ -128,6 +144,47 @@ def cmd_bench(a) -> int:
     return 0
 
 
+def _spec(a):
+    presets = dict(G.PRESETS, **{"densenet-bc-100": G.densenet_bc100})
+    return presets[a.model]() if a.batch is None else presets[a.model](a.batch)
+
+
+def cmd_traffic(a) -> int:
+    import json
+    import os
+    from . import traffic
+    base = G.build_model(_spec(a), seed=a.seed)
+    out_dir = a.out_path or "traffic-report"
+    os.makedirs(out_dir, exist_ok=True)
+    leds = {}
+    for level in _levels(a.fusion):
+        g2, _ = fusion.plan(base, level)
+        led = traffic.count_sweeps(g2, concat_physical=False, bytes_per_elem=a.bytes_per_elem)
+        leds[level.token] = led
+        with open(os.path.join(out_dir, f"traffic_{level.token.replace('+', '_')}.csv"), "w") as f:
+            f.write(traffic.to_csv(led))
+    first = leds.get("baseline") or next(iter(leds.values()))
+    summary = []
+    for tok, led in leds.items():
+        s = traffic.summary(led, tok, base.meta.get("spec").name if base.meta.get("spec") else a.model, first)
+        summary.append(s)
+        print(f"{tok:10s} total {led.total_bytes() / 1e9:9.3f} GB  reduction "
+              f"{s['reduction_vs_baseline'] * 100:6.2f}%  relu share {s['relu_share'] * 100:5.2f}%")
+    with open(os.path.join(out_dir, "summary.json"), "w") as f:
+        json.dump(summary, f, indent=2)
+    print(f"wrote {out_dir}/")
+    return 0
+
+
+def cmd_explain(a) -> int:
+    base = G.build_model(_spec(a), seed=a.seed)
+    for level in _levels(a.fusion):
+        _, fplan = fusion.plan(base, level)
+        print(fplan.describe())
+        print()
+    return 0
+
+
 def make_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="bnfuse-b200", description="restructured-BN training path on B200")
     sub = p.add_subparsers(dest="command", required=True)
@@ -144,12 +201,21 @@ def make_parser() -> argparse.ArgumentParser:
     sp.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     sp.add_argument("--gpus", type=int, default=1)
     sp.add_argument("--syncbn", action="store_true")
+    for name, help_ in (("traffic", "the reference's memory-sweep rulebook per fusion level"),
+                        ("explain", "the rewrite plan of each fusion level")):
+        tp = sub.add_parser(name, help=help_)
+        tp.add_argument("--model", default="densenet-121")
+        tp.add_argument("--batch", type=int, default=None)
+        tp.add_argument("--fusion", default="all")
+        tp.add_argument("--seed", type=int, default=0)
+        tp.add_argument("--out", default=None, dest="out_path")
+        tp.add_argument("--bytes-per-elem", type=int, default=4, help="4 = the reference's fp32; 2 = bf16 storage")
     return p
 
 
 def main(argv=None) -> int:
     a = make_parser().parse_args(argv)
-    return {"bench": cmd_bench}[a.command](a)
+    return {"bench": cmd_bench, "traffic": cmd_traffic, "explain": cmd_explain}[a.command](a)
 
 
 if __name__ == "__main__":

@@ -1508,3 +1508,13 @@ extern "C" int bnff_sums_to_f32(int32_t c, const double* a, const double* b, flo
   launch(sums_to_f32_kernel, dim3((c + 127) / 128), dim3(128), 0, (cudaStream_t)stream, c, a, b, a32, b32);
   return check_launch("sums_to_f32");
 }
+
+// ncu node ledger (tools/ncu_node_ledger.py): an empty kernel launched before every engine
+// launch so a profiler's launch list can be cut into per-launch (per graph node) groups
+namespace bnff {
+__global__ void mark_kernel(int) {}
+}  // namespace bnff
+extern "C" int bnff_debug_mark(int32_t id, void* stream) {
+  bnff::mark_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(id);
+  return check_launch("mark");
+}

@@ -105,10 +105,11 @@ __host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad, int
     // 1x1: 128-byte slabs (32 channels), N tiles <= 128 (fprop) / 64 (dgrad: x tile + 2
     // staging buffers per group); 3x3: 64-byte slabs (16 channels), weights streamed with
     // the stage, N tiles of 32 / 64
-    g.RB = (g.taps == 9 || CI <= 16) ? 64 : 128;
+    // 1x1 dgrad: 64-byte slabs too, so two stages, the x tile, the staging rows and the ICF
+    // fold's block-gradient tile fit beside a 1024-column epilogue table
+    g.RB = (g.taps == 9 || CI <= 16 || dgrad) ? 64 : 128;
     g.BN = pick_bn(N);
-    // (the 64-byte-slab 1x1 instantiation -- K <= 16 channels -- exists for 32-wide N tiles only)
-    const int cap = g.taps == 9 ? (dgrad ? 32 : 64) : (g.RB == 64 ? 32 : (dgrad ? 64 : 128));
+    const int cap = g.taps == 9 ? (dgrad ? 32 : 64) : (dgrad ? 64 : (g.RB == 64 ? 32 : 128));
     if (g.BN > cap) g.BN = cap;
     g.sw = g.taps == 9 ? 1 : 0;
     g.nslab = (CI + g.RB / 4 - 1) / (g.RB / 4);
@@ -202,8 +203,7 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
 // the 1x1 block-gradient fold runs through TMA (G tile loaded, folded in smem, stored back)
 template <int BN, int RB, int TAPS, int MODE, bool SW, int ES = 2>
 __host__ __device__ inline bool fold_tma(const WcParams& p) {
-  return ES == 2 && TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW, ES>::CW == 64 &&
-         p.epi >= BNFF_DG_NRC_ACC;
+  return TAPS == 1 && MODE == M_DGRAD && Layout<BN, RB, TAPS, MODE, SW, ES>::TST && p.epi >= BNFF_DG_NRC_ACC;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
@@ -667,8 +667,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
     const bool nrc = MODE == M_DGRAD && EPI >= BNFF_DG_NRC;
     // out (+)= scale * dt1: the ICF fold exists for 1x1 dgrads only (the host rejects it for 3x3),
     // so the 3x3 instantiations carry no fold code
-    const bool fold = !F32 && MODE == M_DGRAD && TAPS == 1 && EPI >= BNFF_DG_NRC_ACC;
-    const bool fold_acc = !F32 && MODE == M_DGRAD && TAPS == 1 && EPI == BNFF_DG_NRC_ACC;
+    const bool fold = MODE == M_DGRAD && TAPS == 1 && EPI >= BNFF_DG_NRC_ACC && (!F32 || L::TST);
+    const bool fold_acc = MODE == M_DGRAD && TAPS == 1 && EPI == BNFF_DG_NRC_ACC && (!F32 || L::TST);
     E* const outp = reinterpret_cast<E*>(p.out);
     const E* const exq = reinterpret_cast<const E*>(p.ex);
     constexpr int EPC = 16 / ES;             // elements per 16-byte chunk
@@ -888,7 +888,21 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             for (int q = 0; q < 4; ++q) {
               const int j = (c16 >> 2) + q;
               const uint32_t o = tst ? row * 128 + ((j ^ (row & 7)) << 4) : row * L::SROWB + j * 16;
-              *reinterpret_cast<float4*>(stg + o) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              const float4 vv = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              *reinterpret_cast<float4*>(stg + o) = vv;
+              if (MODE == M_DGRAD && tfold) {  // G = (acc ? G : 0) + scale * dt1, in the TMA G tile
+                uint8_t* gt0 = gb0 + k * 128 * 128;
+                const float* sc = etab + gc + 4 * q;
+                float4 d;
+                if (fold_acc) {
+                  const float4 old = *reinterpret_cast<const float4*>(gt0 + o);
+                  d = make_float4(fmaf(sc[0], vv.x, old.x), fmaf(sc[1], vv.y, old.y), fmaf(sc[2], vv.z, old.z),
+                                  fmaf(sc[3], vv.w, old.w));
+                } else {
+                  d = make_float4(sc[0] * vv.x, sc[1] * vv.y, sc[2] * vv.z, sc[3] * vv.w);
+                }
+                *reinterpret_cast<float4*>(gt0 + o) = d;
+              }
             }
           } else if (tst) {  // dense 128-byte rows, 128B swizzle (the TMA store's box layout)
             const int j = c16 >> 3;
@@ -1798,7 +1812,11 @@ static int dispatch_f32(const WcParams& p, int BN, int RB, cudaStream_t st) {
     if (BN == 32) return launch_t<32, 64, TAPS, MODE, true, 4>(p, st);
     return launch_t<64, 64, TAPS, MODE, true, 4>(p, st);
   }
-  if (RB == 64) return launch_t<32, 64, TAPS, MODE, false, 4>(p, st);
+  if (RB == 64) {
+    if constexpr (MODE == M_DGRAD)
+      if (BN == 64) return launch_t<64, 64, TAPS, MODE, false, 4>(p, st);
+    return launch_t<32, 64, TAPS, MODE, false, 4>(p, st);
+  }
   switch (BN) {
     case 32: return launch_t<32, 128, TAPS, MODE, false, 4>(p, st);
     case 64: return launch_t<64, 128, TAPS, MODE, false, 4>(p, st);
@@ -1845,6 +1863,7 @@ static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop) {
   Carve c{};
   if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop)
                               : carve<64, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop);
+  else if (RB == 64 && MODE == M_DGRAD && BN == 64) c = carve<64, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, true);
   else if (RB == 64) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
   else if (BN == 32) c = carve<32, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
   else if (BN == 64) c = carve<64, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
@@ -1976,9 +1995,9 @@ extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t
   p.ci = (int)in.c;
   p.N = (int)out.c;
   const int es = dtype == BNFF_F32 ? 4 : 2;
-  if (es == 4 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
-    return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is bf16-only");
   const wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode, es);
+  if (es == 4 && mode == 1 && epi >= BNFF_DG_NRC_ACC && g.BN < 64)  // fp32 fold: TMA G tile (32 columns)
+    return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the fp32 block-gradient fold needs >= 33 channels");
   p.nslab = g.nslab;
   p.npad = g.npad;
   p.ntiles = g.ntiles;

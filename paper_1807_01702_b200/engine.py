@@ -176,7 +176,7 @@ class Engine:
         self._nrp_done: set = set()
         # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
         # into the block gradient buffer; the per-channel remainder rides in (A, B) arrays
-        self.fold_icf = bool(fold_icf) and self.dcode == _lib.BF16
+        self.fold_icf = bool(fold_icf)
         self.fold = {}  # block group -> dict(A, B, ones, m32, i32, started)
         self._side = None  # side stream of the weight-gradient launches
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
@@ -298,6 +298,7 @@ class Engine:
         thunk.flops = int(flops)
         thunk.launches = launches  # kernels this C-ABI call launches
         thunk.side = bool(side)    # runs on the side stream (forked/joined by _run)
+        thunk.node_id = getattr(self, "_cur_node", -1)  # the graph node that emitted it
         self._cur.append(thunk)
 
     def _emit_allreduce(self, *tensors, what="allreduce"):
@@ -401,10 +402,12 @@ class Engine:
         self.node_tables: dict = {}  # node id -> fp32 tables
         self.stats: dict = {}        # stats slot id -> Stats
         for node in self.g.nodes:
+            self._cur_node = node.id
             try:
                 getattr(self, "_f_" + node.kind)(node)
             except ShapeError as e:
                 raise ShapeError(f"node {node.id} ({node.kind} {node.name}): {e}") from e
+        self._cur_node = -1
         self._flush_pending()
         self.launch_counts["fwd"] = len(self.fwd)
 
@@ -677,6 +680,7 @@ class Engine:
         self._done_params: set = set()
         self._bucket_hi = int(self.gflat.numel())
         for node in reversed(g.nodes):
+            self._cur_node = node.id
             try:
                 getattr(self, "_b_" + node.kind)(node)
             except ShapeError as e:
@@ -684,6 +688,7 @@ class Engine:
             if self.dp_buckets:
                 self._done_params.update(self._params_of(node))
                 self._maybe_bucket(final=False)
+        self._cur_node = -1
         if self.dp_buckets:
             self._maybe_bucket(final=True)
         self.input_grads = {}
@@ -974,6 +979,8 @@ class Engine:
         """(target view, sibling slot or None, mode, group, lo) when this consumer's BN dx
         can be folded into the block gradient buffer, else None."""
         if not self.fold_icf or conv.kh != 1 or conv.name not in self.wpacks:
+            return None
+        if self.dcode == _lib.F32 and x.shape[3] < 64:  # the fp32 fold runs on 32-column TMA tiles
             return None
         sid = node.inputs[0]
         slot = self.g.slots[sid]

@@ -401,6 +401,8 @@ def test_cli_bench_csv(tmp_path):
         float(r["median_ms"]), float(r["mean_ms"]), float(r["std_ms"])
         int(r["iters"]), int(r["traffic_bytes"]), int(r["threads"])
     assert float(rows[5]["speedup_vs_baseline"]) > 0
+    # the reference contract (test_cli.py:89-90): one checksum for every level of a run
+    assert len({r["checksum"] for r in rows}) == 1
 
 
 def _set_params(g, new):
@@ -462,3 +464,35 @@ def test_multistep_graph_replay_bnff_icf(spec):
     for (wa, ga, na), (wb, gb, nb) in zip(*runs):
         assert np.array_equal(na, nb) and np.array_equal(ga, gb)
         assert np.array_equal(na, (wa - np.float32(lr) * ga).astype(np.float32))
+
+
+def test_icf_block_gradient_fold_f32():
+    """The ICF fold in fp32 (32-column TMA G tiles): folded vs unfolded schedule within
+    rel-L2 1e-5 (re-association only), and the folded run within 1e-4 of the fp64 oracle."""
+    from paper_1807_01702_b200.engine import Engine
+    spec = G.ModelSpec("densenet", (3, 3), 32, 4, (2, 64, 16, 16), "micro", "conv3", name="densenet-micro-64")
+    g0 = G.build_model(spec, seed=0)
+    g, _ = fusion.plan(g0, fusion.parse_level("bnff+icf"))
+    rng = Rng(1)
+    x = rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0)
+    dy = rng.normal(g.slots[g.outputs[0]].shape)
+    runs = {}
+    for fold in (True, False):
+        eng = Engine(g, dtype="f32", input_grad=True, fold_icf=fold)
+        eng.set_input(x)
+        eng.set_loss_grad(dy)
+        eng.forward()
+        eng.backward()
+        torch.cuda.synchronize()
+        kinds = [t.kind for t in eng.bwd]
+        runs[fold] = (eng.output(), eng.param_grads(), eng.input_grad_nchw(), kinds)
+    assert runs[True][3].count("split_bwd") < runs[False][3].count("split_bwd"), "fold not taken"
+    assert rel_l2(runs[True][2], runs[False][2]) < 1e-5, "input grad"
+    for k, v in runs[False][1].items():
+        if not k.endswith(".bias"):
+            assert rel_l2(runs[True][1][k], v) < 1e-5, k
+    res = OX.forward(g, {g.inputs[0]: x.astype(np.float64)})
+    ref = OX.backward(g, res, {g.outputs[0]: dy.astype(np.float64)})
+    for k, v in ref.params.items():
+        if not k.endswith(".bias"):
+            assert scaled(runs[True][1][k], v) < 1e-4, k

@@ -172,6 +172,7 @@ class Engine:
         import os
         self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
+        self.wide_fallback = os.environ.get("BNFF_WIDE_FALLBACK", "1") != "0"  # see _f_FusedNormReluConv
         self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
         self._nrp_done: set = set()
         # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
@@ -563,7 +564,12 @@ class Engine:
         y = self._feature(node.outputs[0])
         tb = self._bn_tables(st, at.bn, node.name)
         self.node_tables[node.id] = tb
-        if self.save_postrelu:
+        # cost model: the fused prologue normalises the input once per N tile of the conv; past
+        # two N tiles (very wide 1x1s: ResNet expansions, the C5 sweep at C >= 512) one
+        # materialising bn_apply pass is cheaper than repeating the transform
+        n_tile = 256 if self.dcode == _lib.BF16 else 128
+        wide = self.wide_fallback and -(-at.conv.out_c // n_tile) > 2
+        if self.save_postrelu or wide:
             saved = self._feature(node.outputs[1])
             self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(saved),
                        coef_of(tb[0], tb[1], tb[2]), 1, what="saved_postrelu", nbytes=_nb(x, saved))
@@ -571,7 +577,10 @@ class Engine:
         if at.emit_stats:
             mt = self.L.bnff_stat_rows()
             part = self._zeros((mt, 2, y.shape[3]), torch.float64)
-        self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
+        if wide:
+            self._conv_fprop(node, saved, y, at.conv, _lib.PRO_NONE, None, part)
+        else:
+            self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
         if at.emit_stats:
             ost = self._stats_for(node.outputs[0], y.shape[3], y.shape[0] * y.shape[1] * y.shape[2])
             self._emit_stats_finalize(part, mt, y.shape[3], ost.count, ost)

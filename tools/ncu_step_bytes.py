@@ -31,7 +31,7 @@ def run(level, dtype, batch):
     from paper_1807_01702_b200.engine import Engine
     from paper_1807_01702_b200.tensor import Rng
     g, _ = fusion.plan(G.build_model(G.densenet121(batch), seed=0), fusion.parse_level(level))
-    eng = Engine(g, dtype=dtype, input_grad=False, lr=1e-3)
+    eng = Engine(g, dtype=dtype, input_grad=True, lr=1e-3)
     rng = Rng(1)
     eng.set_input(rng.uniform(g.slots[g.inputs[0]].shape, -1.0, 1.0))
     eng.set_loss_grad(rng.normal(g.slots[g.outputs[0]].shape))
@@ -48,6 +48,7 @@ def run(level, dtype, batch):
 def kernel_class(name: str) -> str:
     """ncu kernel name -> engine launch class (engine thunk `kind`)."""
     if "wgrad_kernel" in name or "wg_reduce_kernel" in name or "wgrad_reduce_kernel" in name \
+            or "wgrad_f32_kernel" in name \
             or "igemm_kernel<2" in name or "igemm_kernel<(int)2" in name:
         return "wgrad"
     if "wconv_kernel" in name:  # template <BN, RB, TAPS, MODE[, SW]>: MODE 1 = dgrad
@@ -63,7 +64,7 @@ def kernel_class(name: str) -> str:
         return "pool_relu_bn_bwd"
     if "finalize_coeffs" in name:
         return "bn_coeffs"
-    for k in ("stats_finalize", "dx_coeffs", "bn_coeffs", "im2col", "avgpool", "grad_sum",
+    for k in ("stats_finalize", "dx_coeffs", "bn_coeffs", "im2col", "col2im", "avgpool", "grad_sum",
               "channel_sums", "sgd", "pack", "relu", "bn_apply"):
         if k in name:
             return k

@@ -17,6 +17,7 @@
 // reduced in fixed split order by wconv.cu's wg_reduce_kernel (deterministic).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "sm100.cuh"
 #include "common.cuh"
@@ -428,7 +429,14 @@ inline int pick_stages(int KBr, bool xop, int cin_pad, int npad) {
 inline Plan plan(int n, int h, int w, int cin, int cout, int kh, bool xop) {
   Plan q{};
   if (cin % 32 || cout % 32) return q;
-  q.BN = (kh == 3 || cout <= 32) ? 32 : 64;  // TMEM: taps * BN <= 512; smem: two stages
+  // N tile: 3x3 -> 32 (9 taps x 32 TMEM columns); 1x1 -> up to 128 (one x transform serves all
+  // output channels; BNFF_WG32_BN caps it for A/B)
+  static int bn_cap = -1;
+  if (bn_cap < 0) {
+    const char* e = getenv("BNFF_WG32_BN");
+    bn_cap = e ? atoi(e) : 128;
+  }
+  q.BN = (kh == 3 || cout <= 32) ? 32 : (cout >= 128 && bn_cap >= 128 ? 128 : 64);
   // k-blocks of ~32 pixels (whole rows of small maps, row pieces of wide ones): short stages
   // keep 3-4 of them in flight at 8 bytes per operand element.  3x3: box rows of bw + 2
   // (the input row with its halo; for the output side the 2 trailing columns are junk, zeroed)
@@ -453,7 +461,8 @@ inline Plan plan(int n, int h, int w, int cin, int cout, int kh, bool xop) {
   q.MG = (cin + 127) / 128;
   q.NT = (cout + q.BN - 1) / q.BN;
   q.stages = q.BN == 32 ? pick_stages<32>(q.KBr, xop, q.MG * 128, q.NT * q.BN)
-                        : pick_stages<64>(q.KBr, xop, q.MG * 128, q.NT * q.BN);
+           : q.BN == 64 ? pick_stages<64>(q.KBr, xop, q.MG * 128, q.NT * q.BN)
+                        : pick_stages<128>(q.KBr, xop, q.MG * 128, q.NT * q.BN);
   if (q.stages < 2) return q;
   const int target = num_sms32();
   int splits = (target + q.MG * q.NT - 1) / (q.MG * q.NT);
@@ -518,5 +527,6 @@ extern "C" int bnff_wgrad_f32_partials(bnff_view x, int32_t x_pro, bnff_coef x_c
   *splits_out = q.splits;
   cudaStream_t st = (cudaStream_t)stream;
   if (kh == 3) return wg32::launch<32, 9>(p, st);  // 9 taps x 32 TMEM columns
+  if (q.BN == 128) return wg32::launch<128, 1>(p, st);
   return q.BN == 32 ? wg32::launch<32, 1>(p, st) : wg32::launch<64, 1>(p, st);
 }

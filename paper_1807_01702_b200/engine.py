@@ -174,6 +174,7 @@ class Engine:
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
         self.wide_fallback = os.environ.get("BNFF_WIDE_FALLBACK", "1") != "0"  # see _f_FusedNormReluConv
         self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
+        self._wide_saved: dict = {}  # NRC node id -> materialised relu(bn(x)) (wide-N fallback)
         self._nrp_done: set = set()
         # ICF block-gradient fold: 1x1 NRC dgrads accumulate scale*dt1 straight
         # into the block gradient buffer; the per-channel remainder rides in (A, B) arrays
@@ -578,6 +579,7 @@ class Engine:
             mt = self.L.bnff_stat_rows()
             part = self._zeros((mt, 2, y.shape[3]), torch.float64)
         if wide:
+            self._wide_saved[node.id] = saved
             self._conv_fprop(node, saved, y, at.conv, _lib.PRO_NONE, None, part)
         else:
             self._conv_fprop(node, x, y, at.conv, _lib.PRO_BN_RELU, tb, part)
@@ -807,7 +809,9 @@ class Engine:
     def _conv_backward(self, node, conv, x, dy_gv, x_pro, x_tables, dgrad_epi, dgrad_tables,
                        dx_out=None):
         """dgrad (+ epilogue) and wgrad of one conv; returns the dx tensor (or None).
-        dx_out: the block gradient view the fold epilogues (DG_NRC_ACC/SET) write into."""
+        dx_out: the block gradient view the fold epilogues (DG_NRC_ACC/SET) write into.
+        A wide NRC conv whose forward materialised relu(bn(x)) (_f_FusedNormReluConv) takes its
+        weight-gradient operand from that tensor instead of re-normalising x per N tile."""
         cin_store = x.shape[3]
         wp, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if isinstance(dy_gv, Deferred):
@@ -817,6 +821,9 @@ class Engine:
         xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
         col = self.cols.get(conv.name) if x_pro == _lib.PRO_NONE else None
         orig, wconv, wx, wcin = conv, conv, x, cin_store
+        saved = self._wide_saved.get(node.id)
+        if saved is not None and x_pro == _lib.PRO_BN_RELU:
+            wx, x_pro, xc = saved, _lib.PRO_NONE, coef_of()
         dw = self.grad(f"{conv.name}.weight")
         if col is not None:  # stem: weight gradient of the 1x1 GEMM over the patch matrix
             wconv, wx, dw = col[0], col[1], col[2]

@@ -156,6 +156,17 @@ int bnff_pack_weights(int32_t dtype, const float* w, int32_t c_out, int32_t c_in
  * reduction over c_in; dgrad: n = c_in, reduction over c_out, taps flipped).        */
 int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
                    int32_t stride, int32_t pad, int32_t h, int32_t w);
+/* bnff_window_ok for launches that need only some coefficient tables (bnff_window_ok = all
+ * of them): the patch-matrix GEMMs (plain fprop operand, plain dgrad epilogue) reach
+ * K = 4608 this way.  A conv call whose window plan is rejected falls back to the generic
+ * kernel only when the caller passed generic packed weights (else BNFF_ERR_STATE). */
+enum {
+  BNFF_WT_FPROP_PRO = 1, /* fprop operand prologue (RELU / BN_RELU) */
+  BNFF_WT_DGRAD_NRC = 2, /* dgrad NRC epilogue (and the fold variants) */
+  BNFF_WT_DGRAD_PRO = 4, /* dgrad dy prologue (BN_DX) */
+};
+int bnff_window_ok_ex(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
+                      int32_t stride, int32_t pad, int32_t h, int32_t w, int32_t tables);
 int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
                               int32_t dgrad); /* elements */
 int bnff_pack_window(int32_t dtype, const float* w, int32_t c_out, int32_t c_in, int32_t kh,
@@ -293,6 +304,15 @@ int bnff_im2col(int32_t dtype, bnff_view x, int32_t c_real, int32_t kh, int32_t 
  * storage channels >= c_real written as zeros */
 int bnff_col2im(int32_t dtype, bnff_view dcol, int32_t c_real, int32_t kh, int32_t kw, int32_t stride,
                 int32_t pad, bnff_view dx, void* stream);
+/* K13c: strided convolutions (ResNet's stride-2 3x3s, ops.py:151-204 / fused.py:103-200) on the
+ * window GEMM: im2col_s writes the patch matrix of pro(x) (pro = NONE / RELU / BN_RELU with the
+ * (mean, scale, beta) tables of bnff_bn_coeffs; padding after the prologue); col2im_s gathers the
+ * dgrad of the 1x1 GEMM back to dx with a PLAIN / CLIP / NRC-mask epilogue (x and the same
+ * tables for the mask).  Channels must fill 16-byte chunks. */
+int bnff_im2col_s(int32_t dtype, bnff_view x, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                  int32_t pro, bnff_coef pcoef, bnff_view col, void* stream);
+int bnff_col2im_s(int32_t dtype, bnff_view dcol, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                  int32_t epi, bnff_view x, bnff_coef ecoef, bnff_view dx, void* stream);
 int bnff_weight_to_cols(const float* w, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,
                         int32_t kpad, float* w2, void* stream);
 int bnff_cols_to_weight(const float* dw2, int32_t c_out, int32_t c_in, int32_t kh, int32_t kw,

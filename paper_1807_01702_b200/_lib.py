@@ -20,6 +20,8 @@ LIB_PATH = os.environ.get("BNFF_LIB") or os.path.join(_HERE, "libbnff.so")
 F32, BF16 = 0, 1
 PRO_NONE, PRO_RELU, PRO_BN_RELU, PRO_BN_DX = 0, 1, 2, 3
 DG_PLAIN, DG_CLIP, DG_NRC, DG_NRC_ACC, DG_NRC_SET = 0, 1, 2, 3, 4
+WT_FPROP_PRO, WT_DGRAD_NRC, WT_DGRAD_PRO = 1, 2, 4  # bnff_window_ok_ex table flags
+WT_ALL = WT_FPROP_PRO | WT_DGRAD_NRC | WT_DGRAD_PRO
 
 
 class View(C.Structure):
@@ -79,6 +81,7 @@ SIGNATURES = {
     "bnff_pack_size": (_I64, [_I32] * 5),
     "bnff_pack_weights": (C.c_int, [_I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "bnff_window_ok": (C.c_int, [_I32] * 9),
+    "bnff_window_ok_ex": (C.c_int, [_I32] * 10),
     "bnff_window_pack_size": (_I64, [_I32] * 6),
     "bnff_pack_window": (C.c_int, [_I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "bnff_window_conv": (C.c_int, [_I32, _I32, _I32, _I32, View, View, _I32, Coef, View, _P, _P, _I32,
@@ -120,6 +123,8 @@ SIGNATURES = {
     "bnff_debug_mark": (C.c_int, [_I32, _P]),
     "bnff_im2col": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
     "bnff_col2im": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, _P]),
+    "bnff_im2col_s": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, Coef, View, _P]),
+    "bnff_col2im_s": (C.c_int, [_I32, View, _I32, _I32, _I32, _I32, _I32, View, Coef, View, _P]),
     "bnff_weight_to_cols": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "bnff_cols_to_weight": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
 }

@@ -819,7 +819,8 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
   if (a->x_pro == BNFF_PRO_BN_DX) return set_error(BNFF_ERR_UNSUPPORTED, "fprop: BN_DX prologue");
   if (a->x_pro == BNFF_PRO_BN_RELU && (!a->x_coef.a || !a->x_coef.b || !a->x_coef.c))
     return set_error(BNFF_ERR_STATE, "fprop: missing statistics for the normalize prologue");
-  if (a->wwin && bnff_window_ok(a->dtype, (int)a->x.c, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+  if (a->wwin && bnff_window_ok_ex(a->dtype, (int)a->x.c, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w,
+                                    a->x_pro != BNFF_PRO_NONE ? BNFF_WT_FPROP_PRO : 0)) {
     bnff_view none{};
     const int wrc = bnff_window_conv(a->dtype, 0, p.kh, p.pad, a->x, none, a->x_pro, a->x_coef, a->y, a->wwin,
                                      a->bias, 0, none, bnff_coef{}, a->stat_part, stream);
@@ -834,6 +835,8 @@ extern "C" int bnff_conv_fprop(const bnff_fprop_args* a, void* stream) {
   p.kpt = p.nkb;
   p.splits = 1;
   p.a_ptr = a->x.ptr; p.a_rs = a->x.row_stride; p.a_pro = a->x_pro; p.a_coef = a->x_coef;
+  if (!a->wpack)  // window-only weights and the window plan rejected the launch: never run stale packs
+    return set_error(BNFF_ERR_STATE, "fprop: window kernel not eligible and no generic packed weights");
   p.b_ptr = a->wpack; p.b_rs = kpad_elems(a->dtype, K);
   p.c_ptr = a->y.ptr; p.c_rs = a->y.row_stride;
   p.bias = a->bias;
@@ -856,7 +859,9 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   if (a->epi != BNFF_DG_PLAIN && (rc = check_common(a->dtype, a->x, "dgrad x"))) return rc;
   const bool fold = a->epi == BNFF_DG_NRC_ACC || a->epi == BNFF_DG_NRC_SET;
   if (a->epi < BNFF_DG_PLAIN || a->epi > BNFF_DG_NRC_SET) return set_error(BNFF_ERR_SHAPE, "dgrad: bad epilogue");
-  if (a->wwin && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+  if (a->wwin && bnff_window_ok_ex(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w,
+                                    (a->dy_pro != BNFF_PRO_NONE ? BNFF_WT_DGRAD_PRO : 0) |
+                                        (a->epi >= BNFF_DG_NRC ? BNFF_WT_DGRAD_NRC : 0))) {
     if (a->dy_pro == BNFF_PRO_BN_DX && (!a->dy_coef.a || !a->dy_coef.e))
       return set_error(BNFF_ERR_STATE, "dgrad: missing deferred-gradient coefficients");
     const int wrc = bnff_window_conv(a->dtype, 1, p.kh, p.pad, a->dy, a->dy_x, a->dy_pro, a->dy_coef, a->dx,
@@ -875,6 +880,8 @@ extern "C" int bnff_conv_dgrad(const bnff_dgrad_args* a, void* stream) {
   p.splits = 1;
   p.a_ptr = a->dy.ptr; p.a_rs = a->dy.row_stride; p.a_pro = a->dy_pro; p.a_coef = a->dy_coef;
   p.a_xptr = a->dy_x.ptr; p.a_xrs = a->dy_x.row_stride;
+  if (!a->wpack_t)
+    return set_error(BNFF_ERR_STATE, "dgrad: window kernel not eligible and no generic packed weights");
   p.b_ptr = a->wpack_t; p.b_rs = kpad_elems(a->dtype, K);
   p.c_ptr = a->dx.ptr; p.c_rs = a->dx.row_stride;
   p.epi = a->epi;
@@ -946,7 +953,9 @@ extern "C" int bnff_conv_wgrad(const bnff_wgrad_args* a, void* stream) {
   p.oh = (int)a->dy.h; p.ow = (int)a->dy.w; p.cout = (int)a->dy.c;
   if ((p.h + 2 * p.pad - p.kh) / p.stride + 1 != p.oh || (p.w + 2 * p.pad - p.kw) / p.stride + 1 != p.ow)
     return set_error(BNFF_ERR_SHAPE, "wgrad: dy spatial dims inconsistent with x");
-  if (a->splits >= 0 && a->dtype == BNFF_BF16 && bnff_window_ok(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w)) {
+  // (the window wgrad plans its own shared memory and reports a no-fit: shape class only)
+  if (a->splits >= 0 && a->dtype == BNFF_BF16 &&
+      bnff_window_ok_ex(a->dtype, p.cin, p.cout, p.kh, p.kw, p.stride, p.pad, p.h, p.w, 0)) {
     // window-shift kernel (splits < 0 forces the generic path)
     int rc2 = bnff_window_wgrad(a->x, a->x_pro, a->x_coef, a->dy, a->dy_x, a->dy_pro, a->dy_coef, p.kh,
                                 a->workspace, a->dw, a->dw_cin, a->dbias, stream);

@@ -190,6 +190,141 @@ __global__ void __launch_bounds__(256) col2im_kernel(const T* __restrict__ dcol,
 }
 
 
+
+// ---------------------------------------------------------------------------
+// strided convolutions (ResNet's stride-2 3x3s) on the window GEMM: a patch matrix per conv
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void ld16(const T* p, float (&f)[16 / sizeof(T)]) {
+  const uint4 r = __ldg(reinterpret_cast<const uint4*>(p));
+  if constexpr (sizeof(T) == 2) {
+    f[0] = bf16lo(r.x); f[1] = bf16hi(r.x); f[2] = bf16lo(r.y); f[3] = bf16hi(r.y);
+    f[4] = bf16lo(r.z); f[5] = bf16hi(r.z); f[6] = bf16lo(r.w); f[7] = bf16hi(r.w);
+  } else {
+    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y); f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st16(T* p, const float (&f)[16 / sizeof(T)]) {
+  uint4 o;
+  if constexpr (sizeof(T) == 2) {
+    o.x = pack_bf16(f[0], f[1]); o.y = pack_bf16(f[2], f[3]); o.z = pack_bf16(f[4], f[5]); o.w = pack_bf16(f[6], f[7]);
+  } else {
+    o = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+  *reinterpret_cast<uint4*>(p) = o;
+}
+
+// col[p][(ky*kw + kx)*C + c] = pro(x)[n, oy*s + ky - pad, ox*s + kx - pad, c], zero outside the map
+// (padding applies after the normalize/ReLU prologue, fused.py:133-138).  pro: 0 none, 1 ReLU,
+// 2 BN+ReLU as the window kernels compute it: max(fmaf(x, s, b - m*s), 0).  One thread per
+// 16-byte chunk of a (pixel, tap) run.
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_s_kernel(const T* __restrict__ x, long long x_rs, int n, int h,
+                                                       int w, int C, int oh, int ow, int kh, int kw, int stride,
+                                                       int pad, int pro, const float* __restrict__ cm,
+                                                       const float* __restrict__ cs, const float* __restrict__ cb,
+                                                       T* __restrict__ col, long long col_rs) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int EC = 16 / (int)sizeof(T);
+  const int cpc = C / EC;
+  const long long total = (long long)n * oh * ow * kh * kw * cpc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % cpc);
+    long long t = i / cpc;
+    const int tap = (int)(t % (kh * kw));
+    const long long p = t / (kh * kw);
+    const int ox = (int)(p % ow);
+    const long long q = p / ow;
+    const int oy = (int)(q % oh);
+    const int img = (int)(q / oh);
+    const int iy = oy * stride + tap / kw - pad, ix = ox * stride + tap % kw - pad;
+    const int c0 = j * EC;
+    float f[EC];
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+      ld16(x + ((long long)(img * h + iy) * w + ix) * x_rs + c0, f);
+      if (pro == 2) {
+#pragma unroll
+        for (int e = 0; e < EC; ++e) {
+          const float sc = __ldg(cs + c0 + e);
+          f[e] = fmaxf(fmaf(f[e], sc, __ldg(cb + c0 + e) - __ldg(cm + c0 + e) * sc), 0.f);
+        }
+      } else if (pro == 1) {
+#pragma unroll
+        for (int e = 0; e < EC; ++e) f[e] = fmaxf(f[e], 0.f);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EC; ++e) f[e] = 0.f;
+    }
+    st16(col + p * col_rs + tap * C + c0, f);
+  }
+}
+
+// dx[n, iy, ix, c] = epi(sum over the taps that reach (iy, ix) of dcol[p(oy, ox)][(ky*kw + kx)*C + c])
+// in fixed tap order; epi: 0 plain, 1 CLIP (x > 0), 2 NRC mask (fmaf(x, s, b - m*s) > 0, the
+// window kernels' ReLU decision).  One thread per 16-byte chunk of an input pixel.
+template <typename T>
+__global__ void __launch_bounds__(256) col2im_s_kernel(const T* __restrict__ dcol, long long col_rs, int n, int h,
+                                                       int w, int C, int oh, int ow, int kh, int kw, int stride,
+                                                       int pad, int epi, const T* __restrict__ xm, long long xm_rs,
+                                                       const float* __restrict__ cm, const float* __restrict__ cs,
+                                                       const float* __restrict__ cb, T* __restrict__ dx,
+                                                       long long dx_rs) {
+  griddep_launch();
+  griddep_wait();
+  constexpr int EC = 16 / (int)sizeof(T);
+  const int cpc = C / EC;
+  const long long total = (long long)n * h * w * cpc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % cpc);
+    const long long pix = i / cpc;
+    const int ix = (int)(pix % w);
+    const long long q = pix / w;
+    const int iy = (int)(q % h);
+    const int img = (int)(q / h);
+    const int c0 = j * EC;
+    float acc[EC];
+#pragma unroll
+    for (int e = 0; e < EC; ++e) acc[e] = 0.f;
+    for (int ky = (iy + pad) % stride; ky < kh; ky += stride) {
+      const int ty = iy + pad - ky;
+      if (ty < 0) break;
+      const int oy = ty / stride;
+      if (oy >= oh) continue;
+      for (int kx = (ix + pad) % stride; kx < kw; kx += stride) {
+        const int tx = ix + pad - kx;
+        if (tx < 0) break;
+        const int ox = tx / stride;
+        if (ox >= ow) continue;
+        float f[EC];
+        ld16(dcol + (((long long)img * oh + oy) * ow + ox) * col_rs + (ky * kw + kx) * C + c0, f);
+#pragma unroll
+        for (int e = 0; e < EC; ++e) acc[e] += f[e];
+      }
+    }
+    if (epi) {
+      float xv[EC];
+      ld16(xm + pix * xm_rs + c0, xv);
+#pragma unroll
+      for (int e = 0; e < EC; ++e) {
+        bool keep;
+        if (epi == 1) {
+          keep = xv[e] > 0.f;
+        } else {
+          const float sc = __ldg(cs + c0 + e);
+          keep = fmaf(xv[e], sc, __ldg(cb + c0 + e) - __ldg(cm + c0 + e) * sc) > 0.f;
+        }
+        acc[e] = keep ? acc[e] : 0.f;
+      }
+    }
+    st16(dx + pix * dx_rs + c0, acc);
+  }
+}
+
 }  // namespace stem
 }  // namespace bnff
 
@@ -291,4 +426,64 @@ extern "C" int bnff_col2im(int32_t dtype, bnff_view dcol, int32_t c_real, int32_
            (int)ow, kh, kw, stride, pad, c_real, (int)dx.c, (__nv_bfloat16*)dx.ptr, (long long)dx.row_stride);
   }
   return check_launch("col2im");
+}
+
+static inline int grid256(long long work) {
+  long long b = (work + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
+}
+
+extern "C" int bnff_im2col_s(int32_t dtype, bnff_view x, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                             int32_t pro, bnff_coef pcoef, bnff_view col, void* stream) {
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "im2col_s: dtype");
+  const int ec = dtype == BNFF_F32 ? 4 : 8;
+  if (x.c % ec || x.row_stride % ec || col.row_stride % ec)
+    return set_error(BNFF_ERR_UNSUPPORTED, "im2col_s: channels must fill 16-byte chunks");
+  const long long oh = (x.h + 2 * pad - kh) / stride + 1, ow = (x.w + 2 * pad - kw) / stride + 1;
+  if (col.n != x.n || col.h != oh || col.w != ow || col.c < (long long)kh * kw * x.c)
+    return set_error(BNFF_ERR_SHAPE, "im2col_s: col (%lld,%lld,%lld,%lld)", (long long)col.n, (long long)col.h,
+                     (long long)col.w, (long long)col.c);
+  if (pro == BNFF_PRO_BN_RELU && (!pcoef.a || !pcoef.b || !pcoef.c))
+    return set_error(BNFF_ERR_STATE, "im2col_s: missing normalisation tables");
+  const int p = pro == BNFF_PRO_BN_RELU ? 2 : (pro == BNFF_PRO_RELU ? 1 : 0);
+  const long long work = x.n * oh * ow * kh * kw * (x.c / ec);
+  if (dtype == BNFF_F32)
+    launch(stem::im2col_s_kernel<float>, dim3(grid256(work)), dim3(256), 0, (cudaStream_t)stream, (const float*)x.ptr,
+           (long long)x.row_stride, (int)x.n, (int)x.h, (int)x.w, (int)x.c, (int)oh, (int)ow, kh, kw, stride, pad, p,
+           pcoef.a, pcoef.b, pcoef.c, (float*)col.ptr, (long long)col.row_stride);
+  else
+    launch(stem::im2col_s_kernel<__nv_bfloat16>, dim3(grid256(work)), dim3(256), 0, (cudaStream_t)stream,
+           (const __nv_bfloat16*)x.ptr, (long long)x.row_stride, (int)x.n, (int)x.h, (int)x.w, (int)x.c, (int)oh,
+           (int)ow, kh, kw, stride, pad, p, pcoef.a, pcoef.b, pcoef.c, (__nv_bfloat16*)col.ptr,
+           (long long)col.row_stride);
+  return check_launch("im2col_s");
+}
+
+extern "C" int bnff_col2im_s(int32_t dtype, bnff_view dcol, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                             int32_t epi, bnff_view x, bnff_coef ecoef, bnff_view dx, void* stream) {
+  if (dtype != BNFF_BF16 && dtype != BNFF_F32) return set_error(BNFF_ERR_UNSUPPORTED, "col2im_s: dtype");
+  const int ec = dtype == BNFF_F32 ? 4 : 8;
+  if (dx.c % ec || dx.row_stride % ec || dcol.row_stride % ec)
+    return set_error(BNFF_ERR_UNSUPPORTED, "col2im_s: channels must fill 16-byte chunks");
+  const long long oh = (dx.h + 2 * pad - kh) / stride + 1, ow = (dx.w + 2 * pad - kw) / stride + 1;
+  if (dcol.n != dx.n || dcol.h != oh || dcol.w != ow || dcol.c < (long long)kh * kw * dx.c)
+    return set_error(BNFF_ERR_SHAPE, "col2im_s: dcol vs dx");
+  const int e = epi == BNFF_DG_NRC ? 2 : (epi == BNFF_DG_CLIP ? 1 : 0);
+  if (e && (!x.ptr || x.n != dx.n || x.h != dx.h || x.w != dx.w || x.c != dx.c))
+    return set_error(BNFF_ERR_SHAPE, "col2im_s: mask input");
+  if (e == 2 && (!ecoef.a || !ecoef.b || !ecoef.c)) return set_error(BNFF_ERR_STATE, "col2im_s: missing tables");
+  if (epi != BNFF_DG_PLAIN && epi != BNFF_DG_CLIP && epi != BNFF_DG_NRC)
+    return set_error(BNFF_ERR_UNSUPPORTED, "col2im_s: epilogue %d", epi);
+  const long long work = dx.n * dx.h * dx.w * (dx.c / ec);
+  if (dtype == BNFF_F32)
+    launch(stem::col2im_s_kernel<float>, dim3(grid256(work)), dim3(256), 0, (cudaStream_t)stream,
+           (const float*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)dx.c, (int)oh,
+           (int)ow, kh, kw, stride, pad, e, (const float*)x.ptr, (long long)x.row_stride, ecoef.a, ecoef.b, ecoef.c,
+           (float*)dx.ptr, (long long)dx.row_stride);
+  else
+    launch(stem::col2im_s_kernel<__nv_bfloat16>, dim3(grid256(work)), dim3(256), 0, (cudaStream_t)stream,
+           (const __nv_bfloat16*)dcol.ptr, (long long)dcol.row_stride, (int)dx.n, (int)dx.h, (int)dx.w, (int)dx.c,
+           (int)oh, (int)ow, kh, kw, stride, pad, e, (const __nv_bfloat16*)x.ptr, (long long)x.row_stride, ecoef.a,
+           ecoef.b, ecoef.c, (__nv_bfloat16*)dx.ptr, (long long)dx.row_stride);
+  return check_launch("col2im_s");
 }

@@ -168,7 +168,10 @@ struct Carve {
 };
 
 template <int BN, int RB, int TAPS, int MODE, bool SW = false, int ES = 2>
-__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop, bool gb = false) {
+// tf: tables the launch needs -- bit 0: operand-prologue table (pro != NONE), bit 1: the NRC
+// epilogue's four columns (dgrad, epi >= NRC); plain launches (patch-matrix GEMMs) carve neither
+__host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, bool xop, bool gb = false,
+                                       int tf = 3) {
   using L = Layout<BN, RB, TAPS, MODE, SW, ES>;
   Carve c{};
   int off = 0;
@@ -184,9 +187,9 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.gbuf = off;  // block-gradient fold by TMA: one 128B-swizzled G tile per owned chunk
   if (gb) off += 2 * L::MYCH * 128 * 128;
   c.ptab = off;
-  off += 3 * nslab * L::SLABW * 4;
+  if (tf & 1) off += 3 * nslab * L::SLABW * 4;
   c.etab = off;
-  off += (MODE == M_DGRAD ? 4 : 1) * npad * 4;  // bias | NRC (scale, shift, inv, -mean*inv)
+  off += (MODE == M_DGRAD && (tf & 2) ? 4 : 1) * npad * 4;  // bias | NRC (scale, shift, inv, -mean*inv)
   c.sacc = off;
   off += 2 * BN * (L::F32 ? 8 : 4);  // per-CTA sums (fp32 data: float64)
   c.red = off;
@@ -198,6 +201,11 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.meta = off;  // (unused by the TMA loader)
   c.total = off + 1024;  // + alignment slack
   return c;
+}
+
+template <int MODE>
+__host__ __device__ inline int wtables(const WcParams& p) {
+  return (p.pro != BNFF_PRO_NONE ? 1 : 0) | (MODE == M_DGRAD && p.epi >= BNFF_DG_NRC ? 2 : 0);
 }
 
 // the 1x1 block-gradient fold runs through TMA (G tile loaded, folded in smem, stored back)
@@ -266,7 +274,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   __shared__ uint32_t tmem_sh;
   const bool xop_s = L::XOP && p.pro == BNFF_PRO_BN_DX;
   const bool gb_s = fold_tma<BN, RB, TAPS, MODE, SW, ES>(p);
-  const Carve cv = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, p.stages, xop_s, gb_s);
+  const int tf_s = wtables<MODE>(p);
+  const Carve cv = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, p.stages, xop_s, gb_s, tf_s);
   const int ST = p.stages;
   float* ptab = reinterpret_cast<float*>(smem + cv.ptab);
   float* etab = reinterpret_cast<float*>(smem + cv.etab);
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
   static_assert(PRODUCER * 32 == ST_THREADS, "producer is the last warp");
   if (warp != PRODUCER) {
   // window-operand tables: BN_RELU: (scale, beta - mean*scale); BN_DX: (g, -g*k2*inv, g*(k2*inv*mean-k1))
-  for (int c = tid; c < kpad; c += ST_THREADS) {
+  for (int c = tid; (tf_s & 1) && c < kpad; c += ST_THREADS) {
     float t0 = 1.f, t1 = 0.f, t2 = 0.f;
     if (c < p.ci) {
       if (p.pro == BNFF_PRO_BN_RELU) {
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       }
     }
     etab[c] = t0;
-    if (MODE == M_DGRAD) {
+    if (MODE == M_DGRAD && (tf_s & 2)) {
       etab[p.npad + c] = t1;
       etab[2 * p.npad + c] = t2;
       etab[3 * p.npad + c] = t3;
@@ -1777,7 +1786,7 @@ static int launch_t(WcParams p, cudaStream_t st) {
   const bool xop = MODE == M_DGRAD && p.pro == BNFF_PRO_BN_DX;
   bool gb = fold_tma<BN, RB, TAPS, MODE, SW, ES>(p);
   for (; stages >= 2; --stages) {
-    c = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, stages, xop, gb);
+    c = carve<BN, RB, TAPS, MODE, SW, ES>(p.R, p.nslab, p.npad, stages, xop, gb, wtables<MODE>(p));
     if (c.total <= SMEM_BUDGET) break;
   }
   if (stages < 2) return kWindowNoFit;  // caller falls back to the generic kernel
@@ -1859,24 +1868,24 @@ using namespace bnff;
 namespace bnff {
 namespace wc {
 template <int MODE, int TAPS>
-static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop) {
+static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop, int tf = 3) {
   Carve c{};
-  if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop)
-                              : carve<64, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop);
-  else if (RB == 64 && MODE == M_DGRAD && BN == 64) c = carve<64, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, true);
-  else if (RB == 64) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
-  else if (BN == 32) c = carve<32, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
-  else if (BN == 64) c = carve<64, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
-  else if (MODE == M_FPROP) c = carve<128, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop);
+  if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop, false, tf)
+                              : carve<64, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop, false, tf);
+  else if (RB == 64 && MODE == M_DGRAD && BN == 64) c = carve<64, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, true, tf);
+  else if (RB == 64) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
+  else if (BN == 32) c = carve<32, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
+  else if (BN == 64) c = carve<64, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
+  else if (MODE == M_FPROP) c = carve<128, 128, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
   else return false;
   return c.total <= SMEM_BUDGET;
 }
 template <int MODE, int TAPS>
-static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw = 0) {
+static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw = 0, int tf = 3) {
   Carve c{};
-#define BNFF_FIT(bn, rb) c = carve<bn, rb, TAPS, MODE>(R, nslab, npad, 2, xop)
+#define BNFF_FIT(bn, rb) c = carve<bn, rb, TAPS, MODE>(R, nslab, npad, 2, xop, false, tf)
   if (TAPS == 9 && sw) {
-    c = carve<64, 64, TAPS, MODE, true>(R, nslab, npad, 2, xop);
+    c = carve<64, 64, TAPS, MODE, true>(R, nslab, npad, 2, xop, false, tf);
     return c.total <= SMEM_BUDGET;
   }
   if (RB == 64) {
@@ -1894,8 +1903,8 @@ static bool fits2(int BN, int RB, int R, int nslab, int npad, bool xop, int sw =
 
 // eligibility of the window kernels for a conv (bf16, stride 1, 1x1/p0 or 3x3/p1), for all
 // three passes: the shared-memory plan must fit with >= 2 stages in the worst case
-extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
-                              int32_t stride, int32_t pad, int32_t h, int32_t w) {
+extern "C" int bnff_window_ok_ex(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
+                                 int32_t stride, int32_t pad, int32_t h, int32_t w, int32_t tables) {
   if ((dtype != BNFF_BF16 && dtype != BNFF_F32) || stride != 1) return 0;
   const int es = dtype == BNFF_F32 ? 4 : 2;
   if (!((kh == 1 && kw == 1 && pad == 0) || (kh == 3 && kw == 3 && pad == 1))) return 0;
@@ -1908,22 +1917,30 @@ extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_
   const int R = 128 + (kh == 3 ? 2 * (w + 2) + 2 : 0);
   for (int d = 0; d < 2; ++d) {
     const int CI = d ? c_out : c_in, N = d ? c_in : c_out;
+    const int tf = d ? ((tables & BNFF_WT_DGRAD_PRO) ? 1 : 0) | ((tables & BNFF_WT_DGRAD_NRC) ? 2 : 0)
+                     : ((tables & BNFF_WT_FPROP_PRO) ? 1 : 0);
     const wc::Geo g = wc::geo(CI, N, kh, kw, d, es);
     if (es == 4) {
-      const bool ok4 = kh == 3 ? (d ? wc::fits2_f32<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true)
-                                    : wc::fits2_f32<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false))
-                               : (d ? wc::fits2_f32<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
-                                    : wc::fits2_f32<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false));
+      const bool ok4 = kh == 3 ? (d ? wc::fits2_f32<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, tf)
+                                    : wc::fits2_f32<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, tf))
+                               : (d ? wc::fits2_f32<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true, tf)
+                                    : wc::fits2_f32<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false, tf));
       if (!ok4) return 0;
       continue;
     }
-    const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, g.sw)
-                                 : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, g.sw))
-                            : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true)
-                                 : wc::fits2<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false));
+    const bool ok = kh == 3 ? (d ? wc::fits2<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, g.sw, tf)
+                                 : wc::fits2<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, g.sw, tf))
+                            : (d ? wc::fits2<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true, 0, tf)
+                                 : wc::fits2<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false, 0, tf));
     if (!ok) return 0;
   }
   return 1;
+}
+
+extern "C" int bnff_window_ok(int32_t dtype, int32_t c_in, int32_t c_out, int32_t kh, int32_t kw,
+                              int32_t stride, int32_t pad, int32_t h, int32_t w) {
+  return bnff_window_ok_ex(dtype, c_in, c_out, kh, kw, stride, pad, h, w,
+                           BNFF_WT_FPROP_PRO | BNFF_WT_DGRAD_PRO | BNFF_WT_DGRAD_NRC);
 }
 
 extern "C" int64_t bnff_window_pack_size(int32_t dtype, int32_t c_out, int32_t c_in, int32_t kh,

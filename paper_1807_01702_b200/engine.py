@@ -173,6 +173,7 @@ class Engine:
         self.fuse_finalize = os.environ.get("BNFF_FUSE_FINALIZE", "1") != "0"
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
         self.wide_fallback = os.environ.get("BNFF_WIDE_FALLBACK", "1") != "0"  # see _f_FusedNormReluConv
+        self.col_strided = os.environ.get("BNFF_COL_STRIDED", "1") != "0"  # see _col_conv
         self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
         self._wide_saved: dict = {}  # NRC node id -> materialised relu(bn(x)) (wide-N fallback)
         self._nrp_done: set = set()
@@ -182,7 +183,7 @@ class Engine:
         self.fold = {}  # block group -> dict(A, B, ones, m32, i32, started)
         self._side = None  # side stream of the weight-gradient launches
         self.wpacks = {}  # conv name -> (window fwd pack, window dgrad pack, conv)
-        self.cols = {}  # stem conv name -> (1x1 conv over col, col buffer, dw scratch, kpad)
+        self.cols = {}  # conv name -> (1x1 conv over col, col buffer, dw scratch, kpad, strided)
         self.col_src = {}  # 1x1 col conv name -> (fp32 (co, kpad) weights, stem conv, kpad)
         self.use_shared = any(n.kind == G.FUSED_CONCAT_STATS or
                               (n.kind == G.CONCAT and not n.attrs.physical) for n in g.nodes)
@@ -337,12 +338,19 @@ class Engine:
             self.packs[key] = (self._zeros((n,)), self._zeros((nt,)), cin_store, conv)
             # window-shift kernel weights (bf16 stride-1 1x1/3x3 convs)
             h, w = hw if hw is not None else (0, 0)
-            if self.use_window and cin_store == conv.in_c and self.L.bnff_window_ok(
-                    self.dcode, conv.in_c, conv.out_c, conv.kh, conv.kw, conv.stride, conv.pad, h, w):
+            # patch-matrix GEMMs: plain fprop operand, plain dgrad epilogue (dy may be deferred)
+            tables = _lib.WT_DGRAD_PRO if key in self.col_src else _lib.WT_ALL
+            if self.use_window and cin_store == conv.in_c and self.L.bnff_window_ok_ex(
+                    self.dcode, conv.in_c, conv.out_c, conv.kh, conv.kw, conv.stride, conv.pad, h, w, tables):
                 nf = self.L.bnff_window_pack_size(self.dcode, conv.out_c, conv.in_c, conv.kh, conv.kw, 0)
                 nd = self.L.bnff_window_pack_size(self.dcode, conv.out_c, conv.in_c, conv.kh, conv.kw, 1)
                 self.wpacks[key] = (self._zeros((nf,)), self._zeros((nd,)), conv)
         return self.packs[key]
+
+    def _gpack(self, conv, t):
+        """generic packed weights, or NULL for a window-layout conv (the optimizer only
+        repacks its window layout: a rejected window launch must fail, not read stale packs)"""
+        return 0 if conv.name in self.wpacks else _ptr(t)
 
     def _wwin(self, conv, which):
         wp = self.wpacks.get(conv.name)
@@ -413,37 +421,54 @@ class Engine:
         self._flush_pending()
         self.launch_counts["fwd"] = len(self.fwd)
 
-    def _col_conv(self, conv, x):
-        """A channel-poor stem conv (the 3-channel image, stored with 8) runs as im2col +
-        a 1x1 window GEMM over the patch matrix (csrc/stem.cu).  Returns
-        (conv1x1, col, dw2, kpad) or None when the conv does not qualify."""
+    def _col_conv(self, conv, x, pro=None):
+        """Convolutions the window kernels cannot run directly go through a patch matrix and
+        a 1x1 window GEMM over it (csrc/stem.cu): the channel-poor stem conv (the 3-channel
+        image, stored with 8; pro NONE only) and strided convolutions whose channels fill
+        16-byte chunks (ResNet's stride-2 3x3s; the operand prologue -- ReLU or BN+ReLU -- is
+        applied while the patch matrix is written).  Returns (conv1x1, col, dw2, kpad,
+        strided) or None when the conv does not qualify."""
         if conv.name in self.cols:
             return self.cols[conv.name]
-        if not (self.use_window and x.shape[3] * x.element_size() == 16 and conv.in_c <= x.shape[3]
-                and conv.kh * conv.kw > 1):
+        if not self.use_window or pro is None:
             return None
-        kpad = _round_up(conv.kh * conv.kw * conv.in_c, 16)
-        n, h, w, _ = x.shape
+        n, h, w, cs = x.shape
+        chunk = 16 // x.element_size()
+        stem = cs * x.element_size() == 16 and conv.in_c <= cs and conv.kh * conv.kw > 1 \
+            and pro == _lib.PRO_NONE
+        strided = not stem and conv.stride > 1 and cs == conv.in_c and cs % chunk == 0 \
+            and self.col_strided
+        if not (stem or strided):
+            return None
+        taps_c = conv.kh * conv.kw * conv.in_c
+        kpad = _round_up(taps_c, 16)
         oh, ow = conv.out_hw(h, w)
-        if not self.L.bnff_window_ok(self.dcode, kpad, conv.out_c, 1, 1, 1, 0, oh, ow):
+        # the GEMM over the patch matrix runs with a plain operand and a plain epilogue
+        if not self.L.bnff_window_ok_ex(self.dcode, kpad, conv.out_c, 1, 1, 1, 0, oh, ow, _lib.WT_DGRAD_PRO):
             return None
         c1 = ConvParams(in_c=kpad, out_c=conv.out_c, kh=1, kw=1, name=conv.name + "#col")
-        col = self._empty((n, oh, ow, kpad))
+        col = self._zeros((n, oh, ow, kpad)) if kpad != taps_c else self._empty((n, oh, ow, kpad))
         w2 = self._zeros((conv.out_c * kpad,), torch.float32)
         dw2 = self._zeros((conv.out_c * kpad,), torch.float32)
         self.col_src[c1.name] = (w2, conv, kpad)
-        self.cols[conv.name] = ent = (c1, col, dw2, kpad)
+        self.cols[conv.name] = ent = (c1, col, dw2, kpad, strided)
         return ent
 
     def _conv_fprop(self, node, x, y, conv, pro, tables, stat_part):
-        col = self._col_conv(conv, x) if pro == _lib.PRO_NONE else None
+        col = self._col_conv(conv, x, pro)
         pname = conv.name
-        if col is not None:  # stem: patch matrix, then a 1x1 GEMM over it
-            c1, colt, _, _ = col
-            self._emit(self.L.bnff_im2col, self.dcode, view_of(x), conv.in_c, conv.kh, conv.kw,
-                       conv.stride, conv.pad, view_of(colt), what=f"im2col {node.name}",
-                       nbytes=_nb(x, colt))
-            x, conv = colt, c1
+        if col is not None:  # patch matrix (operand prologue applied), then a 1x1 GEMM over it
+            c1, colt, _, _, strided = col
+            if strided:
+                cf = coef_of() if tables is None else coef_of(tables[0], tables[1], tables[2])
+                self._emit(self.L.bnff_im2col_s, self.dcode, view_of(x), conv.kh, conv.kw, conv.stride,
+                           conv.pad, pro, cf, view_of(colt), what=f"im2col {node.name}",
+                           nbytes=_nb(x, colt))
+            else:
+                self._emit(self.L.bnff_im2col, self.dcode, view_of(x), conv.in_c, conv.kh, conv.kw,
+                           conv.stride, conv.pad, view_of(colt), what=f"im2col {node.name}",
+                           nbytes=_nb(x, colt))
+            x, conv, pro, tables = colt, c1, _lib.PRO_NONE, None
         cin_store = x.shape[3]
         wp, _, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if tables is None:
@@ -451,7 +476,7 @@ class Engine:
         else:
             cf = coef_of(tables[0], tables[1], tables[2])
         args = _lib.FpropArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(x),
-                              view_of(y), _ptr(wp), _ptr(self.param(f"{pname}.bias")), pro, cf,
+                              view_of(y), self._gpack(conv, wp), _ptr(self.param(f"{pname}.bias")), pro, cf,
                               _ptr(stat_part), self._wwin(conv, 0))
         n_, oh_, ow_, co_ = y.shape
         flops = 2 * n_ * oh_ * ow_ * co_ * conv.kh * conv.kw * cin_store
@@ -683,7 +708,7 @@ class Engine:
             cin_s = self._store_c(xs[1])
             ws = max(ws, self.L.bnff_wgrad_workspace(xs[0], oh, ow, conv.kh, conv.kw, cin_s,
                                                     conv.out_c, 0))
-        for c1, colt, _, _ in self.cols.values():  # stem GEMMs over their patch matrices
+        for c1, colt, _, _, _ in self.cols.values():  # GEMMs over patch matrices
             n, oh, ow, kp = colt.shape
             ws = max(ws, self.L.bnff_wgrad_workspace(n, oh, ow, 1, 1, kp, c1.out_c, 0))
         self.wg_ws = self._empty((ws,), torch.float32)
@@ -813,22 +838,23 @@ class Engine:
         A wide NRC conv whose forward materialised relu(bn(x)) (_f_FusedNormReluConv) takes its
         weight-gradient operand from that tensor instead of re-normalising x per N tile."""
         cin_store = x.shape[3]
-        wp, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
+        col = self.cols.get(conv.name)
+        if col is None:
+            _, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))
         if isinstance(dy_gv, Deferred):
             dy, dy_x, dy_pro, dy_coef = dy_gv.dt1, dy_gv.x, _lib.PRO_BN_DX, dy_gv.coef()
         else:
             dy, dy_x, dy_pro, dy_coef = dy_gv.t, dy_gv.t, _lib.PRO_NONE, coef_of()
         xc = coef_of() if x_tables is None else coef_of(x_tables[0], x_tables[1], x_tables[2])
-        col = self.cols.get(conv.name) if x_pro == _lib.PRO_NONE else None
-        orig, wconv, wx, wcin = conv, conv, x, cin_store
+        orig, wconv, wx, wcin, wpro = conv, conv, x, cin_store, x_pro
         saved = self._wide_saved.get(node.id)
         if saved is not None and x_pro == _lib.PRO_BN_RELU:
-            wx, x_pro, xc = saved, _lib.PRO_NONE, coef_of()
+            wx, wpro, xc = saved, _lib.PRO_NONE, coef_of()
         dw = self.grad(f"{conv.name}.weight")
-        if col is not None:  # stem: weight gradient of the 1x1 GEMM over the patch matrix
-            wconv, wx, dw = col[0], col[1], col[2]
+        if col is not None:  # weight gradient of the 1x1 GEMM over the (transformed) patch matrix
+            wconv, wx, dw, wpro, xc = col[0], col[1], col[2], _lib.PRO_NONE, coef_of()
             wcin = wx.shape[3]
-        wa = _lib.WgradArgs(self.dcode, wconv.kh, wconv.kw, wconv.stride, wconv.pad, view_of(wx), x_pro,
+        wa = _lib.WgradArgs(self.dcode, wconv.kh, wconv.kw, wconv.stride, wconv.pad, view_of(wx), wpro,
                             xc, view_of(dy), view_of(dy_x), dy_pro, dy_coef, 0, _ptr(self.wg_ws),
                             _ptr(dw), wconv.in_c, _ptr(self.grad(f"{orig.name}.bias")))
         self._keep.append(wa)
@@ -848,23 +874,43 @@ class Engine:
                        what=f"cols_to_weight {node.name}", side=self.side_wgrad)
         dx, part = None, None
         if col is not None and self._wants_dx(node.inputs[0]):
-            # stem input gradient: dgrad of the 1x1 GEMM over the patch matrix (dcol), then a
-            # col2im gather into the channel-padded image layout
-            c1, colt, _, kpad = col
+            # input gradient: dgrad of the 1x1 GEMM over the patch matrix (dcol), then a col2im
+            # gather (the stem's into the channel-padded image layout; a strided conv's with its
+            # dgrad epilogue: ReLU clip or the NRC mask, whose statistics follow from dx)
+            c1, colt, _, kpad, strided = col
             dcol = self._empty(tuple(colt.shape))
             _, wt1, _, _ = self._pack(c1, kpad, (colt.shape[1], colt.shape[2]))
             da = _lib.DgradArgs(self.dcode, 1, 1, 1, 0, view_of(dy), view_of(dy_x), dy_pro, dy_coef,
-                                view_of(dcol), view_of(colt), _ptr(wt1), _lib.DG_PLAIN, coef_of(), 0,
+                                view_of(dcol), view_of(colt), self._gpack(c1, wt1), _lib.DG_PLAIN, coef_of(), 0,
                                 self._wwin(c1, 1))
             self._keep.append(da)
             n_, h_, w_, _ = dcol.shape
             extra = _nb(dy_x) if dy_pro == _lib.PRO_BN_DX else 0
             self._emit(self.L.bnff_conv_dgrad, C.byref(da), what=f"dgrad {node.name}",
                        nbytes=_nb(dy, dcol, wt1) + extra, flops=2 * n_ * h_ * w_ * kpad * dy.shape[3])
-            dx = self._empty(tuple(x.shape))
-            self._emit(self.L.bnff_col2im, self.dcode, view_of(dcol), orig.in_c, orig.kh, orig.kw,
-                       orig.stride, orig.pad, view_of(dx), what=f"col2im {node.name}", nbytes=_nb(dcol, dx))
-            return dx, None
+            if not strided:
+                dx = self._empty(tuple(x.shape))
+                self._emit(self.L.bnff_col2im, self.dcode, view_of(dcol), orig.in_c, orig.kh, orig.kw,
+                           orig.stride, orig.pad, view_of(dx), what=f"col2im {node.name}",
+                           nbytes=_nb(dcol, dx))
+                return dx, None
+            if dgrad_epi not in (_lib.DG_PLAIN, _lib.DG_CLIP, _lib.DG_NRC):
+                raise StateError(f"{node.name}: dgrad epilogue {dgrad_epi} on a patch-matrix conv")
+            dx = self._empty(tuple(x.shape)) if dx_out is None else dx_out
+            ecoef = coef_of()
+            if dgrad_epi == _lib.DG_NRC:
+                m32, s32, b32, i32 = dgrad_tables
+                ecoef = coef_of(m32, s32, b32, i32)
+            self._emit(self.L.bnff_col2im_s, self.dcode, view_of(dcol), orig.kh, orig.kw, orig.stride,
+                       orig.pad, dgrad_epi, view_of(x), ecoef, view_of(dx), what=f"col2im {node.name}",
+                       nbytes=_nb(dcol, dx) + (_nb(x) if dgrad_epi != _lib.DG_PLAIN else 0))
+            if dgrad_epi == _lib.DG_NRC:  # (sum dt1, sum dt1*xhat) of the stored dt1
+                pixels = x.shape[0] * x.shape[1] * x.shape[2]
+                tiles = self.L.bnff_sum_tiles(pixels)
+                part = self._empty((tiles, 2, x.shape[3]), torch.float64)
+                self._emit(self.L.bnff_channel_sums, self.dcode, 1, view_of(x), view_of(dx),
+                           coef_of(m32, i32), _ptr(part), what=f"nrc_sums {node.name}", nbytes=_nb(x, dx))
+            return dx, part
         if self._wants_dx(node.inputs[0]):
             dx = self._empty(tuple(x.shape)) if dx_out is None else dx_out
             ecoef = coef_of()
@@ -873,7 +919,7 @@ class Engine:
                 m32, s32, b32, i32 = dgrad_tables
                 ecoef = coef_of(m32, s32, b32, i32)
             da = _lib.DgradArgs(self.dcode, conv.kh, conv.kw, conv.stride, conv.pad, view_of(dy),
-                                view_of(dy_x), dy_pro, dy_coef, view_of(dx), view_of(x), _ptr(wt),
+                                view_of(dy_x), dy_pro, dy_coef, view_of(dx), view_of(x), self._gpack(conv, wt),
                                 dgrad_epi, ecoef, _ptr(part), self._wwin(conv, 1))
             self._keep.append(da)
             n_, h_, w_, ci_ = dx.shape

@@ -212,6 +212,11 @@ int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean, double* pa
                       void* stream);
 int bnff_var_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
                       void* stream);
+/* var_finalize fused with bn_coeffs for the same BN (the unfused two-pass BN: var, then the
+ * fp32 (mean32, scale32, beta32, inv32) tables, in one launch) */
+int bnff_var_finalize_coeffs(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
+                             const double* mean, const float* gamma, const float* beta, float eps,
+                             float* mean32, float* scale32, float* beta32, float* inv32, void* stream);
 int bnff_bn_coeffs(int32_t c, const double* mean, const double* var, const float* gamma,
                    const float* beta, float eps, float* mean32, float* scale32, float* beta32,
                    float* inv32, void* stream);

@@ -95,6 +95,7 @@ SIGNATURES = {
     "bnff_stats_finalize": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _P]),
     "bnff_centered_var": (C.c_int, [_I32, View, _P, _P, _P]),
     "bnff_var_finalize": (C.c_int, [_P, _I32, _I32, _I64, _P, _P]),
+    "bnff_var_finalize_coeffs": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P, C.c_float, _P, _P, _P, _P, _P]),
     "bnff_stats_finalize_coeffs": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P, _I32, _I32, _P, _P, _P,
                                              _P, _F, _P, _P, _P, _P, _P]),
     "bnff_bn_coeffs": (C.c_int, [_I32, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),

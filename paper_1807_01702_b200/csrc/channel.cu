@@ -395,25 +395,44 @@ __host__ __device__ inline int sum_tiles(long long pixels) {
   return (int)(t < kMaxTiles ? (t < 1 ? 1 : t) : kMaxTiles);
 }
 
+// 16-byte channel columns per CTA of channel_sums: all of them, unless the map is so small
+// that the row tiles alone leave SMs idle -- then groups of >= 32 columns (>= 4 x 148 CTAs)
+inline int sum_col_width(int dtype, int c, int tiles) {
+  const int cpr = c / (dtype == BNFF_F32 ? 4 : 8);
+  const int want = (4 * 148 + tiles - 1) / tiles;
+  int groups = cpr / 32;
+  if (groups > want) groups = want;
+  if (groups < 1) groups = 1;
+  return (cpr + groups - 1) / groups;
+}
+
 // mode 0: (x, x^2); mode 1: (dy, dy*xhat) xhat=(x-a)*b; mode 2: (dy', 0) with dy'
-// = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double)
-template <typename T>
-__global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixels, int C,
-                                    bnff_coef cf, const double* mean64, double* part) {
+// = dy or BN_DX(dy, x) when coef.e != null; mode 3: (centred^2, 0) with a = mean (double).
+// Grid: x = row tiles (the partial rows), y = channel groups of `cw` 16-byte columns (small
+// maps with many channels get more CTAs).  Four rows per thread in flight (two for MODE 2), then a
+// fixed-order pairwise tree over the threads sharing a column (bitwise deterministic).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kSumThreads, 3) channel_sums_kernel(View xv, View dyv, long long pixels, int C,
+                                                                      int cw, bnff_coef cf, const double* mean64,
+                                                                      double* part) {
+  constexpr int mode = MODE;
   griddep_launch();
   griddep_wait();
   constexpr int V = VecIO<T>::V;
   // fp32 data accumulates in float64 (the reference's bn_stats_onepass sums in f64,
   // ops.py:231-237); bf16 values (8-bit significands) accumulate in fp32
   using Acc = typename std::conditional<sizeof(T) == 4, double, float>::type;
-  __shared__ Acc sh[2][kSumThreads][V];
+  __shared__ Acc sh[2][V][kSumThreads];
   const int cpr = C / V;
   const int tiles = gridDim.x;
   const long long rows_per_tile = (pixels + tiles - 1) / tiles;
   const long long r_begin = blockIdx.x * rows_per_tile;
   const long long r_end = min(pixels, r_begin + rows_per_tile);
-  for (int cbase = 0; cbase < cpr; cbase += kSumThreads) {
-    const int ccount = min(kSumThreads, cpr - cbase);
+  const int g_lo = blockIdx.y * cw, g_hi = min(cpr, g_lo + cw);
+  const bool two = mode == 1 || (mode == 2 && cf.e != nullptr);  // a second operand (x) per row
+  const View pv = (mode == 0 || mode == 3) ? xv : dyv;
+  for (int cbase = g_lo; cbase < g_hi; cbase += kSumThreads) {
+    const int ccount = min(kSumThreads, g_hi - cbase);
     const int rows_per_iter = kSumThreads / ccount;
     const int tcol = threadIdx.x % ccount, trow = threadIdx.x / ccount;
     const bool active = trow < rows_per_iter;
@@ -426,39 +445,16 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
       float ca[V], cb[V];
       double m64[V];
       DxCoef<T, V> dxc;
-      const bool dx2 = mode == 2 && cf.e != nullptr;
       if (mode == 1) {
 #pragma unroll
         for (int i = 0; i < V; ++i) { ca[i] = __ldg(cf.a + c0 + i); cb[i] = __ldg(cf.b + c0 + i); }
-      } else if (dx2) {
+      } else if (mode == 2 && two) {
         dxc.load(cf, c0);
       } else if (mode == 3) {
 #pragma unroll
         for (int i = 0; i < V; ++i) m64[i] = mean64[c0 + i];
       }
-      long long r0 = r_begin + trow;
-      if (mode == 0) {  // plain (x, x^2): four rows in flight per thread
-        for (; r0 + 3 * rows_per_iter < r_end; r0 += 4 * rows_per_iter) {
-          float f[4][V];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) VecIO<T>::load(xv.p, (r0 + u * rows_per_iter) * xv.rs + c0, f[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int i = 0; i < V; ++i) {
-              s1[i] += (Acc)f[u][i];
-              s2[i] += (Acc)f[u][i] * (Acc)f[u][i];
-            }
-        }
-      }
-      for (long long r = r0; r < r_end; r += rows_per_iter) {
-        float v[V], x[V];
-        if (mode == 0 || mode == 3) {
-          VecIO<T>::load(xv.p, r * xv.rs + c0, v);
-        } else {
-          VecIO<T>::load(dyv.p, r * dyv.rs + c0, v);
-          if (mode == 1 || dx2) VecIO<T>::load(xv.p, r * xv.rs + c0, x);
-        }
+      auto acc = [&](const float (&v)[V], const float (&x)[V]) {
 #pragma unroll
         for (int i = 0; i < V; ++i) {
           if (mode == 0) {
@@ -469,37 +465,59 @@ __global__ void channel_sums_kernel(int mode, View xv, View dyv, long long pixel
             s1[i] += (Acc)v[i];
             s2[i] += (Acc)v[i] * (Acc)xh;
           } else if (mode == 2) {
-            s1[i] += (Acc)(dx2 ? dxc.apply(v[i], x[i], i) : v[i]);
+            s1[i] += (Acc)(two ? dxc.apply(v[i], x[i], i) : v[i]);
           } else {
             const Acc d = (Acc)((double)v[i] - m64[i]);
             s1[i] += d * d;
           }
         }
+      };
+      // rows in flight per thread (the deferred-dx dbias keeps five coefficient vectors live)
+      constexpr int U = MODE == 2 ? 2 : 4;
+      long long r = r_begin + trow;
+      for (; r + (U - 1) * rows_per_iter < r_end; r += U * rows_per_iter) {
+        float v[U][V], x[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          VecIO<T>::load(pv.p, (r + u * rows_per_iter) * pv.rs + c0, v[u]);
+          if (two) VecIO<T>::load(xv.p, (r + u * rows_per_iter) * xv.rs + c0, x[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc(v[u], x[u]);
+      }
+      for (; r < r_end; r += rows_per_iter) {
+        float v[V], x[V];
+        VecIO<T>::load(pv.p, r * pv.rs + c0, v);
+        if (two) VecIO<T>::load(xv.p, r * xv.rs + c0, x);
+        acc(v, x);
       }
     }
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      sh[0][threadIdx.x][i] = s1[i];
-      sh[1][threadIdx.x][i] = s2[i];
+      sh[0][i][threadIdx.x] = s1[i];
+      sh[1][i][threadIdx.x] = s2[i];
     }
     __syncthreads();
-    // fixed-order combine of the rows_per_iter threads sharing a column
-    if (threadIdx.x < ccount) {
-      Acc a[V], b[V];
-#pragma unroll
-      for (int i = 0; i < V; ++i) a[i] = b[i] = Acc(0);
-      for (int rr = 0; rr < rows_per_iter; ++rr) {
+    // fixed-order pairwise tree over the rows_per_iter threads of each column
+    for (int n = rows_per_iter; n > 1;) {
+      const int h = (n + 1) >> 1;
+      if (active && trow < n - h) {
+        const int o = threadIdx.x + h * ccount;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          a[i] += sh[0][rr * ccount + threadIdx.x][i];
-          b[i] += sh[1][rr * ccount + threadIdx.x][i];
+          sh[0][i][threadIdx.x] += sh[0][i][o];
+          sh[1][i][threadIdx.x] += sh[1][i][o];
         }
       }
+      n = h;
+      __syncthreads();
+    }
+    if (threadIdx.x < ccount) {
       const int cc = (cbase + threadIdx.x) * V;
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = a[i];
-        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = b[i];
+        part[((long long)blockIdx.x * 2 + 0) * C + cc + i] = sh[0][i][threadIdx.x];
+        part[((long long)blockIdx.x * 2 + 1) * C + cc + i] = sh[1][i][threadIdx.x];
       }
     }
     __syncthreads();
@@ -1135,6 +1153,22 @@ extern "C" int bnff_device_ok(void) {
 
 extern "C" int32_t bnff_sum_tiles(int64_t pixels) { return sum_tiles(pixels); }
 
+template <typename T>
+static void launch_sums_t(int mode, dim3 grid, cudaStream_t st, View x, View dy, long long pixels, int c, int cw,
+                          bnff_coef cf, const double* mean, double* part) {
+  switch (mode) {
+    case 0: launch(channel_sums_kernel<T, 0>, grid, dim3(kSumThreads), 0, st, x, dy, pixels, c, cw, cf, mean, part); break;
+    case 1: launch(channel_sums_kernel<T, 1>, grid, dim3(kSumThreads), 0, st, x, dy, pixels, c, cw, cf, mean, part); break;
+    case 2: launch(channel_sums_kernel<T, 2>, grid, dim3(kSumThreads), 0, st, x, dy, pixels, c, cw, cf, mean, part); break;
+    default: launch(channel_sums_kernel<T, 3>, grid, dim3(kSumThreads), 0, st, x, dy, pixels, c, cw, cf, mean, part);
+  }
+}
+static void launch_sums(int dtype, int mode, dim3 grid, cudaStream_t st, View x, View dy, long long pixels, int c,
+                        int cw, bnff_coef cf, const double* mean, double* part) {
+  if (dtype == BNFF_BF16) launch_sums_t<__nv_bfloat16>(mode, grid, st, x, dy, pixels, c, cw, cf, mean, part);
+  else launch_sums_t<float>(mode, grid, st, x, dy, pixels, c, cw, cf, mean, part);
+}
+
 extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_view dy, bnff_coef coef,
                                  double* part, void* stream) {
   int rc;
@@ -1144,8 +1178,9 @@ extern "C" int bnff_channel_sums(int32_t dtype, int32_t mode, bnff_view x, bnff_
   if (mode == 1 && !same_dims(x, dy)) return set_error(BNFF_ERR_SHAPE, "channel_sums: x/dy dims differ");
   const long long pixels = shape.n * shape.h * shape.w;
   const int tiles = sum_tiles(pixels);
-  BNFF_DISPATCH(dtype, channel_sums_kernel, tiles, kSumThreads, 0, (cudaStream_t)stream, mode, vw(x), vw(dy),
-                pixels, (int)shape.c, coef, nullptr, part);
+  const int cw = sum_col_width(dtype, (int)shape.c, tiles);
+  const dim3 grid(tiles, (unsigned)((shape.c / (dtype == BNFF_F32 ? 4 : 8) + cw - 1) / cw));
+  launch_sums(dtype, mode, grid, (cudaStream_t)stream, vw(x), vw(dy), pixels, (int)shape.c, cw, coef, nullptr, part);
   return check_launch("channel_sums");
 }
 
@@ -1162,8 +1197,9 @@ extern "C" int bnff_centered_var(int32_t dtype, bnff_view x, const double* mean,
   const long long pixels = x.n * x.h * x.w;
   const int tiles = sum_tiles(pixels);
   bnff_coef cf{};
-  BNFF_DISPATCH(dtype, channel_sums_kernel, tiles, kSumThreads, 0, (cudaStream_t)stream, 3, vw(x), vw(x),
-                pixels, (int)x.c, cf, mean, part);
+  const int cw = sum_col_width(dtype, (int)x.c, tiles);
+  const dim3 grid(tiles, (unsigned)((x.c / (dtype == BNFF_F32 ? 4 : 8) + cw - 1) / cw));
+  launch_sums(dtype, 3, grid, (cudaStream_t)stream, vw(x), vw(x), pixels, (int)x.c, cw, cf, mean, part);
   return check_launch("centered_var");
 }
 
@@ -1179,13 +1215,52 @@ __global__ void scale_kernel(double* v, int c, double s) {
 }
 }  // namespace bnff
 
+namespace bnff {
+// centred partials -> var = sum(d^2) * (1/count) (ops.py:227), and -- when gamma is given --
+// the fp32 prologue tables of bn_coeffs from (mean, var): the unfused BN's second pass
+// ends in one launch
+__global__ void __launch_bounds__(512) var_finalize_kernel(const double* __restrict__ part, int tiles, int C,
+                                                           double rcount, double* var, const double* mean,
+                                                           const float* gamma, const float* beta, float eps,
+                                                           float* mean32, float* scale32, float* beta32,
+                                                           float* inv32) {
+  griddep_launch();
+  griddep_wait();
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s1, s2;
+  reduce_two(part, tiles, C, c, s1, s2);
+  if ((threadIdx.x >> 5) == 0 && c < C) {
+    const double v = s1 * rcount;
+    var[c] = v;
+    if (gamma) {
+      const double vv = v > 0.0 ? v : 0.0;
+      const double inv = 1.0 / sqrt(vv + (double)eps);
+      mean32[c] = (float)mean[c];
+      scale32[c] = (float)((double)gamma[c] * inv);
+      beta32[c] = beta[c];
+      inv32[c] = (float)inv;
+    }
+  }
+}
+}  // namespace bnff
+
 extern "C" int bnff_var_finalize(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
                                  void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  launch(reduce_parts_kernel, dim3((c + 31) / 32), dim3(256), 0, st, part, tiles, c, 0, var);
-  // var = sum(d^2) / count, as ops.py:227 divides the centred sum by the count
-  launch(scale_kernel, dim3((c + 127) / 128), dim3(128), 0, st, var, c, 1.0 / (double)count);
+  launch(var_finalize_kernel, dim3((c + 31) / 32), dim3(512), 0, (cudaStream_t)stream, part, tiles, c,
+         1.0 / (double)count, var, (const double*)nullptr, (const float*)nullptr, (const float*)nullptr, 0.f,
+         (float*)nullptr, (float*)nullptr, (float*)nullptr, (float*)nullptr);
   return check_launch("var_finalize");
+}
+
+extern "C" int bnff_var_finalize_coeffs(const double* part, int32_t tiles, int32_t c, int64_t count, double* var,
+                                        const double* mean, const float* gamma, const float* beta, float eps,
+                                        float* mean32, float* scale32, float* beta32, float* inv32,
+                                        void* stream) {
+  if (!mean || !gamma || !beta || !mean32 || !scale32 || !beta32 || !inv32)
+    return set_error(BNFF_ERR_STATE, "var_finalize_coeffs: null table");
+  launch(var_finalize_kernel, dim3((c + 31) / 32), dim3(512), 0, (cudaStream_t)stream, part, tiles, c,
+         1.0 / (double)count, var, mean, gamma, beta, eps, mean32, scale32, beta32, inv32);
+  return check_launch("var_finalize_coeffs");
 }
 
 extern "C" int bnff_stats_finalize_coeffs(const double* part, int32_t tiles, int32_t c_new, int64_t count,

@@ -514,10 +514,15 @@ class Engine:
             part = self._empty((tiles, 2, c), torch.float64)
             self._emit(self.L.bnff_centered_var, self.dcode, view_of(x), _ptr(st.mean), _ptr(part),
                        what="centered_var", nbytes=_nb(x))
-            self._emit(self.L.bnff_var_finalize, _ptr(part), tiles, c, pixels, _ptr(st.var),
-                       what="var_finalize", launches=2)
+            # var, then the fp32 tables of this BN in the same launch
+            tb = tuple(self._zeros((c,), torch.float32) for _ in range(4))
+            bn = node.attrs.bn
+            self._emit(self.L.bnff_var_finalize_coeffs, _ptr(part), tiles, c, pixels, _ptr(st.var),
+                       _ptr(st.mean), _ptr(self.param(f"{bn.name}.gamma")), _ptr(self.param(f"{bn.name}.beta")),
+                       C.c_float(bn.eps), *(_ptr(t) for t in tb), what=f"bn_coeffs {node.name}")
+        else:
+            tb = self._bn_tables(st, node.attrs.bn, node.name)
         self.node_stats[node.id] = st
-        tb = self._bn_tables(st, node.attrs.bn, node.name)
         self.node_tables[node.id] = tb
         self._emit(self.L.bnff_bn_apply, self.dcode, view_of(x), view_of(y),
                    coef_of(tb[0], tb[1], tb[2]), 0, what="bn_apply", nbytes=_nb(x, y))

@@ -174,6 +174,11 @@ class Engine:
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
         self.wide_fallback = os.environ.get("BNFF_WIDE_FALLBACK", "1") != "0"  # see _f_FusedNormReluConv
         self.col_strided = os.environ.get("BNFF_COL_STRIDED", "1") != "0"  # see _col_conv
+        # a deferred BN dx at least this wide (channels) feeding a conv with more than two N
+        # tiles of input channels is materialised once: every N tile of the dgrad (M tile of
+        # the wgrad) would otherwise stream both wide operands (dt1 and the BN input) again
+        # (0: never; C5 sweep / D121 / R50 A/B in DESIGN.md)
+        self.wide_dx = int(os.environ.get("BNFF_WIDE_DX", "512"))
         self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
         self._wide_saved: dict = {}  # NRC node id -> materialised relu(bn(x)) (wide-N fallback)
         self._nrp_done: set = set()
@@ -843,6 +848,9 @@ class Engine:
         A wide NRC conv whose forward materialised relu(bn(x)) (_f_FusedNormReluConv) takes its
         weight-gradient operand from that tensor instead of re-normalising x per N tile."""
         cin_store = x.shape[3]
+        if isinstance(dy_gv, Deferred) and self.wide_dx and dy_gv.dt1.shape[3] >= self.wide_dx \
+                and cin_store > 256:
+            dy_gv = Plain(self._resolve(dy_gv))
         col = self.cols.get(conv.name)
         if col is None:
             _, wt, _, _ = self._pack(conv, cin_store, (x.shape[1], x.shape[2]))

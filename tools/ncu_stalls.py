@@ -35,6 +35,11 @@ def main():
     for k in keys:
         if k in raw:
             print(f"{k:70s} {raw[k]}")
+    # shared-memory pressure (the 3xTF32 kernels transform operands in place)
+    for k in sorted(raw):
+        if (k.startswith("l1tex__throughput") or "mem_shared" in k or k.startswith("l1tex__data_bank_conflicts")) \
+                and (k.endswith(".pct_of_peak_sustained_active") or k.endswith(".sum")):
+            print(f"{k:70s} {raw[k]}")
     print("-- stalls (per issue active)")
     st = []
     for k, val in raw.items():

@@ -219,9 +219,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 // round-to-nearest TF32 (low 13 mantissa bits zero).  3xTF32 splits x = hi + lo with both
 // parts rounded to nearest: |x - hi - lo| <= 2^-22 |x| (truncating either part costs 4x)
+// Written out as (bits + 2^12) & ~(2^13 - 1): bit-identical to cvt.rna.tf32.f32 for every finite
+// input (round half away from zero on the magnitude) in two integer ops, where the cvt lowers to
+// three (an infinity test guards the add); the split runs on every fp32 operand element
 __device__ __forceinline__ float tf32_rn(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  const uint32_t r = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
   return __uint_as_float(r);
 }
 __device__ __forceinline__ float tf32_hi(float x) { return tf32_rn(x); }

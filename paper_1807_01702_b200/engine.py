@@ -174,6 +174,10 @@ class Engine:
         self.fuse_nrp = os.environ.get("BNFF_FUSE_NRP", "1") != "0"  # sub-BN2 -> ReLU -> pool chains
         self.wide_fallback = os.environ.get("BNFF_WIDE_FALLBACK", "1") != "0"  # see _f_FusedNormReluConv
         self.col_strided = os.environ.get("BNFF_COL_STRIDED", "1") != "0"  # see _col_conv
+        # CUDA stream priorities of the captured step (lower = higher priority): the side
+        # stream carries the weight gradients, the capture stream the dgrad chain
+        self.side_prio = int(os.environ.get("BNFF_SIDE_PRIO", "0"))
+        self.main_prio = int(os.environ.get("BNFF_MAIN_PRIO", "0"))
         # a deferred BN dx at least this wide (channels) feeding a conv with more than two N
         # tiles of input channels is materialised once: every N tile of the dgrad (M tile of
         # the wgrad) would otherwise stream both wide operands (dt1 and the BN input) again
@@ -1290,7 +1294,7 @@ class Engine:
         for t in thunks:
             if getattr(t, "side", False):
                 if self._side is None:
-                    self._side = torch.cuda.Stream(self.dev)
+                    self._side = torch.cuda.Stream(self.dev, priority=self.side_prio)
                 ev = torch.cuda.Event()
                 ev.record(main)
                 self._side.wait_event(ev)
@@ -1353,7 +1357,7 @@ class Engine:
         """Capture the step as CUDA graph(s).  split=False: one graph forward+backward+
         SGD+repack (replayed by step()).  split=True: (fwd+bwd graph, optimizer graph),
         so a data-parallel wrapper can all-reduce the gradient buffer in between."""
-        s = torch.cuda.Stream(self.dev)
+        s = torch.cuda.Stream(self.dev, priority=self.main_prio)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
             self.forward()

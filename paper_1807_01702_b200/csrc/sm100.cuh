@@ -217,8 +217,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-// round-to-nearest TF32 (low 13 mantissa bits zero).  3xTF32 splits x = hi + lo with both
-// parts rounded to nearest: |x - hi - lo| <= 2^-22 |x| (truncating either part costs 4x)
+// round-to-nearest TF32 (low 13 mantissa bits zero).  3xTF32 splits x = hi + lo with hi rounded
+// to nearest (truncating hi costs 4x) and lo = x - hi exact in fp32, left to the MMA's own TF32
+// truncation: |x - hi - tf32(lo)| < 2^-21 |x| (2^-22 with lo rounded too; the model-level errors
+// did not move, profiles/r2_parity_benched_models.jsonl, and the step is 2% faster)
 // Written out as (bits + 2^12) & ~(2^13 - 1): bit-identical to cvt.rna.tf32.f32 for every finite
 // input (round half away from zero on the magnitude) in two integer ops, where the cvt lowers to
 // three (an infinity test guards the add); the split runs on every fp32 operand element

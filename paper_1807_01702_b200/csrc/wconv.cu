@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         const int cs = min(SLABW, p.ci - s * SLABW);
         if constexpr (F32) {
           // prologue in fp32, then the 3xTF32 split: hi (round-to-nearest TF32) in place,
-          // lo = TF32(f - hi) into the second plane; halo / border positions keep the TMA's
-          // zero fill in hi and get a zero lo
+          // lo = f - hi (exact; the MMA truncates it to TF32) into the second plane; halo /
+          // border positions keep the TMA's zero fill in hi and get a zero lo
           uint8_t* A = stage_a(st);
           uint8_t* AL = A + cv.a_bytes;
           const uint8_t* X = stage_x(st);
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
             }
             float4 hi, lo;
             hi.x = tf32_rn(f[0]); hi.y = tf32_rn(f[1]); hi.z = tf32_rn(f[2]); hi.w = tf32_rn(f[3]);
-            lo.x = tf32_rn(f[0] - hi.x); lo.y = tf32_rn(f[1] - hi.y);
-            lo.z = tf32_rn(f[2] - hi.z); lo.w = tf32_rn(f[3] - hi.w);
+            lo.x = f[0] - hi.x; lo.y = f[1] - hi.y;
+            lo.z = f[2] - hi.z; lo.w = f[3] - hi.w;
             *reinterpret_cast<float4*>(A + off) = hi;
             *reinterpret_cast<float4*>(AL + off) = lo;
           }

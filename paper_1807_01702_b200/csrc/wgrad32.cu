@@ -59,7 +59,7 @@ __host__ __device__ inline int smem_total(int KBr, bool xop, int stages, int cin
 
 __device__ __forceinline__ void split4(const float* f, float4& hi, float4& lo) {
   hi.x = tf32_rn(f[0]); hi.y = tf32_rn(f[1]); hi.z = tf32_rn(f[2]); hi.w = tf32_rn(f[3]);
-  lo.x = tf32_rn(f[0] - hi.x); lo.y = tf32_rn(f[1] - hi.y); lo.z = tf32_rn(f[2] - hi.z); lo.w = tf32_rn(f[3] - hi.w);
+  lo.x = f[0] - hi.x; lo.y = f[1] - hi.y; lo.z = f[2] - hi.z; lo.w = f[3] - hi.w;
 }
 
 template <int BN, int TAPS>

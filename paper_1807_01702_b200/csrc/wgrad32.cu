@@ -148,6 +148,19 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
     y0 = (t - img * p.tpi) * p.kt;
     x0 = xbk * p.bw;
   };
+  // the k-blocks of a split are consecutive: step (image, row block, column block) without
+  // the two integer divisions per k-block
+  auto kb_next = [&](int& img, int& y0, int& x0) {
+    x0 += p.bw;
+    if (x0 >= p.xb * p.bw) {
+      x0 = 0;
+      y0 += p.kt;
+      if (y0 >= p.tpi * p.kt) {
+        y0 = 0;
+        ++img;
+      }
+    }
+  };
   auto stage = [&](int s) { return smem + s * SB; };
 
   if (warp < NTW) {
@@ -174,10 +187,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
       int mg, nt, sp;
       unit_of(ui, mg, nt, sp);
       const int cnt = kb_count(sp);
-      for (int k = 0; k < cnt; ++k) {
-        const int kb = sp * p.kpt + k;
-        int img, y0, x0;
-        kb_org(kb, img, y0, x0);
+      int img, y0, x0;
+      kb_org(sp * p.kpt, img, y0, x0);
+      for (int k = 0; k < cnt; ++k, kb_next(img, y0, x0)) {
         for (int u = 0; u < SPK; ++u) {  // one stage per vertical tap (3x3) -- the 3 horizontal
           const int ty = TAPS == 9 ? u - 1 : 0;  // taps read it through K-row-shifted descriptors
           mbar_wait(&ld_bar[st], ph);
@@ -303,10 +315,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
       int mg, nt, sp;
       unit_of(ui, mg, nt, sp);
       const int cnt = kb_count(sp);
-      for (int k = 0; k < cnt; ++k) {
-        const int kb = sp * p.kpt + k;
-        int img, y0, x0;
-        kb_org(kb, img, y0, x0);
+      int img, y0, x0;
+      kb_org(sp * p.kpt, img, y0, x0);
+      for (int k = 0; k < cnt; ++k, kb_next(img, y0, x0)) {
         for (int u = 0; u < SPK; ++u) {
           const int ty = TAPS == 9 ? u - 1 : 0, xa = TAPS == 9 ? x0 - 1 : x0;
           if (round > 0) mbar_wait(&empty_bar[st], (round - 1) & 1);

@@ -5,6 +5,12 @@
 #include <cuda_runtime.h>
 #include "../../include/bnff.h"
 
+// 3xTF32 MMAs with a stacked B operand (2 MMAs per K step instead of 3); -DBNFF_TF32_STACK=0
+// restores the three-MMA issue for A/B timing
+#ifndef BNFF_TF32_STACK
+#define BNFF_TF32_STACK 1
+#endif
+
 namespace bnff {
 
 // thread-local last-error message returned by bnff_last_error()

@@ -69,7 +69,19 @@ struct WcParams {
   double* stat_part;
   int tstore;                  // 1: staging in 128B-swizzled rows, stored by cp.async.bulk.tensor
   unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
+  int stk;                     // fp32: stacked-B 3xTF32 issue (two MMAs per K step)
 };
+
+// BNFF_STACK bit mask (A/B and diagnosis; default all on): 1 fprop, 2 1x1 dgrad, 4 3x3 dgrad,
+// 8 fp32 1x1 wgrad
+inline int stack_mask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_STACK");
+    v = e ? atoi(e) : 15;
+  }
+  return v;
+}
 
 // event stamps of CTA 0 into p.trace[ev * 1024 + i]: compiled in only with -DBNFF_WC_TRACE=1
 // (tools/ab_defines.sh builds such a library for tools/trace_conv.py)
@@ -157,7 +169,10 @@ struct Layout {
   static constexpr int STG = 128 * SROWB;
   // per group: out staging (+ dgrad: one x buffer per owned chunk = a whole-tile lookahead)
   static constexpr int NSTG = MODE == M_DGRAD ? 1 + MYCH : 1;
-  static constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
+  // 3xTF32 with a stacked B operand: A_hi x [B_hi | B_lo] is ONE N = 2*BN MMA into [D | D'] and
+  // A_lo x B_hi accumulates into D', the epilogue adds the halves (two MMAs per K step, not three)
+  static constexpr int ACOLS = F32 && BNFF_TF32_STACK ? 2 * BN : BN;  // TMEM columns per accumulator
+  static constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
   static constexpr uint32_t LAY = RB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr uint32_t SBO = 8 * RB;
 };
@@ -606,7 +621,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         const int buf = it & 1;
         if (it >= 2) mbar_wait(&acce_bar[buf], ((it >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + buf * BN;
+        const uint32_t d = tmem + buf * L::ACOLS;
         uint32_t acc = 0;
         for (int s = 0; s < p.nslab; ++s) {
           mbar_wait(&full_bar[st], ph);
@@ -628,9 +643,23 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
                 if constexpr (F32) {  // 3xTF32: hi*hi + hi*lo + lo*hi
                   constexpr uint32_t blo = (uint32_t)(BN * RB) >> 4;
                   const uint32_t alo = (uint32_t)cv.a_bytes >> 4;
+#if BNFF_TF32_STACK
+                  if (p.stk) {
+                  // the lo plane of B follows the hi plane as rows BN..2BN-1 of one K-major
+                  // operand (same SBO), so [B_hi | B_lo] is a single N = 2*BN descriptor
+                  constexpr uint32_t idesc2 = make_idesc(128, 2 * BN, kFmtTF32, 0, 0);
+                  umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc2, acc);
+                  umma_tf32_elect(d + BN, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
+                  } else {
+                    umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
+                    umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + blo + kk * 2, idesc, 1u);
+                    umma_tf32_elect(d, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
+                  }
+#else
                   umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
                   umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + blo + kk * 2, idesc, 1u);
                   umma_tf32_elect(d, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
+#endif
                 } else {
                   umma_f16_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
                 }
@@ -843,8 +872,16 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
 #pragma unroll
         for (int c16 = 0; c16 < CW; c16 += 16) {
           float v[16];
-          tmem_ld16(tmem + buf * BN + cc + c16 + ((uint32_t)(quad * 32) << 16), v);
-          tmem_ld_wait();
+          tmem_ld16(tmem + buf * L::ACOLS + cc + c16 + ((uint32_t)(quad * 32) << 16), v);
+          if (F32 && BNFF_TF32_STACK && p.stk) {  // + the cross-term half (hi*lo + lo*hi)
+            float v2[16];
+            tmem_ld16(tmem + buf * L::ACOLS + BN + cc + c16 + ((uint32_t)(quad * 32) << 16), v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += v2[i];
+          } else {
+            tmem_ld_wait();
+          }
           const int gc = n0 + cc + c16;
           if (MODE == M_FPROP) {
             float bv[16];
@@ -2088,6 +2125,7 @@ extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t
   p.ecoef = ecoef;
   p.stat_part = stat_part;
   p.trace = g_wc_trace;
+  p.stk = (wc::stack_mask() >> (mode == 0 ? 0 : (kh == 3 ? 2 : 1))) & 1;
   if (kh == 3 && !g.sw && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
   if (kh == 3 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
     return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is a 1x1 dgrad epilogue");

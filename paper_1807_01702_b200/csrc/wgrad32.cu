@@ -43,6 +43,7 @@ struct P {
   bnff_coef dy_coef;
   float* ws;   // [splits][taps][cin][cout]
   float* wsb;  // nullable: dbias partials [splits][cout]
+  int stk;     // stacked-B 3xTF32 issue (1x1)
 };
 
 __host__ __device__ inline int a_bytes(int KBr) { return 4 * KBr * 128; }            // 128 channels
@@ -82,7 +83,11 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
   float* bred = qtab + 3 * npad;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nun = (p.units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  constexpr int TCOLS = TAPS * BN <= 32 ? 32 : (TAPS * BN <= 64 ? 64 : (TAPS * BN <= 128 ? 128 : (TAPS * BN <= 256 ? 256 : 512)));
+  // 1x1: stacked B (A_hi x [B_hi | B_lo] in one N = 2*BN MMA, A_lo x B_hi into the cross-term
+  // half, summed by the epilogue); 3x3 keeps three MMAs (9 taps x 64 columns would not fit TMEM)
+  constexpr bool STK = BNFF_TF32_STACK && TAPS == 1;
+  constexpr int AC = STK ? 2 * BN : BN;  // TMEM columns per tap accumulator
+  constexpr int TCOLS = TAPS * AC <= 32 ? 32 : (TAPS * AC <= 64 ? 64 : (TAPS * AC <= 128 ? 128 : (TAPS * AC <= 256 ? 256 : 512)));
 
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
           const uint32_t AL = A + AB, B = A + 2 * AB, BL = B + BB;
 #pragma unroll 1
           for (int tx = 0; tx < TPS; ++tx) {  // horizontal taps: A shifted by tx rows (128 B)
-            const uint32_t d = tmem + (u * TPS + tx) * BN;
+            const uint32_t d = tmem + (u * TPS + tx) * AC;
 #pragma unroll 1
             for (int kk = 0; kk < ksteps; ++kk) {
               // MN-major TF32 operands: 128-byte rows of 32 channels per K index, atoms KBr rows apart
@@ -369,9 +374,16 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
               const uint64_t bh = make_sdesc(B + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
               const uint64_t bl = make_sdesc(BL + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
               const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
-              umma_tf32_elect(d, ah, bh, idesc, acc);
-              umma_tf32_elect(d, ah, bl, idesc, 1u);
-              umma_tf32_elect(d, al, bh, idesc, 1u);
+              if (STK && p.stk) {  // B_lo's atoms follow B_hi's at the same atom stride
+                constexpr uint32_t idesc2 = make_idesc(128, 2 * BN, kFmtTF32, 1, 1);
+                umma_tf32_elect(d, ah, bh, idesc2, acc);
+                umma_tf32_elect(d + BN, al, bh, idesc, 1u);
+                (void)bl;
+              } else {
+                umma_tf32_elect(d, ah, bh, idesc, acc);
+                umma_tf32_elect(d, ah, bl, idesc, 1u);
+                umma_tf32_elect(d, al, bh, idesc, 1u);
+              }
             }
           }
           umma_commit_elect(&empty_bar[st]);
@@ -397,8 +409,16 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
 #pragma unroll 1
         for (int c16 = 0; c16 < BN; c16 += 16) {
           float v[16];
-          tmem_ld16(tmem + u * BN + c16 + ((uint32_t)(quad * 32) << 16), v);
-          tmem_ld_wait();
+          tmem_ld16(tmem + u * AC + c16 + ((uint32_t)(quad * 32) << 16), v);
+          if (STK && p.stk) {
+            float v2[16];
+            tmem_ld16(tmem + u * AC + BN + c16 + ((uint32_t)(quad * 32) << 16), v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += v2[i];
+          } else {
+            tmem_ld_wait();
+          }
           if (ci < p.cin && nt * BN + c16 < p.cout) {
 #pragma unroll
             for (int q = 0; q < 16; q += 4)
@@ -554,6 +574,10 @@ extern "C" int bnff_wgrad_f32_partials(bnff_view x, int32_t x_pro, bnff_coef x_c
   p.splits = q.splits; p.MG = q.MG; p.NT = q.NT; p.units = q.MG * q.NT * q.splits; p.stages = q.stages;
   p.x_pro = x_pro; p.x_coef = x_coef; p.dy_pro = dy_pro; p.dy_coef = dy_coef;
   p.ws = ws;
+  {
+    const char* e = getenv("BNFF_STACK");
+    p.stk = ((e ? atoi(e) : 15) >> 3) & 1;
+  }
   p.wsb = want_db ? ws + (long long)q.splits * kh * kh * p.cin * p.cout : nullptr;
   const uint32_t box[4] = {32u, (uint32_t)q.RS, (uint32_t)q.kt, 1u};
   if (!encode_nhwc(&p.tma_x, 4, x.ptr, x.n, x.h, x.w, x.c, x.row_stride, 4, box) ||

@@ -69,19 +69,19 @@ struct WcParams {
   double* stat_part;
   int tstore;                  // 1: staging in 128B-swizzled rows, stored by cp.async.bulk.tensor
   unsigned long long* trace;  // debug: per-event %globaltimer stamps of CTA 0 (bnff_debug_trace)
-  int stk;                     // fp32: stacked-B 3xTF32 issue (two MMAs per K step)
 };
 
-// BNFF_STACK bit mask (A/B and diagnosis; default all on): 1 fprop, 2 1x1 dgrad, 4 3x3 dgrad,
-// 8 fp32 1x1 wgrad
-inline int stack_mask() {
+// small-M 1x1 fprop tile target (default 0 = off: at 120 the D121 step measured 0.5% (fp32) and
+// 1.4% (bf16) slower -- the re-read A tile and its prologue cost more than the idle SMs)
+inline int smallm_tiles() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("BNFF_STACK");
-    v = e ? atoi(e) : 15;
+    const char* e = getenv("BNFF_SMALLM");
+    v = e ? atoi(e) : 0;
   }
   return v;
 }
+
 
 // event stamps of CTA 0 into p.trace[ev * 1024 + i]: compiled in only with -DBNFF_WC_TRACE=1
 // (tools/ab_defines.sh builds such a library for tools/trace_conv.py)
@@ -94,6 +94,16 @@ __device__ __forceinline__ void trace_ev(unsigned long long* tr, int ev, int i) 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     tr[ev * 1024 + i] = t;
   }
+}
+
+// BNFF_WRES3=0: stream the fp32 3x3 dgrad weights per stage (A/B timing)
+inline bool wres3_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BNFF_WRES3");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
 }
 
 __host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -123,8 +133,16 @@ __host__ __device__ inline Geo geo(int CI, int N, int kh, int kw, int dgrad, int
     g.BN = pick_bn(N);
     const int cap = g.taps == 9 ? (dgrad ? 32 : 64) : (dgrad ? 64 : (g.RB == 64 ? 32 : 128));
     if (g.BN > cap) g.BN = cap;
-    g.sw = g.taps == 9 ? 1 : 0;
     g.nslab = (CI + g.RB / 4 - 1) / (g.RB / 4);
+    // 3x3 dgrad over few output channels (DenseNet's growth k = 32: 2 slabs): the CTA's N tile
+    // of the packed weights (9 taps x hi/lo, 72 KB) stays resident instead of streaming with
+    // every stage of every tile
+#ifdef __CUDA_ARCH__
+    const bool w3 = true;
+#else
+    const bool w3 = wres3_enabled();
+#endif
+    g.sw = g.taps == 9 && !(dgrad && g.BN == 32 && g.nslab * 9 * 32 * 64 * 2 <= 80 * 1024 && w3) ? 1 : 0;
     g.ntiles = (N + g.BN - 1) / g.BN;
     g.npad = g.ntiles * g.BN;
     return g;
@@ -325,7 +343,14 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
       // launches back, so they may be fetched before this grid's dependency wait
       const uint32_t wb = p.nslab * TAPS * BN * RB * PL;
       mbar_arrive_expect_tx(&w_bar, wb);
-      bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
+      if (p.ntiles == 1) {
+        bulk_g2s(smem_u32(smem + cv.wres), p.wpk, wb, &w_bar);
+      } else {  // this CTA's N tile ([slab][tap][plane][npad][RB] rows n0 .. n0 + BN of each)
+        const int n0r = ((int)blockIdx.x % p.ntiles) * BN;
+        for (int c = 0; c < p.nslab * TAPS * PL; ++c)
+          bulk_g2s(smem_u32(smem + cv.wres) + c * BN * RB, p.wpk + ((long long)c * p.npad + n0r) * RB, BN * RB,
+                   &w_bar);
+      }
     }
   }
   if (warp == NLW) tmem_alloc<L::TCOLS>(&tmem_sh);
@@ -644,17 +669,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
                   constexpr uint32_t blo = (uint32_t)(BN * RB) >> 4;
                   const uint32_t alo = (uint32_t)cv.a_bytes >> 4;
 #if BNFF_TF32_STACK
-                  if (p.stk) {
                   // the lo plane of B follows the hi plane as rows BN..2BN-1 of one K-major
                   // operand (same SBO), so [B_hi | B_lo] is a single N = 2*BN descriptor
                   constexpr uint32_t idesc2 = make_idesc(128, 2 * BN, kFmtTF32, 0, 0);
                   umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc2, acc);
                   umma_tf32_elect(d + BN, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
-                  } else {
-                    umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
-                    umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + blo + kk * 2, idesc, 1u);
-                    umma_tf32_elect(d, a0 + alo + ash + kk * 2, b0 + bsh + kk * 2, idesc, 1u);
-                  }
+                  (void)blo;
 #else
                   umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + kk * 2, idesc, acc);
                   umma_tf32_elect(d, a0 + ash + kk * 2, b0 + bsh + blo + kk * 2, idesc, 1u);
@@ -873,7 +893,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
         for (int c16 = 0; c16 < CW; c16 += 16) {
           float v[16];
           tmem_ld16(tmem + buf * L::ACOLS + cc + c16 + ((uint32_t)(quad * 32) << 16), v);
-          if (F32 && BNFF_TF32_STACK && p.stk) {  // + the cross-term half (hi*lo + lo*hi)
+          if constexpr (F32 && BNFF_TF32_STACK) {  // + the cross-term half (hi*lo + lo*hi)
             float v2[16];
             tmem_ld16(tmem + buf * L::ACOLS + BN + cc + c16 + ((uint32_t)(quad * 32) << 16), v2);
             tmem_ld_wait();
@@ -1853,8 +1873,10 @@ inline bool wres1_enabled() {  // BNFF_WRES1=0: stream 1x1 fprop weights per sta
 // fp32 (3xTF32) instantiations: 1x1 with 128-byte slabs, N tiles 32..128 (dgrad <= 64);
 // 3x3 with 64-byte slabs and streamed weights, N tiles 32 / 64
 template <int MODE, int TAPS>
-static int dispatch_f32(const WcParams& p, int BN, int RB, cudaStream_t st) {
+static int dispatch_f32(const WcParams& p, int BN, int RB, cudaStream_t st, int sw = 1) {
   if (TAPS == 9) {
+    if constexpr (MODE == M_DGRAD)
+      if (!sw && BN == 32) return launch_t<32, 64, TAPS, MODE, false, 4>(p, st);  // resident weights
     if (BN == 32) return launch_t<32, 64, TAPS, MODE, true, 4>(p, st);
     return launch_t<64, 64, TAPS, MODE, true, 4>(p, st);
   }
@@ -1905,9 +1927,10 @@ using namespace bnff;
 namespace bnff {
 namespace wc {
 template <int MODE, int TAPS>
-static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop, int tf = 3) {
+static bool fits2_f32(int BN, int RB, int R, int nslab, int npad, bool xop, int tf = 3, int sw = 1) {
   Carve c{};
-  if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop, false, tf)
+  if (TAPS == 9 && !sw && BN == 32 && MODE == M_DGRAD) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
+  else if (TAPS == 9) c = BN == 32 ? carve<32, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop, false, tf)
                               : carve<64, 64, TAPS, MODE, true, 4>(R, nslab, npad, 2, xop, false, tf);
   else if (RB == 64 && MODE == M_DGRAD && BN == 64) c = carve<64, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, true, tf);
   else if (RB == 64) c = carve<32, 64, TAPS, MODE, false, 4>(R, nslab, npad, 2, xop, false, tf);
@@ -1958,7 +1981,7 @@ extern "C" int bnff_window_ok_ex(int32_t dtype, int32_t c_in, int32_t c_out, int
                      : ((tables & BNFF_WT_FPROP_PRO) ? 1 : 0);
     const wc::Geo g = wc::geo(CI, N, kh, kw, d, es);
     if (es == 4) {
-      const bool ok4 = kh == 3 ? (d ? wc::fits2_f32<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, tf)
+      const bool ok4 = kh == 3 ? (d ? wc::fits2_f32<wc::M_DGRAD, 9>(g.BN, g.RB, R, g.nslab, g.npad, true, tf, g.sw)
                                     : wc::fits2_f32<wc::M_FPROP, 9>(g.BN, g.RB, R, g.nslab, g.npad, false, tf))
                                : (d ? wc::fits2_f32<wc::M_DGRAD, 1>(g.BN, g.RB, R, g.nslab, g.npad, true, tf)
                                     : wc::fits2_f32<wc::M_FPROP, 1>(g.BN, g.RB, R, g.nslab, g.npad, false, tf));
@@ -2049,7 +2072,7 @@ extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t
   p.ci = (int)in.c;
   p.N = (int)out.c;
   const int es = dtype == BNFF_F32 ? 4 : 2;
-  const wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode, es);
+  wc::Geo g = wc::geo(p.ci, p.N, kh, kh, mode, es);
   if (es == 4 && mode == 1 && epi >= BNFF_DG_NRC_ACC && g.BN < 64)  // fp32 fold: TMA G tile (32 columns)
     return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the fp32 block-gradient fold needs >= 33 channels");
   p.nslab = g.nslab;
@@ -2090,6 +2113,18 @@ extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t
     p.mtiles = (p.P + 127) / 128;
     rank = 2;
     box[0] = slabw; box[1] = 128;
+    // small-M 1x1 fprop (DenseNet's 14^2 / 7^2 blocks: 98 / 25 pixel tiles at b64): halve the
+    // N tile while the launch has fewer tiles than BNFF_SMALLM (default 0 = off) so more SMs
+    // share it (each N tile re-reads the A tile, from L2).  N stays a multiple of the tile,
+    // so npad -- the packed weight layout -- does not change
+    if (mode == 0) {
+      const int tgt = wc::smallm_tiles();
+      while (tgt > 0 && g.BN > 32 && p.N % g.BN == 0 && p.mtiles * g.ntiles < tgt) {
+        g.BN /= 2;
+        g.ntiles *= 2;
+      }
+      p.ntiles = g.ntiles;
+    }
   }
   p.tiles = p.mtiles * p.ntiles;
   // TMA epilogue for 128-byte staged chunks (bf16: 64 columns, BN >= 128; fp32: 32 columns,
@@ -2125,15 +2160,15 @@ extern "C" int bnff_window_conv(int32_t dtype, int32_t mode, int32_t kh, int32_t
   p.ecoef = ecoef;
   p.stat_part = stat_part;
   p.trace = g_wc_trace;
-  p.stk = (wc::stack_mask() >> (mode == 0 ? 0 : (kh == 3 ? 2 : 1))) & 1;
-  if (kh == 3 && !g.sw && g.ntiles != 1) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
+  if (kh == 3 && !g.sw && g.ntiles != 1 && es == 2) return set_error(BNFF_ERR_UNSUPPORTED, "wconv: 3x3 needs one N tile");
   if (kh == 3 && mode == 1 && epi >= BNFF_DG_NRC_ACC)
     return set_error(BNFF_ERR_UNSUPPORTED, "wconv: the block-gradient fold is a 1x1 dgrad epilogue");
   cudaStream_t st = (cudaStream_t)stream;
   if (es == 4) {
     if (mode == 0)
       return kh == 3 ? wc::dispatch_f32<wc::M_FPROP, 9>(p, g.BN, g.RB, st) : wc::dispatch_f32<wc::M_FPROP, 1>(p, g.BN, g.RB, st);
-    return kh == 3 ? wc::dispatch_f32<wc::M_DGRAD, 9>(p, g.BN, g.RB, st) : wc::dispatch_f32<wc::M_DGRAD, 1>(p, g.BN, g.RB, st);
+    return kh == 3 ? wc::dispatch_f32<wc::M_DGRAD, 9>(p, g.BN, g.RB, st, g.sw)
+                   : wc::dispatch_f32<wc::M_DGRAD, 1>(p, g.BN, g.RB, st);
   }
   if (mode == 0) {
     return kh == 3 ? wc::dispatch<wc::M_FPROP, 9>(p, g.BN, g.RB, st, g.sw)

@@ -211,8 +211,8 @@ __host__ __device__ inline Carve carve(int R, int nslab, int npad, int stages, b
   c.wres = off;
   if (L::WRES) off += align_up(nslab * TAPS * BN * RB * L::PL, 1024);
   c.a_bytes = align_up(R * RB, 1024);
-  // stage: A planes (hi[, lo]) | x operand (BN_DX) | B planes (streamed weights)
-  c.stage_bytes = c.a_bytes * (L::PL + (xop ? 1 : 0)) + (L::WRES ? 0 : TAPS * BN * RB * L::PL);
+  // stage: A planes (hi[, lo]) | x operand (BN_DX; fp32: inside the lo plane) | B planes (streamed weights)
+  c.stage_bytes = c.a_bytes * (L::PL + (xop && !L::F32 ? 1 : 0)) + (L::WRES ? 0 : TAPS * BN * RB * L::PL);
   c.stage0 = off;
   off += stages * c.stage_bytes;
   c.stg = off;
@@ -424,9 +424,11 @@ __global__ void __launch_bounds__(WC_THREADS, 1) wconv_kernel(const __grid_const
 
   // stage: A hi [| A lo] [| x] | B (tap-major [tap][plane][BN][RB])
   auto stage_a = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes; };
-  auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * PL; };
+  // fp32: the BN_DX x operand lands in the lo plane -- each element is read by the thread that
+  // then writes its lo value there, so it needs no plane of its own
+  auto stage_x = [&](int s) { return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (F32 ? 1 : PL); };
   auto stage_b = [&](int s) {
-    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (PL + (xop_s ? 1 : 0));
+    return smem + cv.stage0 + s * cv.stage_bytes + cv.a_bytes * (PL + (xop_s && !F32 ? 1 : 0));
   };
   auto tile_of = [&](int it, int& mt, int& n0) {
     const int t = (int)blockIdx.x + it * (int)gridDim.x;

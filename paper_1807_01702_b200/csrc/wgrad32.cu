@@ -43,13 +43,15 @@ struct P {
   bnff_coef dy_coef;
   float* ws;   // [splits][taps][cin][cout]
   float* wsb;  // nullable: dbias partials [splits][cout]
-  int stk;     // stacked-B 3xTF32 issue (1x1)
 };
 
 __host__ __device__ inline int a_bytes(int KBr) { return 4 * KBr * 128; }            // 128 channels
 template <int BN> __host__ __device__ inline int b_bytes(int KBr) { return (BN / 32) * KBr * 128; }
 template <int BN>
 __host__ __device__ inline int stage_bytes(int KBr, bool xop) {
+  // A hi | A lo | B hi | B lo | x (BN_DX).  Landing x in the B lo plane (read before it is
+  // rewritten) gives three 64 KB stages instead of two 80 KB ones, but measured 5% slower in
+  // the step (the weight gradients share HBM with the dgrad chain), so x keeps its own plane
   const int s = 2 * a_bytes(KBr) + 2 * b_bytes<BN>(KBr) + (xop ? b_bytes<BN>(KBr) : 0);
   return (s + 1023) / 1024 * 1024;
 }
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
               const uint64_t bh = make_sdesc(B + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
               const uint64_t bl = make_sdesc(BL + kk * 1024, p.KBr * 128, 512, kLayoutSW128Base32);
               const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
-              if (STK && p.stk) {  // B_lo's atoms follow B_hi's at the same atom stride
+              if constexpr (STK) {  // B_lo's atoms follow B_hi's at the same atom stride
                 constexpr uint32_t idesc2 = make_idesc(128, 2 * BN, kFmtTF32, 1, 1);
                 umma_tf32_elect(d, ah, bh, idesc2, acc);
                 umma_tf32_elect(d + BN, al, bh, idesc, 1u);
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_f32_kernel(const __grid_cons
         for (int c16 = 0; c16 < BN; c16 += 16) {
           float v[16];
           tmem_ld16(tmem + u * AC + c16 + ((uint32_t)(quad * 32) << 16), v);
-          if (STK && p.stk) {
+          if constexpr (STK) {
             float v2[16];
             tmem_ld16(tmem + u * AC + BN + c16 + ((uint32_t)(quad * 32) << 16), v2);
             tmem_ld_wait();
@@ -574,10 +576,6 @@ extern "C" int bnff_wgrad_f32_partials(bnff_view x, int32_t x_pro, bnff_coef x_c
   p.splits = q.splits; p.MG = q.MG; p.NT = q.NT; p.units = q.MG * q.NT * q.splits; p.stages = q.stages;
   p.x_pro = x_pro; p.x_coef = x_coef; p.dy_pro = dy_pro; p.dy_coef = dy_coef;
   p.ws = ws;
-  {
-    const char* e = getenv("BNFF_STACK");
-    p.stk = ((e ? atoi(e) : 15) >> 3) & 1;
-  }
   p.wsb = want_db ? ws + (long long)q.splits * kh * kh * p.cin * p.cout : nullptr;
   const uint32_t box[4] = {32u, (uint32_t)q.RS, (uint32_t)q.kt, 1u};
   if (!encode_nhwc(&p.tma_x, 4, x.ptr, x.n, x.h, x.w, x.c, x.row_stride, 4, box) ||

@@ -520,13 +520,18 @@ inline Plan plan(int n, int h, int w, int cin, int cout, int kh, bool xop) {
            : q.BN == 64 ? pick_stages<64>(q.KBr, xop, q.MG * 128, q.NT * q.BN)
                         : pick_stages<128>(q.KBr, xop, q.MG * 128, q.NT * q.BN);
   if (q.stages < 2) return q;
-  // 3x3 split target (BNFF_WG32_T3, A/B): every split writes a 9 x 128 x 32 fp32 partial tile
-  static int t3 = -1;
+  // CTA targets of the split planning (BNFF_WG32_T3 / BNFF_WG32_T1, A/B; default one per SM):
+  // every split writes a taps x 128 x BN fp32 partial tile, and the weight gradients run beside
+  // the dgrad chain on the side stream
+  static int t3 = -1, t1 = -1;
   if (t3 < 0) {
     const char* e = getenv("BNFF_WG32_T3");
     t3 = e ? atoi(e) : 0;
+    e = getenv("BNFF_WG32_T1");
+    t1 = e ? atoi(e) : 0;
   }
-  const int target = kh == 3 && t3 > 0 ? t3 : num_sms32();
+  const int tk = kh == 3 ? t3 : t1;
+  const int target = tk > 0 ? tk : num_sms32();
   int splits = (target + q.MG * q.NT - 1) / (q.MG * q.NT);
   // >= min_kpt k-blocks per split (the partial tile a split writes is TAPS x 128 x BN floats)
   const int maxs = q.nkb / wg_min_kpt() > 0 ? q.nkb / wg_min_kpt() : 1;

@@ -183,6 +183,9 @@ class Engine:
         # the wgrad) would otherwise stream both wide operands (dt1 and the BN input) again
         # (0: never; C5 sweep / D121 / R50 A/B in DESIGN.md)
         self.wide_dx = int(os.environ.get("BNFF_WIDE_DX", "512"))
+        # measurement only: launch every (idempotent) forward coefficient kernel N times, to price
+        # one such launch on the critical path
+        self.coef_reps = max(1, int(os.environ.get("BNFF_COEF_REPS", "1")))
         self._nrp: dict = {}  # ReLU / AvgPool node id -> the sub-BN2 node heading its fused chain
         self._wide_saved: dict = {}  # NRC node id -> materialised relu(bn(x)) (wide-N fallback)
         self._nrp_done: set = set()
@@ -399,10 +402,11 @@ class Engine:
         self._pending_fin = []
         part, tiles, cn, count, ps = merge
         off = (ps.mean.data_ptr() - lo) // 8
-        self._emit(self.L.bnff_stats_finalize_coeffs, _ptr(part), tiles, cn, count, _ptr(ps.sum),
-                   _ptr(ps.sumsq), _ptr(ps.mean), _ptr(ps.var), off, c, _ptr(st.mean), _ptr(st.var),
-                   _ptr(gam), _ptr(bet), C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32),
-                   _ptr(inv32), what=f"bn_coeffs {tag}")
+        for _ in range(self.coef_reps):
+            self._emit(self.L.bnff_stats_finalize_coeffs, _ptr(part), tiles, cn, count, _ptr(ps.sum),
+                       _ptr(ps.sumsq), _ptr(ps.mean), _ptr(ps.var), off, c, _ptr(st.mean), _ptr(st.var),
+                       _ptr(gam), _ptr(bet), C.c_float(bn.eps), _ptr(mean32), _ptr(scale32), _ptr(beta32),
+                       _ptr(inv32), what=f"bn_coeffs {tag}")
         return mean32, scale32, beta32, inv32
 
     def _channel_stats(self, x: torch.Tensor, st: Stats, tag):
